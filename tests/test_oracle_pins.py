@@ -1,0 +1,323 @@
+"""Pins for the CPU oracle (runs on CPU, -m "not gpu").
+
+Each test ties an oracle function to something other than itself: a value
+printed in SPEC.md/PAPER.md (tests/golden/spec_examples.json, each with its
+citation), a closed form, an invariant of the mathematics, an independent
+library routine, or brute force on tiny inputs.  The mistakes these catch:
+a dropped norm (scale invariance, golden values), a transposed operand
+(rectangular shapes, pairwise loop), a wrong prefix length (truncation test),
+a wrong blend weight (0.09375), a wrong tie rule (duplicates), an off-by-one
+in the greedy stop (brute force), a wrong victim rule (brute-force argmax).
+"""
+import itertools
+import json
+import math
+import os
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import fmoe_oracle as O
+
+GOLD = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "spec_examples.json")))
+rng = np.random.default_rng(2502053700)
+
+
+# ---------------------------------------------------------------- quantize
+def test_quantize_bf16_matches_torch_rne():
+    x = rng.standard_normal(20000).astype(np.float32) * np.float32(10.0) ** rng.integers(-30, 30, 20000).astype(np.float32)
+    x = np.concatenate([x, np.array([0.0, -0.0, 1.0, 1.00390625, 1.005859375, 3.0e38], np.float32)])
+    ref = torch.from_numpy(x).to(torch.bfloat16).to(torch.float64).numpy()
+    got = O.quantize(x, "bf16")
+    assert np.array_equal(got, ref)
+    assert np.array_equal(O.quantize(x, "f32"), x.astype(np.float64))
+
+
+def test_quantize_bf16_ties_to_even():
+    # 1 + 2^-8 is exactly half-way between bf16 1.0 and 1+2^-7: RNE -> 1.0 (even)
+    assert O.quantize(np.float32(1 + 2 ** -8), "bf16")[()] == 1.0
+    # 1 + 3*2^-8 half-way between 1+2^-7 (odd) and 1+2^-6 (even) -> 1+2^-6
+    assert O.quantize(np.float32(1 + 3 * 2 ** -8), "bf16")[()] == 1 + 2 ** -6
+
+
+# ---------------------------------------------------------------- Eq. 1
+@pytest.mark.parametrize("ex", GOLD["semantic_cosine"], ids=lambda e: e["cite"])
+def test_semantic_golden(ex):
+    got = O.semantic_scores(ex["q"], ex["s"])
+    assert np.allclose(got, ex["expect"], atol=ex.get("tol", 1e-12), rtol=0)
+
+
+def test_semantic_matches_pairwise_python_loop_and_scipy():
+    from scipy.spatial.distance import cosine as scipy_cos_dist
+    Q = rng.standard_normal((3, 17))
+    S = rng.standard_normal((5, 17))
+    got = O.semantic_scores(Q, S)
+    assert got.shape == (3, 5)
+    for x in range(3):
+        for y in range(5):
+            num = sum(Q[x, i] * S[y, i] for i in range(17))
+            den = math.sqrt(sum(v * v for v in Q[x])) * math.sqrt(sum(v * v for v in S[y]))
+            assert abs(got[x, y] - num / den) < 1e-14
+            assert abs(got[x, y] - (1.0 - scipy_cos_dist(Q[x], S[y]))) < 1e-12
+
+
+def test_cosine_invariants():
+    a, b = rng.standard_normal(64), rng.standard_normal(64)
+    assert abs(O.cosine(a, a) - 1.0) < 1e-15
+    assert abs(O.cosine(a, -a) + 1.0) < 1e-15
+    assert abs(O.cosine(a, b) - O.cosine(b, a)) < 1e-15
+    for alpha in (1e-3, 0.5, 7.0, 1e6):  # positive scale invariance
+        assert abs(O.cosine(alpha * a, b) - O.cosine(a, b)) < 1e-14
+    assert -1.0 <= O.cosine(a, b) <= 1.0
+    # Reading R3: zero-norm query -> NaN, zero-norm stored row -> 0
+    assert math.isnan(O.cosine(np.zeros(4), np.ones(4)))
+    assert O.cosine(np.ones(4), np.zeros(4)) == 0.0
+    m = O.semantic_scores(np.array([[0.0, 0.0], [1.0, 0.0]]), np.array([[1.0, 1.0], [0.0, 0.0]]))
+    assert np.isnan(m[0]).all() and m[1, 1] == 0.0
+
+
+# ---------------------------------------------------------------- Eq. 2
+@pytest.mark.parametrize("ex", GOLD["trajectory_cosine"], ids=lambda e: e["cite"])
+def test_trajectory_golden(ex):
+    got = O.trajectory_scores(ex["q"], ex["m"], ex["ell"])
+    assert np.allclose(got, ex["expect"], atol=1e-12, rtol=0)
+
+
+def test_trajectory_naive_loop_random_2layer_prefix_store_of_3():
+    # random 2-layer prefix vs a store of 3 -> direct per-pair cosine
+    L, E = 4, 5
+    q = rng.dirichlet(np.ones(E), size=(2, L))
+    m = rng.dirichlet(np.ones(E), size=(3, L))
+    got = O.trajectory_scores(q, m, 2)
+    for x in range(2):
+        for y in range(3):
+            a = [q[x, l, j] for l in range(2) for j in range(E)]
+            b = [m[y, l, j] for l in range(2) for j in range(E)]
+            num = sum(u * v for u, v in zip(a, b))
+            den = math.sqrt(sum(u * u for u in a)) * math.sqrt(sum(v * v for v in b))
+            assert abs(got[x, y] - num / den) < 1e-14
+
+
+def test_trajectory_truncates_stored_maps_and_ignores_query_tail():
+    L, E, ell = 6, 4, 3
+    q = rng.dirichlet(np.ones(E), size=(2, L))
+    m = rng.dirichlet(np.ones(E), size=(5, L))
+    base = O.trajectory_scores(q, m, ell)
+    m2, q2 = m.copy(), q.copy()
+    m2[:, ell:, :] = rng.dirichlet(np.ones(E), size=(5, L - ell))
+    q2[:, ell:, :] = 0.0
+    assert np.array_equal(base, O.trajectory_scores(q2, m2, ell))
+    # changing an observed layer does change it
+    m2[:, ell - 1, :] = rng.dirichlet(np.ones(E), size=5)
+    assert not np.allclose(base, O.trajectory_scores(q, m2, ell))
+    # probabilities >= 0  =>  score in [0, 1]
+    assert (base >= 0).all() and (base <= 1 + 1e-15).all()
+    # ell = L is the full-map cosine
+    full = O.semantic_scores(q.reshape(2, -1), m.reshape(5, -1))
+    assert np.allclose(O.trajectory_scores(q, m, L), full, atol=1e-15)
+    with pytest.raises(ValueError):
+        O.trajectory_scores(q, m, 0)
+
+
+# ---------------------------------------------------------------- RDY
+@pytest.mark.parametrize("ex", GOLD["rdy"], ids=lambda e: e["cite"])
+def test_rdy_golden(ex):
+    d, L = ex["d"], ex["L"]
+    got = O.blend_scores(np.array([[ex["cos_sem"]]]), np.array([[ex["cos_map"]]]), d / L)
+    assert abs(got[0, 0] - ex["expect"]) < 1e-15
+
+
+def test_rdy_constructed_vectors():
+    # build pairs with cos_sem = 1 and cos_map = 0 exactly, L=32, d=3 -> 0.09375
+    L, E, D = 32, 2, 3
+    e = np.array([[1.0, 2.0, 2.0]])
+    qm = np.zeros((1, L, E)); qm[..., 0] = 1.0
+    sm = np.zeros((1, L, E)); sm[..., 1] = 1.0
+    assert abs(O.rdy_scores(2 * e, qm, e, sm, 3)[0, 0] - 0.09375) < 1e-15
+    assert abs(O.rdy_scores(e, sm, e, sm, 3)[0, 0] - 1.0) < 1e-15
+
+
+# ---------------------------------------------------------------- top-k
+def test_topk_brute_force_and_ties():
+    for _ in range(50):
+        B, C, k = 3, int(rng.integers(1, 40)), int(rng.integers(1, 12))
+        s = np.round(rng.standard_normal((B, C)), 1)  # many exact ties
+        gs, gi = O.topk(s, k)
+        for x in range(B):
+            pairs = sorted([(s[x, j], j) for j in range(C)], key=lambda t: (-t[0], t[1]))
+            for r in range(k):
+                if r < C:
+                    assert gs[x, r] == pairs[r][0] and gi[x, r] == pairs[r][1]
+                else:
+                    assert gs[x, r] == -np.inf and gi[x, r] == -1
+    s = np.array([[0.5, np.nan, 0.1]])
+    gs, gi = O.topk(s, 2)
+    assert np.isnan(gs).all() and (gi == -1).all()
+
+
+def test_topk_scale_invariance_of_argmax():
+    Q = rng.standard_normal((4, 9)); S = rng.standard_normal((30, 9))
+    _, i1 = O.topk(O.semantic_scores(Q, S), 3)
+    _, i2 = O.topk(O.semantic_scores(Q * np.array([[0.1], [3.0], [50.0], [1e-4]]), S), 3)
+    assert np.array_equal(i1, i2)
+
+
+def test_merge_of_shards_equals_unsharded():
+    # merging per-shard top-k by (score desc, global id asc) = global top-k
+    for G in (2, 3, 4, 8):
+        s = np.round(rng.standard_normal((5, 103)), 1)
+        k = 7
+        ref_s, ref_i = O.topk(s, k)
+        bounds = np.linspace(0, 103, G + 1).astype(int)
+        cs, ci = [], []
+        for g in range(G):
+            lo, hi = bounds[g], bounds[g + 1]
+            ls, li = O.topk(s[:, lo:hi], k, ids=np.arange(lo, hi))
+            cs.append(ls); ci.append(li)
+        ms, mi = O.merge_topk(cs, ci, k)
+        assert np.array_equal(mi, ref_i) and np.array_equal(ms, ref_s)
+
+
+# ---------------------------------------------------------------- delta
+@pytest.mark.parametrize("ex", GOLD["delta"], ids=lambda e: e["cite"])
+def test_delta_golden(ex):
+    assert abs(O.selection_threshold(ex["score"]) - ex["expect"]) < 1e-15
+
+
+def test_delta_monotone_and_clamped():
+    xs = np.linspace(-1.5, 1.5, 301)
+    ds = [O.selection_threshold(x) for x in xs]
+    assert all(a >= b for a, b in zip(ds, ds[1:]))
+    assert all(0.0 <= v <= 1.0 for v in ds)
+    assert O.selection_threshold(float("nan")) == 1.0
+
+
+# ---------------------------------------------------------------- Eq. 4-6
+@pytest.mark.parametrize("ex", GOLD["select"], ids=lambda e: e["cite"])
+def test_select_golden(ex):
+    picked, mask = O.select_prefetch_set(ex["p"], ex["delta"], ex["K"])
+    assert picked == ex["expect"]
+    assert mask == sum(1 << j for j in ex["expect"])
+
+
+def test_select_greedy_is_minimum_cardinality_bruteforce():
+    # SPEC A2: greedy cardinality = exhaustive minimum over 2^E subsets
+    for trial in range(600):
+        E = int(rng.integers(2, 9))
+        K = int(rng.integers(1, E + 1))
+        p = rng.dirichlet(np.full(E, 0.5))
+        if trial % 5 == 0:
+            p = np.round(p, 1)  # ties
+        delta = float(rng.choice([0.0, 1.0, rng.random()]))
+        picked, _ = O.select_prefetch_set(p, delta, K)
+        size, feasible = O.brute_force_min_prefetch_set(p, delta, K)
+        assert len(picked) == size
+        assert tuple(sorted(picked)) in feasible
+        assert len(picked) >= K
+        # the greedy set is the size-`size` prefix of (p desc, index asc)
+        order = sorted(range(E), key=lambda j: (-p[j], j))
+        assert picked == order[:size]
+
+
+def test_select_special_cases():
+    p = np.array([0.3, 0.3, 0.2, 0.1, 0.1])
+    assert O.select_prefetch_set(p, 0.0, 2)[0] == [0, 1]          # delta 0 -> exactly top-K
+    short = np.array([0.4, 0.3, 0.2])                              # mass 0.9 < 1
+    assert O.select_prefetch_set(short, 1.0, 1)[0] == [0, 1, 2]    # never reached -> all E
+    # monotone in delta for fixed guidance
+    q = rng.dirichlet(np.ones(16))
+    sizes = [len(O.select_prefetch_set(q, dl, 2)[0]) for dl in np.linspace(0, 1, 41)]
+    assert all(a <= b for a, b in zip(sizes, sizes[1:]))
+
+
+def test_select_experts_dynamic_delta_uses_matched_score():
+    m = np.zeros((2, 3, 4)); m[:, :, :] = [0.4, 0.3, 0.2, 0.1]
+    masks, counts = O.select_experts(m, [1, -1], [0.4, 0.9], -1.0, [0, 2], 2)
+    # delta = 0.6 -> {0, 1}; unmatched query -> empty
+    assert masks == [[0b11, 0b11], [0, 0]] and counts == [[2, 2], [0, 0]]
+    masks, _ = O.select_experts(m, [0], [1.0], 0.9, [1], 2)   # fixed delta 0.9 -> 4 experts
+    assert masks == [[0b1111]]
+
+
+# ---------------------------------------------------------------- store / dedup
+def _ctx(n, L=4, E=3, D=5):
+    return rng.standard_normal((n, D)), rng.dirichlet(np.ones(E), size=(n, L))
+
+
+def test_store_append_below_capacity():
+    st = O.Store(8, 4, 3, 5)
+    e, m = _ctx(5)
+    slots, rep = st.insert(e, m)
+    assert slots == [0, 1, 2, 3, 4] and rep == [-1] * 5 and st.n == 5
+    assert np.array_equal(st.emb[:5], e)
+
+
+def test_store_duplicate_is_replaced():
+    st = O.Store(4, 4, 3, 5)
+    e, m = _ctx(4)
+    st.insert(e, m)
+    slots, rep = st.insert(e[2:3] * 3.0, m[2:3])   # RDY = 1 with slot 2
+    assert slots == [2] and rep == [2] and st.n == 4
+
+
+def test_store_batch_of_2_into_full_store_of_4_bruteforce():
+    # replacements match exhaustive argmax over RDY
+    for _ in range(30):
+        L, E, D, d = 4, 3, 5, 1
+        st = O.Store(4, L, E, D, d)
+        e, m = _ctx(4, L, E, D)
+        st.insert(e, m)
+        ne, nm = _ctx(2, L, E, D)
+        # brute force, the definition written out with python loops
+        def rdy(x, y):
+            sem = O.cosine(ne[x], e[y])
+            tr = O.cosine(nm[x].ravel(), m[y].ravel())
+            return d / L * sem + (L - d) / L * tr
+        first = max(range(4), key=lambda y: (rdy(0, y), -y))
+        second = max([y for y in range(4) if y != first], key=lambda y: (rdy(1, y), -y))
+        slots, rep = st.insert(ne, nm)
+        assert slots == [first, second] and rep == [first, second]
+        assert st.n == 4
+
+
+def test_store_mixed_batch_and_size_bound():
+    st = O.Store(6, 4, 3, 5)
+    e, m = _ctx(4)
+    st.insert(e, m)
+    e2, m2 = _ctx(4)
+    slots, rep = st.insert(e2, m2)
+    assert slots[:2] == [4, 5] and rep[:2] == [-1, -1]
+    assert all(0 <= s < 4 for s in slots[2:]) and len(set(slots)) == 4   # never evicts own rows
+    for _ in range(200):                                                 # |store| <= C
+        st.insert(*_ctx(int(rng.integers(1, 5))))
+        assert st.n <= 6
+
+
+def test_store_sequential_single_inserts_equal_batch_when_victims_distinct():
+    L, E, D = 4, 3, 5
+    a = O.Store(5, L, E, D); b = O.Store(5, L, E, D)
+    e, m = _ctx(5, L, E, D); a.insert(e, m); b.insert(e, m)
+    ne, nm = _ctx(3, L, E, D)
+    sb, _ = b.insert(ne, nm)
+    sa = [a.insert(ne[i:i + 1], nm[i:i + 1])[0][0] for i in range(3)]
+    if len(set(sa)) == 3:
+        assert sa == sb
+
+
+def test_store_search_blend_matches_definition():
+    st = O.Store(10, 4, 3, 5)
+    e, m = _ctx(10)
+    st.insert(e, m)
+    qe, qm = _ctx(2)
+    s, i = st.search(qe, qm, 2, 0.25, 3)
+    ref = 0.25 * O.semantic_scores(qe, e) + 0.75 * O.trajectory_scores(qm, m, 2)
+    rs, ri = O.topk(ref, 3)
+    assert np.array_equal(i, ri) and np.allclose(s, rs, atol=1e-15)
+
+
+@pytest.mark.parametrize("ex", GOLD["store_bytes"], ids=lambda e: e["cite"])
+def test_paper_store_memory_closed_form(ex):
+    # "< 200 MB" at 32K maps; the fp32 map payload alone gives 188.7 MB
+    mb = ex["n_maps"] * ex["L"] * ex["E"] * ex["bytes_per_elem"] / 1e6
+    assert abs(mb - ex["expect_mb"]) < 1e-5 and mb < 200
