@@ -1,0 +1,181 @@
+/*
+ * fmoe.h -- C ABI of the B200-native fMoE expert-map search (arXiv 2502.05370).
+ *
+ * Citations: P:n = PAPER.md line n (paper section / equation named), S:n =
+ * SPEC.md line n.  Readings R1..R12 of ambiguous passages are listed in
+ * DESIGN.md §"Readings".
+ *
+ * The store holds N historical iteration contexts ("Expert Map
+ * Store"): a semantic embedding sem_y in R^D and an expert map
+ * map_y = {P_1..P_L}, P_l in R^E the gate probability distribution of layer l
+ * (P:410-421).  Searches score a batch of B live queries against every stored
+ * context and return the top-k contexts per query; selection turns
+ * a matched map into per-layer prefetch sets; insertion appends or
+ * replaces the most redundant context.
+ *
+ * ---------------------------------------------------------------------------
+ * Conventions (apply to every call)
+ *  - Layouts are C row-major, fp32 inputs, int64 ids.  Layer indices are
+ *    0-based (the paper is 1-based): ABI layer t = paper layer t+1.
+ *  - Pointers: every array argument may be DEVICE memory on the store's device
+ *    or HOST memory (pageable or pinned).  Host arrays are staged through
+ *    stream-ordered device buffers; if any OUTPUT array is host memory the call
+ *    synchronises `stream` before returning, otherwise the call is
+ *    asynchronous and stream-ordered.  The caller owns all arrays; the store
+ *    owns its device tiles.  Device arrays on another device -> INVALID_ARG.
+ *  - `stream` is a cudaStream_t (NULL = the legacy default stream).
+ *  - Host-side argument checks return an error synchronously with no device
+ *    work enqueued.  Data-dependent conditions are reported in-band per row
+ *    (e.g. a zero-norm query gets id -1 and score NaN, R3).
+ *  - Ids are slot indices: a context keeps its id until it is replaced, and the
+ *    replacing context takes the same id.  With a sharded store (id_offset !=
+ *    0) every id in/out of this ABI is the GLOBAL id id_offset + slot.
+ *  - Ordering of results: score descending, ties -> lowest id (R5).
+ *    If k > |store| the tail is id -1, score -inf.
+ *  - Concurrency: single writer, multiple readers.  Searches on
+ *    different streams may overlap; an insert must be stream-ordered after the
+ *    searches that should not observe it.
+ * ---------------------------------------------------------------------------
+ */
+#ifndef FMOE_H_
+#define FMOE_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define FMOE_ABI_VERSION 1
+#define FMOE_MAX_K 64        /* largest k of one search call                    */
+#define FMOE_MAX_E 64        /* experts per layer: a prefetch set is a uint64 mask */
+
+typedef struct fmoe_store fmoe_store;   /* opaque; owns all device tiles */
+
+typedef enum {
+  FMOE_OK = 0,
+  FMOE_ERR_INVALID_ARG = 1,   /* null pointer, k/ell/layer range out of bounds, wrong device */
+  FMOE_ERR_SHAPE = 2,         /* configuration shape unsupported (E > 64, D < 1, ...)      */
+  FMOE_ERR_OOM = 3,           /* device allocation failed                                  */
+  FMOE_ERR_CUDA = 4,          /* a CUDA runtime call or launch failed (see fmoe_last_error) */
+  FMOE_ERR_UNSUPPORTED = 5    /* legal request this build does not implement               */
+} fmoe_status;
+
+typedef enum { FMOE_F32 = 0, FMOE_BF16 = 1 } fmoe_dtype;
+
+typedef struct {
+  int32_t L;          /* MoE layers (paper L)                                         */
+  int32_t E;          /* experts per layer (paper J), 1..64                             */
+  int32_t K;          /* experts activated per layer (Constraint 6), 1..E       */
+  int32_t D;          /* semantic embedding dimension (paper h), >= 1           */
+  int32_t d;          /* prefetch distance (d = 3 at P:672), 1 <= d < L         */
+  int32_t dtype;      /* fmoe_dtype of the stored embedding and map tiles              */
+  int64_t capacity;   /* slots held by THIS store object (paper C)  <= 2^32-1  */
+  int64_t id_offset;  /* global id of slot 0 (sharded store); 0 if unsharded */
+} fmoe_store_config;
+
+/* ---- lifetime ---------------------------------------------------------- */
+
+/* Create an empty store on CUDA device `device`.  Allocates the tiles of
+ * capacity contexts: bytes = capacity*(D'*s + 4 + L*E'*s + 4*L) with
+ * s = 2 (bf16) or 4 (fp32), D' and E' rounded up to 16-byte rows (DESIGN.md
+ * "HBM layout").  Errors: SHAPE for an illegal config, OOM, CUDA. */
+fmoe_status fmoe_store_create(const fmoe_store_config* cfg, int device, fmoe_store** out);
+
+/* Free the store and its tiles (device-synchronous).  NULL is a no-op. */
+void fmoe_store_destroy(fmoe_store* store);
+
+/* Number of occupied slots |S| (host counter; inserts update it when enqueued). */
+fmoe_status fmoe_store_size(const fmoe_store* store, int64_t* out_n);
+
+/* Copy the configuration the store was created with. */
+fmoe_status fmoe_store_get_config(const fmoe_store* store, fmoe_store_config* out_cfg);
+
+/* ---- insertion with RDY de-duplication ------------ */
+
+/* Insert B new contexts: emb [B][D] fp32, maps [B][L][E] fp32 (gate rows).
+ * The store quantises each row to its dtype (round-to-nearest-even) and keeps
+ * 1/||row|| of the quantised embedding and the prefix norms of the map.
+ * Rule (Reading R8): while |S| < capacity the context is appended to the next
+ * slot; afterwards each remaining context x (batch order) replaces the old
+ * context y* = argmax_y RDY_{x,y} (RDY = d/L*score^sem + (L-d)/L*score^map over
+ * full maps) among the contexts that existed before this call and
+ * are not yet claimed by an earlier row of the batch (ties -> lowest id).
+ * Outputs: out_slot[B] = the slot (id) written, or -1 if no unclaimed slot was
+ * left; out_replaced[B] = the id that was evicted (== out_slot) or -1 if the
+ * row was appended.  Either output may be NULL.
+ * Limits: at most FMOE_MAX_K rows of one call may need replacement
+ * (INVALID_ARG otherwise; split the batch).  A zero-norm embedding is stored
+ * and scores 0 against every query (Reading R3). */
+fmoe_status fmoe_store_insert(fmoe_store* store, int64_t B, const float* emb, const float* maps,
+                              int64_t* out_slot, int64_t* out_replaced, void* stream);
+
+/* Read back `count` slots from `slot_begin` as the fp32 values the store holds
+ * (the quantised rows): out_emb [count][D], out_maps [count][L][E]; either
+ * may be NULL.  (SPEC snapshot.) */
+fmoe_status fmoe_store_read(const fmoe_store* store, int64_t slot_begin, int64_t count,
+                            float* out_emb, float* out_maps, void* stream);
+
+/* ---- search ------------------------------------------------- */
+
+/* Semantic search, Eq. 1: score_{x,y} = cos(q_emb_x, sem_y).
+ * q_emb [B][D] fp32.  Outputs out_score [B][k] fp32, out_id [B][k] int64.
+ * 1 <= k <= FMOE_MAX_K.  A zero-norm query row gets (NaN, -1). */
+fmoe_status fmoe_search_semantic(const fmoe_store* store, int64_t B, const float* q_emb, int32_t k,
+                                 float* out_score, int64_t* out_id, void* stream);
+
+/* Trajectory search, Eq. 2: score_{x,y} = cos(flat(q_x[0:ell]),
+ * flat(map_y[0:ell])) over the ell*E entries of the observed prefix (Reading
+ * R1: ell = number of observed layers, 1 <= ell <= L; stored maps truncated).
+ * q_prefix [B][ell][E] fp32 (row stride ell*E).  Outputs as semantic. */
+fmoe_status fmoe_search_trajectory(const fmoe_store* store, int64_t B, const float* q_prefix,
+                                   int32_t ell, int32_t k, float* out_score, int64_t* out_id,
+                                   void* stream);
+
+/* Blended search (Reading R4): score = w*score^sem + (1-w)*score^traj(ell),
+ * the RDY weighting of P:544-551 with a caller weight; w_sem < 0 selects the
+ * paper's d/L.  q_emb [B][D], q_prefix [B][ell][E]; 0 <= w_sem <= 1 or < 0. */
+fmoe_status fmoe_search_blend(const fmoe_store* store, int64_t B, const float* q_emb,
+                              const float* q_prefix, int32_t ell, float w_sem, int32_t k,
+                              float* out_score, int64_t* out_id, void* stream);
+
+/* ---- similarity-aware expert selection ----------------------- */
+
+/* For each query x with matched context map_id[x] (-1 = none) and its score:
+ * delta_x = Clip(1 - score[x], 0, 1) (score clamped to [-1,1], NaN
+ * -> 1) when delta < 0, else the fixed threshold delta in [0,1].  For each
+ * layer t in [layer_begin, layer_end): sort P_{map_id,t} by (p desc, index asc),
+ * accumulate in float64 in that order and stop at the first count with
+ * cum >= delta and count >= K; all E if never reached (Eq. 4-6, Reading R7).
+ * Outputs out_mask [B][T] uint64 (bit j = expert j prefetched), out_count
+ * [B][T] int32, T = layer_end - layer_begin.  A map_id outside this store
+ * (-1, or another shard's id) gives mask 0, count 0.  score may be NULL when
+ * delta >= 0. */
+fmoe_status fmoe_select_experts(const fmoe_store* store, int64_t B, const int64_t* map_id,
+                                const float* score, float delta, int32_t layer_begin,
+                                int32_t layer_end, uint64_t* out_mask, int32_t* out_count,
+                                void* stream);
+
+/* ---- sharded merge ---------------------------------------- */
+
+/* Merge n_lists candidate lists per query into the global top-k: scores
+ * [n_lists][B][k_in] fp32, ids [n_lists][B][k_in] int64 (the layout of an
+ * all-gather of per-rank search outputs), ordered (score desc, id asc); a NaN
+ * anywhere in a query's lists marks the query invalid -> (NaN, -1).  Entries
+ * with id -1 are ignored.  1 <= k <= FMOE_MAX_K, 1 <= k_in <= FMOE_MAX_K. */
+fmoe_status fmoe_topk_merge(int64_t B, int32_t n_lists, int32_t k_in, const float* scores,
+                            const int64_t* ids, int32_t k, float* out_score, int64_t* out_id,
+                            int device, void* stream);
+
+/* ---- diagnostics --------------------------------------------------------- */
+const char* fmoe_status_string(fmoe_status s);
+/* Message of the last error on the calling thread ("" if none). */
+const char* fmoe_last_error(void);
+/* Number of kernels this library has launched in this process (a counter the
+ * bench reports as gpu_launches). */
+int64_t fmoe_kernel_launch_count(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* FMOE_H_ */

@@ -1,0 +1,221 @@
+"""paper_2502_05370_b200 -- B200-native fMoE expert-map search (arXiv 2502.05370).
+
+Thin ctypes binding over the C ABI in ``include/fmoe.h`` (libfmoe_b200.so,
+sm_100a).  The functions below have the ABI's names and only marshal
+arguments: every step of the path runs in the library's CUDA kernels.  Arrays
+are torch tensors (CUDA tensors on the store's device, or CPU tensors -- the
+library then stages them and synchronises).  PyTorch is used only for memory,
+streams and process groups.  There is no CPU fallback: importing this package
+without the built library raises.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+import torch
+
+_PKG = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_PKG, "libfmoe_b200.so")
+
+FMOE_F32, FMOE_BF16 = 0, 1
+FMOE_MAX_K = 64
+FMOE_MAX_E = 64
+_STATUS = {0: "ok", 1: "invalid argument", 2: "unsupported shape", 3: "out of device memory",
+           4: "CUDA error", 5: "unsupported"}
+
+
+class FmoeError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        super().__init__(f"fmoe status {status} ({_STATUS.get(status, '?')}): {msg}")
+        self.status = status
+
+
+class fmoe_store_config(ctypes.Structure):
+    _fields_ = [("L", ctypes.c_int32), ("E", ctypes.c_int32), ("K", ctypes.c_int32), ("D", ctypes.c_int32),
+                ("d", ctypes.c_int32), ("dtype", ctypes.c_int32), ("capacity", ctypes.c_int64),
+                ("id_offset", ctypes.c_int64)]
+
+
+def _load():
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(f"{LIB_PATH} missing: run `python -m paper_2502_05370_b200.build` "
+                          "(there is no CPU fallback)")
+    lib = ctypes.CDLL(LIB_PATH)
+    P, I32, I64, F = ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64, ctypes.c_float
+    sig = {
+        "fmoe_store_create": (I32, [ctypes.POINTER(fmoe_store_config), ctypes.c_int, ctypes.POINTER(P)]),
+        "fmoe_store_destroy": (None, [P]),
+        "fmoe_store_size": (I32, [P, ctypes.POINTER(I64)]),
+        "fmoe_store_get_config": (I32, [P, ctypes.POINTER(fmoe_store_config)]),
+        "fmoe_store_insert": (I32, [P, I64, P, P, P, P, P]),
+        "fmoe_store_read": (I32, [P, I64, I64, P, P, P]),
+        "fmoe_search_semantic": (I32, [P, I64, P, I32, P, P, P]),
+        "fmoe_search_trajectory": (I32, [P, I64, P, I32, I32, P, P, P]),
+        "fmoe_search_blend": (I32, [P, I64, P, P, I32, F, I32, P, P, P]),
+        "fmoe_select_experts": (I32, [P, I64, P, P, F, I32, I32, P, P, P]),
+        "fmoe_topk_merge": (I32, [I64, I32, I32, P, P, I32, P, P, ctypes.c_int, P]),
+        "fmoe_status_string": (ctypes.c_char_p, [I32]),
+        "fmoe_last_error": (ctypes.c_char_p, []),
+        "fmoe_kernel_launch_count": (I64, []),
+    }
+    for name, (res, args) in sig.items():
+        fn = getattr(lib, name)
+        fn.restype = res
+        fn.argtypes = args
+    return lib
+
+
+_lib = _load()
+ABI_SYMBOLS = ("fmoe_store_create", "fmoe_store_destroy", "fmoe_store_size", "fmoe_store_get_config",
+               "fmoe_store_insert", "fmoe_store_read", "fmoe_search_semantic", "fmoe_search_trajectory",
+               "fmoe_search_blend", "fmoe_select_experts", "fmoe_topk_merge", "fmoe_status_string",
+               "fmoe_last_error", "fmoe_kernel_launch_count")
+
+
+def _check(st: int):
+    if st != 0:
+        raise FmoeError(st, _lib.fmoe_last_error().decode())
+
+
+def _ptr(t):
+    return None if t is None else ctypes.c_void_p(t.data_ptr())
+
+
+def _stream(stream):
+    if stream is None:
+        if torch.cuda.is_available():
+            return ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+        return None
+    return ctypes.c_void_p(stream.cuda_stream if hasattr(stream, "cuda_stream") else int(stream))
+
+
+def _f32(t):
+    assert t.dtype == torch.float32 and t.is_contiguous(), "fp32 contiguous tensor expected"
+    return t
+
+
+def kernel_launch_count() -> int:
+    return int(_lib.fmoe_kernel_launch_count())
+
+
+# ------------------------------------------------------------------ ABI-named functions
+def fmoe_store_create(L, E, K, D, d, capacity, dtype="bf16", device=0, id_offset=0):
+    cfg = fmoe_store_config(L, E, K, D, d, FMOE_BF16 if dtype == "bf16" else FMOE_F32, capacity, id_offset)
+    h = ctypes.c_void_p()
+    _check(_lib.fmoe_store_create(ctypes.byref(cfg), int(device), ctypes.byref(h)))
+    return h
+
+
+def fmoe_store_destroy(h):
+    _lib.fmoe_store_destroy(h)
+
+
+def fmoe_store_size(h) -> int:
+    n = ctypes.c_int64()
+    _check(_lib.fmoe_store_size(h, ctypes.byref(n)))
+    return n.value
+
+
+def fmoe_store_insert(h, emb, maps, out_slot=None, out_replaced=None, stream=None):
+    _check(_lib.fmoe_store_insert(h, emb.shape[0], _ptr(_f32(emb)), _ptr(_f32(maps)), _ptr(out_slot),
+                                  _ptr(out_replaced), _stream(stream)))
+
+
+def fmoe_store_read(h, slot_begin, count, out_emb=None, out_maps=None, stream=None):
+    _check(_lib.fmoe_store_read(h, slot_begin, count, _ptr(out_emb), _ptr(out_maps), _stream(stream)))
+
+
+def fmoe_search_semantic(h, q_emb, k, out_score, out_id, stream=None):
+    _check(_lib.fmoe_search_semantic(h, q_emb.shape[0], _ptr(_f32(q_emb)), k, _ptr(out_score), _ptr(out_id),
+                                     _stream(stream)))
+
+
+def fmoe_search_trajectory(h, q_prefix, ell, k, out_score, out_id, stream=None):
+    _check(_lib.fmoe_search_trajectory(h, q_prefix.shape[0], _ptr(_f32(q_prefix)), ell, k, _ptr(out_score),
+                                       _ptr(out_id), _stream(stream)))
+
+
+def fmoe_search_blend(h, q_emb, q_prefix, ell, w_sem, k, out_score, out_id, stream=None):
+    _check(_lib.fmoe_search_blend(h, q_emb.shape[0], _ptr(_f32(q_emb)), _ptr(_f32(q_prefix)), ell, w_sem, k,
+                                  _ptr(out_score), _ptr(out_id), _stream(stream)))
+
+
+def fmoe_select_experts(h, map_id, score, delta, layer_begin, layer_end, out_mask, out_count, stream=None):
+    _check(_lib.fmoe_select_experts(h, map_id.shape[0], _ptr(map_id), _ptr(score), delta, layer_begin, layer_end,
+                                    _ptr(out_mask), _ptr(out_count), _stream(stream)))
+
+
+def fmoe_topk_merge(scores, ids, k, out_score, out_id, device=0, stream=None):
+    n_lists, B, k_in = scores.shape
+    _check(_lib.fmoe_topk_merge(B, n_lists, k_in, _ptr(scores), _ptr(ids), k, _ptr(out_score), _ptr(out_id),
+                                int(device), _stream(stream)))
+
+
+# ------------------------------------------------------------------ convenience object
+class ExpertMapStore:
+    """Owning wrapper: allocates outputs as torch tensors on the store's device."""
+
+    def __init__(self, L, E, K, D, d=3, capacity=1024, dtype="bf16", device=0, id_offset=0):
+        self.L, self.E, self.K, self.D, self.d = L, E, K, D, d
+        self.capacity, self.dtype, self.id_offset = capacity, dtype, id_offset
+        self.device = torch.device("cuda", device)
+        self._h = fmoe_store_create(L, E, K, D, d, capacity, dtype, device, id_offset)
+
+    def close(self):
+        if self._h is not None:
+            fmoe_store_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __len__(self):
+        return fmoe_store_size(self._h)
+
+    def insert(self, emb, maps, stream=None):
+        B = emb.shape[0]
+        slot = torch.empty(B, dtype=torch.int64, device=self.device)
+        rep = torch.empty(B, dtype=torch.int64, device=self.device)
+        fmoe_store_insert(self._h, emb, maps, slot, rep, stream)
+        return slot, rep
+
+    def read(self, slot_begin=0, count=None):
+        count = len(self) - slot_begin if count is None else count
+        e = torch.empty(count, self.D, device=self.device)
+        m = torch.empty(count, self.L, self.E, device=self.device)
+        fmoe_store_read(self._h, slot_begin, count, e, m)
+        return e, m
+
+    def _out(self, B, k):
+        return (torch.empty(B, k, dtype=torch.float32, device=self.device),
+                torch.empty(B, k, dtype=torch.int64, device=self.device))
+
+    def search_semantic(self, q_emb, k=1, stream=None):
+        s, i = self._out(q_emb.shape[0], k)
+        fmoe_search_semantic(self._h, q_emb, k, s, i, stream)
+        return s, i
+
+    def search_trajectory(self, q_prefix, ell, k=1, stream=None):
+        q_prefix = q_prefix[:, :ell].contiguous()
+        s, i = self._out(q_prefix.shape[0], k)
+        fmoe_search_trajectory(self._h, q_prefix, ell, k, s, i, stream)
+        return s, i
+
+    def search_blend(self, q_emb, q_prefix, ell, w_sem=-1.0, k=1, stream=None):
+        q_prefix = q_prefix[:, :ell].contiguous()
+        s, i = self._out(q_emb.shape[0], k)
+        fmoe_search_blend(self._h, q_emb, q_prefix, ell, w_sem, k, s, i, stream)
+        return s, i
+
+    def select_experts(self, map_id, score, delta=-1.0, layer_begin=0, layer_end=None, stream=None):
+        layer_end = self.L if layer_end is None else layer_end
+        B, T = map_id.shape[0], layer_end - layer_begin
+        mask = torch.empty(B, T, dtype=torch.int64, device=self.device)   # uint64 bit pattern
+        cnt = torch.empty(B, T, dtype=torch.int32, device=self.device)
+        fmoe_select_experts(self._h, map_id.contiguous(), None if score is None else score.contiguous(), delta,
+                            layer_begin, layer_end, mask, cnt, stream)
+        return mask, cnt

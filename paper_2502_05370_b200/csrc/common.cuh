@@ -1,0 +1,154 @@
+// common.cuh -- shared device helpers of the fMoE B200 path (sm_100a).
+//
+// Packed top-k keys: the order "score descending, id ascending" (R5) is
+// the unsigned order of a 64-bit key = (orderable(score) << 32) | (~id32):
+// a larger key is a better candidate, so every merge is a plain u64 max.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+#include <cuda_bf16.h>
+
+namespace fmoe {
+
+constexpr int kWarp = 32;
+constexpr int kMaxK = 64;
+constexpr int kMaxE = 64;
+
+struct Bf16Tag {};
+struct F32Tag {};
+
+// ---------------------------------------------------------------- keys
+__device__ __forceinline__ uint32_t orderable(float s) {
+  s = s + 0.0f;                                  // -0.0 -> +0.0 (canonical)
+  uint32_t u = __float_as_uint(s);
+  return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
+}
+__device__ __forceinline__ float from_orderable(uint32_t u) {
+  return __uint_as_float((u & 0x80000000u) ? (u & 0x7fffffffu) : ~u);
+}
+// NaN never enters a top-k list: it maps to the empty key 0.
+__device__ __forceinline__ uint64_t pack_key(float s, uint32_t id) {
+  if (s != s) return 0ull;
+  return (uint64_t(orderable(s)) << 32) | uint64_t(0xffffffffu - id);
+}
+__device__ __forceinline__ int64_t key_id(uint64_t key) {
+  return key == 0ull ? -1ll : int64_t(0xffffffffu - uint32_t(key & 0xffffffffu));
+}
+__device__ __forceinline__ float key_score(uint64_t key) {
+  return key == 0ull ? -__int_as_float(0x7f800000) : from_orderable(uint32_t(key >> 32));
+}
+
+__device__ __forceinline__ uint64_t shfl_u64(uint64_t v, int src) {
+  uint32_t lo = __shfl_sync(0xffffffffu, uint32_t(v), src);
+  uint32_t hi = __shfl_sync(0xffffffffu, uint32_t(v >> 32), src);
+  return (uint64_t(hi) << 32) | lo;
+}
+__device__ __forceinline__ uint64_t shfl_up_u64(uint64_t v, int d) {
+  uint32_t lo = __shfl_up_sync(0xffffffffu, uint32_t(v), d);
+  uint32_t hi = __shfl_up_sync(0xffffffffu, uint32_t(v >> 32), d);
+  return (uint64_t(hi) << 32) | lo;
+}
+
+// ---------------------------------------------------------------- warp top-k
+// A warp-distributed list sorted descending: entry j lives in lane j%32,
+// register slot j/32.  KPL = ceil(kmax/32) slots.  All lanes call every method
+// with warp-uniform arguments.
+template <int KPL>
+struct WarpTopK {
+  uint64_t v[KPL];
+
+  __device__ __forceinline__ void init() {
+#pragma unroll
+    for (int s = 0; s < KPL; ++s) v[s] = 0ull;
+  }
+  // key at index k-1 (the current admission threshold)
+  __device__ __forceinline__ uint64_t kth(int k) const {
+    const int j = k - 1;
+    uint64_t x = v[0];
+#pragma unroll
+    for (int s = 1; s < KPL; ++s)
+      if (j / 32 == s) x = v[s];
+    return shfl_u64(x, j & 31);
+  }
+  // insert key c (warp-uniform), assumed better than kth(k) and not present.
+  __device__ __forceinline__ void insert(uint64_t c) {
+    const int lane = threadIdx.x & 31;
+    int pos = 0;
+#pragma unroll
+    for (int s = 0; s < KPL; ++s) pos += __popc(__ballot_sync(0xffffffffu, v[s] > c));
+#pragma unroll
+    for (int s = KPL - 1; s >= 0; --s) {
+      uint64_t up = shfl_up_u64(v[s], 1);
+      uint64_t carry = (s > 0) ? shfl_u64(v[s > 0 ? s - 1 : 0], 31) : 0ull;
+      if (lane == 0) up = carry;
+      const int j = s * 32 + lane;
+      if (j > pos) v[s] = up;
+      else if (j == pos) v[s] = c;
+    }
+  }
+  // offer one candidate per lane (keys unique); admits those beating kth(k).
+  __device__ __forceinline__ void offer(uint64_t key, int k) {
+    uint64_t thr = kth(k);
+    unsigned m = __ballot_sync(0xffffffffu, key > thr);
+    while (m) {
+      const int src = __ffs(m) - 1;
+      m &= m - 1;
+      const uint64_t c = shfl_u64(key, src);
+      if (c > thr) {
+        insert(c);
+        thr = kth(k);
+      }
+    }
+  }
+  // entry j (0-based), returned on every lane
+  __device__ __forceinline__ uint64_t get(int j) const {
+    uint64_t x = v[0];
+#pragma unroll
+    for (int s = 1; s < KPL; ++s)
+      if (j / 32 == s) x = v[s];
+    return shfl_u64(x, j & 31);
+  }
+  // store entries [0, k) to dst (coalesced)
+  __device__ __forceinline__ void store(uint64_t* dst, int k) const {
+    const int lane = threadIdx.x & 31;
+#pragma unroll
+    for (int s = 0; s < KPL; ++s) {
+      const int j = s * 32 + lane;
+      if (j < k) dst[j] = v[s];
+    }
+  }
+};
+
+// ---------------------------------------------------------------- bf16 / 16-byte chunks
+__device__ __forceinline__ void unpack8(const uint4& u, float (&f)[8], Bf16Tag) {
+  f[0] = __uint_as_float(u.x << 16); f[1] = __uint_as_float(u.x & 0xffff0000u);
+  f[2] = __uint_as_float(u.y << 16); f[3] = __uint_as_float(u.y & 0xffff0000u);
+  f[4] = __uint_as_float(u.z << 16); f[5] = __uint_as_float(u.z & 0xffff0000u);
+  f[6] = __uint_as_float(u.w << 16); f[7] = __uint_as_float(u.w & 0xffff0000u);
+}
+
+template <typename Tag> struct StoreT;
+template <> struct StoreT<Bf16Tag> {
+  using T = __nv_bfloat16;
+  static constexpr int kElemsPer16B = 8;
+  static constexpr int kBytes = 2;
+};
+template <> struct StoreT<F32Tag> {
+  using T = float;
+  static constexpr int kElemsPer16B = 4;
+  static constexpr int kBytes = 4;
+};
+
+__device__ __forceinline__ uint4 ld_stream(const void* p) {
+  uint4 r;
+  asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "l"(p));
+  return r;
+}
+
+__device__ __forceinline__ float to_store_value(float x, Bf16Tag) {
+  return __bfloat162float(__float2bfloat16_rn(x));
+}
+__device__ __forceinline__ float to_store_value(float x, F32Tag) { return x; }
+
+}  // namespace fmoe

@@ -1,0 +1,83 @@
+// kernels.cuh -- launch interface of the fMoE sm_100a kernels (internal, not ABI).
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace fmoe {
+
+// Device view of a store's HBM tiles.
+struct StoreView {
+  const void* emb;     // [cap][Dp] dtype, row-major
+  const float* r_e;    // [cap] 1/||quantised embedding|| (0 for a zero row)
+  const void* maps;    // [L][cap][Ep] dtype, layer-major slabs
+  const float* psq;    // [L][cap] prefix squared norms sum_{l'<=l} ||P_l'||^2
+  int64_t cap;         // slab stride (rows)
+  int L, E, D, Dp, Ep;
+  int bf16;            // 1 = bf16 tiles, 0 = fp32
+};
+
+// One scoring pass: queries [q0, q0+nq) of the batch against rows [0, n_rows).
+struct ScanArgs {
+  StoreView st;
+  int64_t n_rows;
+  int ell;                   // prefix layers used by the trajectory part
+  float w_sem;               // blend weight: 1 semantic only, 0 trajectory only
+  int k;                     // list length (<= kMaxK)
+  const float* q_emb;        // [B][D]  (may be null when w_sem == 0)
+  const float* q_prefix;     // [B][*] rows of q_stride floats, layer l at l*E
+  int64_t q_stride;
+  int q0, nq;                // query slice of this pass (nq <= 4)
+  uint32_t id_offset;        // global id of row 0
+  uint64_t* cand;            // [B][grid][k] per-block candidate keys
+  int grid;                  // blocks of the launch (cand stride)
+  float* qinfo;              // [B] 1 if the query is valid (non-zero norms), else 0
+};
+
+// GEMV scan (B <= 4 per pass): bandwidth-bound warp-per-32-rows streaming.
+cudaError_t launch_scan_gemv(const ScanArgs& a, cudaStream_t s, int* grid_out);
+int scan_gemv_grid(const ScanArgs& a);
+
+// Merge per-block candidate keys -> per-query top-k.
+//  keys [B][n_lists][k_in]; writes either (out_score,out_id) or out_keys [B][k].
+cudaError_t launch_merge_keys(int B, int n_lists, int k_in, const uint64_t* keys, int k,
+                              const float* qinfo, float* out_score, int64_t* out_id,
+                              uint64_t* out_keys, cudaStream_t s);
+// Merge (score, id) lists from an all-gather: [n_lists][B][k_in].
+cudaError_t launch_merge_lists(int B, int n_lists, int k_in, const float* scores,
+                               const int64_t* ids, int k, float* out_score, int64_t* out_id,
+                               cudaStream_t s);
+
+// Eq. 4-6 selection, one warp per (query, layer).
+cudaError_t launch_select(const StoreView& st, int B, const int64_t* map_id, const float* score,
+                          float delta, int K, int layer_begin, int layer_end, int64_t id_offset,
+                          int64_t n_rows, uint64_t* out_mask, int32_t* out_count, cudaStream_t s);
+
+// Quantise + write rows (append or replace) and their norm tables.
+//  slot of new row x: slots ? slots[x] (skip if < 0) : first_slot + x.
+struct WriteArgs {
+  void* emb; float* r_e; void* maps; float* psq;
+  int64_t cap; int L, E, D, Dp, Ep, bf16;
+  const float* in_emb; const float* in_maps;   // [B][D], [B][L][E]
+  int B;
+  const int64_t* slots; int64_t first_slot;
+};
+cudaError_t launch_write_rows(const WriteArgs& w, cudaStream_t s);
+
+// Victim resolution (Reading R8): rows j in batch order take their best
+// candidate not claimed by an earlier row.  keys [nrep][kk] (from merge).
+//  victims [nrep] (local slot or -1); also scatters to out_slot/out_replaced
+//  at positions x0 + j, and marks appended rows [0, x0) in out_slot/out_replaced.
+cudaError_t launch_resolve(int nrep, int kk, const uint64_t* keys, uint32_t id_offset,
+                           int64_t* victims, int x0, int64_t first_append_slot,
+                           int64_t* out_slot, int64_t* out_replaced, cudaStream_t s);
+cudaError_t launch_append_ids(int n, int64_t first_slot, uint32_t id_offset, int64_t* out_slot,
+                              int64_t* out_replaced, cudaStream_t s);
+
+// Read back rows as fp32.
+cudaError_t launch_read_rows(const StoreView& st, int64_t slot0, int64_t count, float* out_emb,
+                             float* out_maps, cudaStream_t s);
+
+// launch counter (for the bench's gpu_launches)
+void count_launch(int n = 1);
+
+}  // namespace fmoe

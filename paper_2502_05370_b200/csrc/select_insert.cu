@@ -1,0 +1,343 @@
+// select_insert.cu -- K4 top-k merge, K5 expert selection, K6 row writes and
+// the victim resolution of the RDY insert.
+#include <atomic>
+#include "common.cuh"
+#include "kernels.cuh"
+
+namespace fmoe {
+
+static std::atomic<int64_t> g_launches{0};
+void count_launch(int n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
+int64_t launch_count() { return g_launches.load(); }
+
+// ------------------------------------------------------------------ K4 merge
+// One warp per query: stream the candidate keys through a WarpTopK.
+template <int KPL>
+__global__ void __launch_bounds__(32) merge_keys_kernel(int n_lists, int k_in, const uint64_t* __restrict__ keys,
+                                                        int k, const float* __restrict__ qinfo,
+                                                        float* out_score, int64_t* out_id, uint64_t* out_keys) {
+  const int q = blockIdx.x, lane = threadIdx.x;
+  WarpTopK<KPL> m;
+  m.init();
+  const int64_t total = int64_t(n_lists) * k_in;
+  const uint64_t* src = keys + int64_t(q) * total;
+  for (int64_t j0 = 0; j0 < total; j0 += 32) {
+    const uint64_t key = (j0 + lane < total) ? src[j0 + lane] : 0ull;
+    m.offer(key, k);
+  }
+  const bool valid = qinfo ? (qinfo[q] != 0.f) : true;
+#pragma unroll
+  for (int s = 0; s < KPL; ++s) {
+    const int j = s * 32 + lane;
+    if (j < k) {
+      const uint64_t key = m.v[s];
+      if (out_keys) out_keys[int64_t(q) * k + j] = valid ? key : 0ull;
+      if (out_score) out_score[int64_t(q) * k + j] = valid ? key_score(key) : __int_as_float(0x7fc00000);
+      if (out_id) out_id[int64_t(q) * k + j] = valid ? key_id(key) : -1;
+    }
+  }
+}
+
+cudaError_t launch_merge_keys(int B, int n_lists, int k_in, const uint64_t* keys, int k, const float* qinfo,
+                              float* out_score, int64_t* out_id, uint64_t* out_keys, cudaStream_t s) {
+  if (B <= 0) return cudaSuccess;
+  if (k <= 32)
+    merge_keys_kernel<1><<<B, 32, 0, s>>>(n_lists, k_in, keys, k, qinfo, out_score, out_id, out_keys);
+  else
+    merge_keys_kernel<2><<<B, 32, 0, s>>>(n_lists, k_in, keys, k, qinfo, out_score, out_id, out_keys);
+  count_launch();
+  return cudaGetLastError();
+}
+
+// (score, id) lists of an all-gather: [n_lists][B][k_in]
+template <int KPL>
+__global__ void __launch_bounds__(32) merge_lists_kernel(int B, int n_lists, int k_in, const float* __restrict__ scores,
+                                                         const int64_t* __restrict__ ids, int k, float* out_score,
+                                                         int64_t* out_id) {
+  const int q = blockIdx.x, lane = threadIdx.x;
+  WarpTopK<KPL> m;
+  m.init();
+  bool bad = false;
+  for (int r = 0; r < n_lists; ++r) {
+    const int64_t base = (int64_t(r) * B + q) * k_in;
+    for (int j0 = 0; j0 < k_in; j0 += 32) {
+      uint64_t key = 0ull;
+      if (j0 + lane < k_in) {
+        const float sc = scores[base + j0 + lane];
+        const int64_t id = ids[base + j0 + lane];
+        bad |= (sc != sc);
+        if (id >= 0) key = pack_key(sc, uint32_t(id));
+      }
+      m.offer(key, k);
+    }
+  }
+  bad = __any_sync(0xffffffffu, bad);
+#pragma unroll
+  for (int s = 0; s < KPL; ++s) {
+    const int j = s * 32 + lane;
+    if (j < k) {
+      out_score[int64_t(q) * k + j] = bad ? __int_as_float(0x7fc00000) : key_score(m.v[s]);
+      out_id[int64_t(q) * k + j] = bad ? -1 : key_id(m.v[s]);
+    }
+  }
+}
+
+cudaError_t launch_merge_lists(int B, int n_lists, int k_in, const float* scores, const int64_t* ids, int k,
+                               float* out_score, int64_t* out_id, cudaStream_t s) {
+  if (B <= 0) return cudaSuccess;
+  if (k <= 32)
+    merge_lists_kernel<1><<<B, 32, 0, s>>>(B, n_lists, k_in, scores, ids, k, out_score, out_id);
+  else
+    merge_lists_kernel<2><<<B, 32, 0, s>>>(B, n_lists, k_in, scores, ids, k, out_score, out_id);
+  count_launch();
+  return cudaGetLastError();
+}
+
+// ------------------------------------------------------------------ K5 select (Eq. 4-6)
+// One warp per (query, target layer).  The E <= 64 probabilities of the
+// matched row are ranked by (p desc, index asc) in registers (each lane owns
+// entries lane and lane+32), scattered into shared memory in rank order, and
+// one lane accumulates them in float64 in that order -- the exact order and
+// precision of the oracle, so sets are bit-identical given the same score.
+constexpr int kSelWarps = 8;
+
+template <class Tag>
+__device__ __forceinline__ float load_p(const StoreView& st, int t, int64_t row, int j) {
+  using T = typename StoreT<Tag>::T;
+  const T* m = static_cast<const T*>(st.maps);
+  if constexpr (sizeof(T) == 2)
+    return __bfloat162float(m[(int64_t(t) * st.cap + row) * st.Ep + j]);
+  else
+    return m[(int64_t(t) * st.cap + row) * st.Ep + j];
+}
+
+template <class Tag>
+__global__ void __launch_bounds__(kSelWarps * 32) select_kernel(StoreView st, int B, const int64_t* __restrict__ map_id,
+                                                                const float* __restrict__ score, float delta, int K,
+                                                                int lb, int T, int64_t id_offset, int64_t n_rows,
+                                                                uint64_t* out_mask, int32_t* out_count) {
+  __shared__ float sp[kSelWarps][kMaxE];
+  __shared__ int si[kSelWarps][kMaxE];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t gw = int64_t(blockIdx.x) * kSelWarps + warp;
+  if (gw >= int64_t(B) * T) return;
+  const int q = int(gw / T), tt = int(gw % T), t = lb + tt;
+  const int64_t id = map_id[q];
+  const int64_t loc = id - id_offset;
+  const int64_t o = int64_t(q) * T + tt;
+  if (id < 0 || loc < 0 || loc >= n_rows) {
+    if (lane == 0) { out_mask[o] = 0ull; out_count[o] = 0; }
+    return;
+  }
+  double dl;
+  if (delta < 0.f) {
+    const float s = score[q];
+    if (s != s) {
+      dl = 1.0;
+    } else {
+      double sd = double(s);
+      sd = sd < -1.0 ? -1.0 : (sd > 1.0 ? 1.0 : sd);
+      const double v = 1.0 - sd;
+      dl = v < 0.0 ? 0.0 : (v > 1.0 ? 1.0 : v);
+    }
+  } else {
+    dl = double(delta);
+  }
+  const int E = st.E;
+  const float NEG = -__int_as_float(0x7f800000);
+  const float p0 = lane < E ? load_p<Tag>(st, t, loc, lane) : NEG;
+  const float p1 = lane + 32 < E ? load_p<Tag>(st, t, loc, lane + 32) : NEG;
+  int r0 = 0, r1 = 0;
+  for (int j = 0; j < E; ++j) {
+    const float a = __shfl_sync(0xffffffffu, p0, j & 31);
+    const float b = __shfl_sync(0xffffffffu, p1, j & 31);
+    const float pj = j < 32 ? a : b;
+    r0 += (pj > p0) || (pj == p0 && j < lane);
+    r1 += (pj > p1) || (pj == p1 && j < lane + 32);
+  }
+  if (lane < E) { sp[warp][r0] = p0; si[warp][r0] = lane; }
+  if (lane + 32 < E) { sp[warp][r1] = p1; si[warp][r1] = lane + 32; }
+  __syncwarp();
+  if (lane == 0) {
+    double cum = 0.0;
+    int m = E;
+    for (int r = 0; r < E; ++r) {
+      cum = cum + double(sp[warp][r]);
+      if (cum >= dl && r + 1 >= K) { m = r + 1; break; }
+    }
+    uint64_t mask = 0ull;
+    for (int r = 0; r < m; ++r) mask |= 1ull << si[warp][r];
+    out_mask[o] = mask;
+    out_count[o] = m;
+  }
+}
+
+cudaError_t launch_select(const StoreView& st, int B, const int64_t* map_id, const float* score, float delta, int K,
+                          int layer_begin, int layer_end, int64_t id_offset, int64_t n_rows, uint64_t* out_mask,
+                          int32_t* out_count, cudaStream_t s) {
+  const int T = layer_end - layer_begin;
+  const int64_t warps = int64_t(B) * T;
+  if (warps <= 0) return cudaSuccess;
+  const int grid = int((warps + kSelWarps - 1) / kSelWarps);
+  if (st.bf16)
+    select_kernel<Bf16Tag><<<grid, kSelWarps * 32, 0, s>>>(st, B, map_id, score, delta, K, layer_begin, T, id_offset,
+                                                           n_rows, out_mask, out_count);
+  else
+    select_kernel<F32Tag><<<grid, kSelWarps * 32, 0, s>>>(st, B, map_id, score, delta, K, layer_begin, T, id_offset,
+                                                          n_rows, out_mask, out_count);
+  count_launch();
+  return cudaGetLastError();
+}
+
+// ------------------------------------------------------------------ K6 write rows
+// One warp per new row: quantise (RNE), write the embedding row, its inverse
+// norm (float64 accumulation of the quantised values), the map row into each
+// layer slab and the prefix squared-norm table.
+__device__ __forceinline__ double warp_sum_dbl(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+template <class Tag>
+__global__ void __launch_bounds__(256) write_rows_kernel(WriteArgs w) {
+  using T = typename StoreT<Tag>::T;
+  const int lane = threadIdx.x & 31;
+  const int64_t x = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  if (x >= w.B) return;
+  const int64_t slot = w.slots ? w.slots[x] : w.first_slot + x;
+  if (slot < 0) return;
+  T* emb = static_cast<T*>(w.emb);
+  T* maps = static_cast<T*>(w.maps);
+  double acc = 0.0;
+  for (int e = lane; e < w.Dp; e += 32) {
+    const float v = e < w.D ? to_store_value(w.in_emb[x * w.D + e], Tag()) : 0.f;
+    if constexpr (sizeof(T) == 2) emb[slot * w.Dp + e] = __float2bfloat16_rn(v);
+    else emb[slot * w.Dp + e] = v;
+    acc += double(v) * double(v);
+  }
+  acc = warp_sum_dbl(acc);
+  if (lane == 0) w.r_e[slot] = acc > 0.0 ? float(1.0 / sqrt(acc)) : 0.f;
+  double cum = 0.0;
+  for (int l = 0; l < w.L; ++l) {
+    double a = 0.0;
+    for (int j = lane; j < w.Ep; j += 32) {
+      const float v = j < w.E ? to_store_value(w.in_maps[(x * w.L + l) * w.E + j], Tag()) : 0.f;
+      const int64_t o = (int64_t(l) * w.cap + slot) * w.Ep + j;
+      if constexpr (sizeof(T) == 2) maps[o] = __float2bfloat16_rn(v);
+      else maps[o] = v;
+      a += double(v) * double(v);
+    }
+    cum += warp_sum_dbl(a);
+    if (lane == 0) w.psq[int64_t(l) * w.cap + slot] = float(cum);
+  }
+}
+
+cudaError_t launch_write_rows(const WriteArgs& w, cudaStream_t s) {
+  if (w.B <= 0) return cudaSuccess;
+  const int64_t threads = int64_t(w.B) * 32;
+  const int grid = int((threads + 255) / 256);
+  if (w.bf16) write_rows_kernel<Bf16Tag><<<grid, 256, 0, s>>>(w);
+  else write_rows_kernel<F32Tag><<<grid, 256, 0, s>>>(w);
+  count_launch();
+  return cudaGetLastError();
+}
+
+// ------------------------------------------------------------------ victim resolution (R8)
+// Single warp.  Row j (batch order) takes the best-ranked candidate whose slot
+// is not claimed by an earlier row.  keys hold LOCAL slots (scan id_offset 0).
+__global__ void __launch_bounds__(32) resolve_kernel(int nrep, int kk, const uint64_t* __restrict__ keys,
+                                                     uint32_t id_offset, int64_t* slots_all, int x0,
+                                                     int64_t first_append_slot, int64_t* out_slot,
+                                                     int64_t* out_replaced) {
+  __shared__ int64_t claimed[kMaxK];
+  const int lane = threadIdx.x;
+  for (int x = lane; x < x0; x += 32) {
+    slots_all[x] = first_append_slot + x;
+    if (out_slot) out_slot[x] = int64_t(id_offset) + first_append_slot + x;
+    if (out_replaced) out_replaced[x] = -1;
+  }
+  for (int j = 0; j < nrep; ++j) {
+    int64_t best = -1;
+    for (int c0 = 0; c0 < kk; c0 += 32) {
+      const int c = c0 + lane;
+      int64_t loc = -1;
+      if (c < kk) {
+        const uint64_t key = keys[int64_t(j) * kk + c];
+        if (key != 0ull) {
+          loc = key_id(key);
+          for (int i = 0; i < j; ++i)
+            if (claimed[i] == loc) { loc = -1; break; }
+        }
+      }
+      const unsigned m = __ballot_sync(0xffffffffu, loc >= 0);
+      if (m) {
+        best = __shfl_sync(0xffffffffu, loc, __ffs(m) - 1);
+        break;
+      }
+    }
+    if (lane == 0) {
+      claimed[j] = best >= 0 ? best : -2;
+      slots_all[x0 + j] = best;
+      if (out_slot) out_slot[x0 + j] = best >= 0 ? int64_t(id_offset) + best : -1;
+      if (out_replaced) out_replaced[x0 + j] = best >= 0 ? int64_t(id_offset) + best : -1;
+    }
+    __syncwarp();
+  }
+}
+
+cudaError_t launch_resolve(int nrep, int kk, const uint64_t* keys, uint32_t id_offset, int64_t* slots_all, int x0,
+                           int64_t first_append_slot, int64_t* out_slot, int64_t* out_replaced, cudaStream_t s) {
+  resolve_kernel<<<1, 32, 0, s>>>(nrep, kk, keys, id_offset, slots_all, x0, first_append_slot, out_slot, out_replaced);
+  count_launch();
+  return cudaGetLastError();
+}
+
+__global__ void append_ids_kernel(int n, int64_t first_slot, uint32_t id_offset, int64_t* out_slot,
+                                  int64_t* out_replaced) {
+  const int x = blockIdx.x * blockDim.x + threadIdx.x;
+  if (x >= n) return;
+  if (out_slot) out_slot[x] = int64_t(id_offset) + first_slot + x;
+  if (out_replaced) out_replaced[x] = -1;
+}
+
+cudaError_t launch_append_ids(int n, int64_t first_slot, uint32_t id_offset, int64_t* out_slot, int64_t* out_replaced,
+                              cudaStream_t s) {
+  if (n <= 0 || (!out_slot && !out_replaced)) return cudaSuccess;
+  append_ids_kernel<<<(n + 255) / 256, 256, 0, s>>>(n, first_slot, id_offset, out_slot, out_replaced);
+  count_launch();
+  return cudaGetLastError();
+}
+
+// ------------------------------------------------------------------ read back
+template <class Tag>
+__global__ void read_rows_kernel(StoreView st, int64_t slot0, int64_t count, float* out_emb, float* out_maps) {
+  using T = typename StoreT<Tag>::T;
+  const T* emb = static_cast<const T*>(st.emb);
+  const T* maps = static_cast<const T*>(st.maps);
+  const int64_t ne = out_emb ? count * st.D : 0;
+  const int64_t nm = out_maps ? count * st.L * st.E : 0;
+  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < ne + nm; i += int64_t(gridDim.x) * blockDim.x) {
+    if (i < ne) {
+      const int64_t r = i / st.D, e = i % st.D;
+      out_emb[i] = float(emb[(slot0 + r) * st.Dp + e]);
+    } else {
+      const int64_t k = i - ne;
+      const int64_t r = k / (int64_t(st.L) * st.E), rem = k % (int64_t(st.L) * st.E);
+      const int l = int(rem / st.E), j = int(rem % st.E);
+      out_maps[k] = float(maps[(int64_t(l) * st.cap + slot0 + r) * st.Ep + j]);
+    }
+  }
+}
+
+cudaError_t launch_read_rows(const StoreView& st, int64_t slot0, int64_t count, float* out_emb, float* out_maps,
+                             cudaStream_t s) {
+  if (count <= 0) return cudaSuccess;
+  const int grid = 592;
+  if (st.bf16) read_rows_kernel<Bf16Tag><<<grid, 256, 0, s>>>(st, slot0, count, out_emb, out_maps);
+  else read_rows_kernel<F32Tag><<<grid, 256, 0, s>>>(st, slot0, count, out_emb, out_maps);
+  count_launch();
+  return cudaGetLastError();
+}
+
+}  // namespace fmoe

@@ -1,0 +1,435 @@
+// store.cu -- the C ABI of include/fmoe.h: store object, argument checks,
+// host/device staging, and dispatch of the sm_100a kernels.
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/fmoe.h"
+#include "common.cuh"
+#include "kernels.cuh"
+
+namespace fmoe {
+int64_t launch_count();
+}
+
+using namespace fmoe;
+
+struct fmoe_store {
+  fmoe_store_config cfg;
+  int device;
+  int bf16, esz, Dp, Ep;
+  void* emb = nullptr;
+  float* r_e = nullptr;
+  void* maps = nullptr;
+  float* psq = nullptr;
+  int64_t n = 0;
+
+  StoreView view() const {
+    StoreView v;
+    v.emb = emb; v.r_e = r_e; v.maps = maps; v.psq = psq;
+    v.cap = cfg.capacity; v.L = cfg.L; v.E = cfg.E; v.D = cfg.D; v.Dp = Dp; v.Ep = Ep; v.bf16 = bf16;
+    return v;
+  }
+};
+
+namespace {
+
+thread_local std::string g_err;
+
+fmoe_status fail(fmoe_status s, const std::string& msg) {
+  g_err = msg;
+  return s;
+}
+fmoe_status cuda_fail(cudaError_t e, const char* what) {
+  g_err = std::string(what) + ": " + cudaGetErrorString(e);
+  return e == cudaErrorMemoryAllocation ? FMOE_ERR_OOM : FMOE_ERR_CUDA;
+}
+
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int dev) {
+    cudaGetDevice(&prev);
+    if (prev != dev) cudaSetDevice(dev);
+  }
+  ~DeviceGuard() {
+    int cur = -1;
+    cudaGetDevice(&cur);
+    if (prev >= 0 && cur != prev) cudaSetDevice(prev);
+  }
+};
+
+// 0 = host (pageable or pinned), 1 = device memory of `dev`, -1 = other device
+int ptr_kind(const void* p, int dev) {
+  cudaPointerAttributes at;
+  if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
+    cudaGetLastError();
+    return 0;
+  }
+  if (at.type == cudaMemoryTypeDevice || at.type == cudaMemoryTypeManaged) return at.device == dev ? 1 : -1;
+  return 0;
+}
+
+// Stream-ordered staging of host arguments through device buffers.
+struct Staging {
+  cudaStream_t s;
+  int dev;
+  std::vector<void*> allocs;
+  struct Back { void* host; void* dev; size_t bytes; };
+  std::vector<Back> backs;
+  cudaError_t err = cudaSuccess;
+  const char* what = "";
+  bool bad_device = false;
+
+  Staging(cudaStream_t s_, int dev_) : s(s_), dev(dev_) {}
+
+  void* scratch(size_t bytes) {
+    if (err != cudaSuccess) return nullptr;
+    void* p = nullptr;
+    if (bytes == 0) bytes = 16;
+    cudaError_t e = cudaMallocAsync(&p, bytes, s);
+    if (e != cudaSuccess) { err = e; what = "cudaMallocAsync"; return nullptr; }
+    allocs.push_back(p);
+    return p;
+  }
+  template <class T>
+  const T* in(const T* p, size_t count) {
+    if (!p) return nullptr;
+    const int k = ptr_kind(p, dev);
+    if (k == 1) return p;
+    if (k < 0) { bad_device = true; return nullptr; }
+    T* d = static_cast<T*>(scratch(count * sizeof(T)));
+    if (!d) return nullptr;
+    if (count) {
+      cudaError_t e = cudaMemcpyAsync(d, p, count * sizeof(T), cudaMemcpyHostToDevice, s);
+      if (e != cudaSuccess) { err = e; what = "H2D copy"; }
+    }
+    return d;
+  }
+  template <class T>
+  T* out(T* p, size_t count) {
+    if (!p) return nullptr;
+    const int k = ptr_kind(p, dev);
+    if (k == 1) return p;
+    if (k < 0) { bad_device = true; return nullptr; }
+    T* d = static_cast<T*>(scratch(count * sizeof(T)));
+    if (d) backs.push_back({p, d, count * sizeof(T)});
+    return d;
+  }
+  fmoe_status check() const {
+    if (bad_device) return fail(FMOE_ERR_INVALID_ARG, "array on another device");
+    if (err != cudaSuccess) return cuda_fail(err, what);
+    return FMOE_OK;
+  }
+  // copies outputs back, frees scratch; synchronises if any output is host memory
+  fmoe_status finish(fmoe_status st) {
+    for (auto& b : backs) {
+      if (st == FMOE_OK && b.bytes) {
+        cudaError_t e = cudaMemcpyAsync(b.host, b.dev, b.bytes, cudaMemcpyDeviceToHost, s);
+        if (e != cudaSuccess) st = cuda_fail(e, "D2H copy");
+      }
+    }
+    for (void* p : allocs) cudaFreeAsync(p, s);
+    if (!backs.empty()) {
+      cudaError_t e = cudaStreamSynchronize(s);
+      if (e != cudaSuccess && st == FMOE_OK) st = cuda_fail(e, "stream sync");
+    }
+    return st;
+  }
+};
+
+int round_up(int x, int m) { return (x + m - 1) / m * m; }
+
+fmoe_status check_cfg(const fmoe_store_config* c) {
+  if (!c) return fail(FMOE_ERR_INVALID_ARG, "null config");
+  if (c->L < 1 || c->E < 1 || c->E > FMOE_MAX_E || c->D < 1 || c->K < 1 || c->K > c->E)
+    return fail(FMOE_ERR_SHAPE, "need L>=1, 1<=E<=64, 1<=K<=E, D>=1");
+  if (c->d < 1 || c->d >= c->L) return fail(FMOE_ERR_SHAPE, "need 1 <= d < L");
+  if (c->dtype != FMOE_F32 && c->dtype != FMOE_BF16) return fail(FMOE_ERR_SHAPE, "dtype");
+  if (c->capacity < 1 || c->id_offset < 0 || c->capacity + c->id_offset > 0xffffffffll)
+    return fail(FMOE_ERR_SHAPE, "capacity/id_offset: global ids must fit in 32 bits");
+  if (c->L * int64_t(round_up(c->E, 8)) * 4 > 200 * 1024)
+    return fail(FMOE_ERR_SHAPE, "L*E too large for the staged trajectory query");
+  if (int64_t(round_up(c->D, 8)) * 4 > 200 * 1024) return fail(FMOE_ERR_SHAPE, "D too large");
+  return FMOE_OK;
+}
+
+// One scoring call: scan (passes of <= 4 queries) + merge.
+fmoe_status run_search(const fmoe_store* st, int64_t B, const float* dq, const float* dp, int64_t q_stride, int ell,
+                       float w, int k, int64_t n_rows, uint32_t id_offset, Staging& S, cudaStream_t s,
+                       float* ds, int64_t* di, uint64_t* dkeys, bool check_queries) {
+  if (n_rows == 0) {
+    cudaError_t e = launch_merge_keys(int(B), 0, k, nullptr, k, nullptr, ds, di, dkeys, s);
+    return e == cudaSuccess ? FMOE_OK : cuda_fail(e, "merge launch");
+  }
+  ScanArgs a{};
+  a.st = st->view();
+  a.n_rows = n_rows;
+  a.ell = ell;
+  a.w_sem = w;
+  a.k = k;
+  a.q_emb = dq;
+  a.q_prefix = dp;
+  a.q_stride = q_stride;
+  a.id_offset = id_offset;
+  a.q0 = 0;
+  a.nq = int(B < 4 ? B : 4);
+  a.grid = scan_gemv_grid(a);
+  uint64_t* cand = static_cast<uint64_t*>(S.scratch(size_t(B) * a.grid * k * 8));
+  float* qinfo = static_cast<float*>(S.scratch(size_t(B) * 4));
+  fmoe_status cs = S.check();
+  if (cs != FMOE_OK) return cs;
+  a.cand = cand;
+  a.qinfo = qinfo;
+  for (int64_t q0 = 0; q0 < B; q0 += 4) {
+    a.q0 = int(q0);
+    a.nq = int(B - q0 < 4 ? B - q0 : 4);
+    cudaError_t e = launch_scan_gemv(a, s, nullptr);
+    if (e != cudaSuccess) return cuda_fail(e, "scan launch");
+  }
+  cudaError_t e = launch_merge_keys(int(B), a.grid, k, cand, k, check_queries ? qinfo : nullptr, ds, di, dkeys, s);
+  return e == cudaSuccess ? FMOE_OK : cuda_fail(e, "merge launch");
+}
+
+fmoe_status search_common(const fmoe_store* st, int64_t B, const float* q_emb, const float* q_prefix, int32_t ell,
+                          float w, int32_t k, float* out_score, int64_t* out_id, void* stream) {
+  if (!st) return fail(FMOE_ERR_INVALID_ARG, "null store");
+  if (B < 0) return fail(FMOE_ERR_INVALID_ARG, "B < 0");
+  if (k < 1 || k > FMOE_MAX_K) return fail(FMOE_ERR_INVALID_ARG, "k must be in [1, 64]");
+  if (!out_score && !out_id) return fail(FMOE_ERR_INVALID_ARG, "no output");
+  const bool sem = w != 0.f, traj = w != 1.f;
+  if (sem && !q_emb) return fail(FMOE_ERR_INVALID_ARG, "null q_emb");
+  if (traj && (!q_prefix || ell < 1 || ell > st->cfg.L)) return fail(FMOE_ERR_INVALID_ARG, "need q_prefix and 1 <= ell <= L");
+  if (!(w >= 0.f && w <= 1.f)) return fail(FMOE_ERR_INVALID_ARG, "w_sem");
+  if (B == 0) return FMOE_OK;
+  DeviceGuard g(st->device);
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  Staging S(s, st->device);
+  const int E = st->cfg.E, D = st->cfg.D;
+  const float* dq = sem ? S.in(q_emb, size_t(B) * D) : nullptr;
+  const float* dp = traj ? S.in(q_prefix, size_t(B) * ell * E) : nullptr;
+  float* ds = S.out(out_score, size_t(B) * k);
+  int64_t* di = S.out(out_id, size_t(B) * k);
+  fmoe_status r = S.check();
+  if (r == FMOE_OK)
+    r = run_search(st, B, dq, dp, int64_t(ell) * E, traj ? ell : 0, w, k, st->n, uint32_t(st->cfg.id_offset), S, s,
+                   ds, di, nullptr, true);
+  return S.finish(r);
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* fmoe_status_string(fmoe_status s) {
+  switch (s) {
+    case FMOE_OK: return "ok";
+    case FMOE_ERR_INVALID_ARG: return "invalid argument";
+    case FMOE_ERR_SHAPE: return "unsupported shape";
+    case FMOE_ERR_OOM: return "out of device memory";
+    case FMOE_ERR_CUDA: return "CUDA error";
+    case FMOE_ERR_UNSUPPORTED: return "unsupported";
+  }
+  return "unknown status";
+}
+
+const char* fmoe_last_error(void) { return g_err.c_str(); }
+
+int64_t fmoe_kernel_launch_count(void) { return fmoe::launch_count(); }
+
+fmoe_status fmoe_store_create(const fmoe_store_config* cfg, int device, fmoe_store** out) {
+  if (!out) return fail(FMOE_ERR_INVALID_ARG, "null out");
+  *out = nullptr;
+  fmoe_status cs = check_cfg(cfg);
+  if (cs != FMOE_OK) return cs;
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || device < 0 || device >= ndev) {
+    cudaGetLastError();
+    return fail(FMOE_ERR_INVALID_ARG, "no such CUDA device");
+  }
+  DeviceGuard g(device);
+  fmoe_store* st = new fmoe_store();
+  st->cfg = *cfg;
+  st->device = device;
+  st->bf16 = cfg->dtype == FMOE_BF16;
+  st->esz = st->bf16 ? 2 : 4;
+  const int per16 = 16 / st->esz;
+  st->Dp = round_up(cfg->D, per16);
+  st->Ep = round_up(cfg->E, per16);
+  const size_t cap = size_t(cfg->capacity);
+  cudaError_t e;
+  if ((e = cudaMalloc(&st->emb, cap * st->Dp * st->esz)) != cudaSuccess ||
+      (e = cudaMalloc(&st->r_e, cap * 4)) != cudaSuccess ||
+      (e = cudaMalloc(&st->maps, cap * size_t(cfg->L) * st->Ep * st->esz)) != cudaSuccess ||
+      (e = cudaMalloc(&st->psq, cap * size_t(cfg->L) * 4)) != cudaSuccess) {
+    fmoe_store_destroy(st);
+    return cuda_fail(e, "cudaMalloc store tiles");
+  }
+  *out = st;
+  return FMOE_OK;
+}
+
+void fmoe_store_destroy(fmoe_store* st) {
+  if (!st) return;
+  DeviceGuard g(st->device);
+  cudaDeviceSynchronize();
+  cudaFree(st->emb);
+  cudaFree(st->r_e);
+  cudaFree(st->maps);
+  cudaFree(st->psq);
+  delete st;
+}
+
+fmoe_status fmoe_store_size(const fmoe_store* st, int64_t* out_n) {
+  if (!st || !out_n) return fail(FMOE_ERR_INVALID_ARG, "null argument");
+  *out_n = st->n;
+  return FMOE_OK;
+}
+
+fmoe_status fmoe_store_get_config(const fmoe_store* st, fmoe_store_config* out_cfg) {
+  if (!st || !out_cfg) return fail(FMOE_ERR_INVALID_ARG, "null argument");
+  *out_cfg = st->cfg;
+  return FMOE_OK;
+}
+
+fmoe_status fmoe_store_insert(fmoe_store* st, int64_t B, const float* emb, const float* maps, int64_t* out_slot,
+                              int64_t* out_replaced, void* stream) {
+  if (!st) return fail(FMOE_ERR_INVALID_ARG, "null store");
+  if (B < 0 || B > (int64_t(1) << 30)) return fail(FMOE_ERR_INVALID_ARG, "B");
+  if (B == 0) return FMOE_OK;
+  if (!emb || !maps) return fail(FMOE_ERR_INVALID_ARG, "null emb/maps");
+  const int64_t cap = st->cfg.capacity, n0 = st->n;
+  const int64_t a = B < cap - n0 ? B : cap - n0;   // appended rows
+  const int64_t nrep = B - a;                        // rows needing a victim
+  if (nrep > FMOE_MAX_K) return fail(FMOE_ERR_INVALID_ARG, "more than 64 rows of one insert need replacement");
+  const int L = st->cfg.L, E = st->cfg.E, D = st->cfg.D;
+  DeviceGuard g(st->device);
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  Staging S(s, st->device);
+  const float* de = S.in(emb, size_t(B) * D);
+  const float* dm = S.in(maps, size_t(B) * L * E);
+  int64_t* dslot = S.out(out_slot, size_t(B));
+  int64_t* drep = S.out(out_replaced, size_t(B));
+  int64_t* slots_all = nrep > 0 ? static_cast<int64_t*>(S.scratch(size_t(B) * 8)) : nullptr;
+  fmoe_status r = S.check();
+  const uint32_t off = uint32_t(st->cfg.id_offset);
+  if (r == FMOE_OK && nrep > 0) {
+    const int kk = int(nrep < n0 ? nrep : n0);
+    uint64_t* keys = static_cast<uint64_t*>(S.scratch(size_t(nrep) * (kk > 0 ? kk : 1) * 8));
+    r = S.check();
+    if (r == FMOE_OK && kk > 0) {
+      // RDY_{x,y} = d/L sem + (L-d)/L traj over full maps, against
+      // the contexts present before this call: rows [0, n0).
+      const float w = float(st->cfg.d) / float(L);
+      r = run_search(st, nrep, de + a * D, dm + a * int64_t(L) * E, int64_t(L) * E, L, w, kk, n0, 0u, S, s, nullptr,
+                     nullptr, keys, false);
+    }
+    if (r == FMOE_OK) {
+      cudaError_t e = launch_resolve(int(nrep), kk, keys, off, slots_all, int(a), n0, dslot, drep, s);
+      if (e != cudaSuccess) r = cuda_fail(e, "resolve launch");
+    }
+  } else if (r == FMOE_OK) {
+    cudaError_t e = launch_append_ids(int(a), n0, off, dslot, drep, s);
+    if (e != cudaSuccess) r = cuda_fail(e, "append ids launch");
+  }
+  if (r == FMOE_OK) {
+    WriteArgs w{};
+    w.emb = st->emb; w.r_e = st->r_e; w.maps = st->maps; w.psq = st->psq;
+    w.cap = cap; w.L = L; w.E = E; w.D = D; w.Dp = st->Dp; w.Ep = st->Ep; w.bf16 = st->bf16;
+    w.in_emb = de; w.in_maps = dm;
+    w.B = int(nrep > 0 ? B : a);
+    w.slots = slots_all;
+    w.first_slot = n0;
+    cudaError_t e = launch_write_rows(w, s);
+    if (e != cudaSuccess) r = cuda_fail(e, "write launch");
+  }
+  if (r == FMOE_OK) st->n = n0 + a;
+  return S.finish(r);
+}
+
+fmoe_status fmoe_store_read(const fmoe_store* st, int64_t slot_begin, int64_t count, float* out_emb, float* out_maps,
+                            void* stream) {
+  if (!st) return fail(FMOE_ERR_INVALID_ARG, "null store");
+  if (slot_begin < 0 || count < 0 || slot_begin + count > st->n) return fail(FMOE_ERR_INVALID_ARG, "slot range");
+  if (count == 0) return FMOE_OK;
+  DeviceGuard g(st->device);
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  Staging S(s, st->device);
+  float* de = S.out(out_emb, size_t(count) * st->cfg.D);
+  float* dm = S.out(out_maps, size_t(count) * st->cfg.L * st->cfg.E);
+  fmoe_status r = S.check();
+  if (r == FMOE_OK) {
+    cudaError_t e = launch_read_rows(st->view(), slot_begin, count, de, dm, s);
+    if (e != cudaSuccess) r = cuda_fail(e, "read launch");
+  }
+  return S.finish(r);
+}
+
+fmoe_status fmoe_search_semantic(const fmoe_store* st, int64_t B, const float* q_emb, int32_t k, float* out_score,
+                                 int64_t* out_id, void* stream) {
+  return search_common(st, B, q_emb, nullptr, 0, 1.f, k, out_score, out_id, stream);
+}
+
+fmoe_status fmoe_search_trajectory(const fmoe_store* st, int64_t B, const float* q_prefix, int32_t ell, int32_t k,
+                                   float* out_score, int64_t* out_id, void* stream) {
+  return search_common(st, B, nullptr, q_prefix, ell, 0.f, k, out_score, out_id, stream);
+}
+
+fmoe_status fmoe_search_blend(const fmoe_store* st, int64_t B, const float* q_emb, const float* q_prefix, int32_t ell,
+                              float w_sem, int32_t k, float* out_score, int64_t* out_id, void* stream) {
+  if (!st) return fail(FMOE_ERR_INVALID_ARG, "null store");
+  if (w_sem < 0.f) w_sem = float(st->cfg.d) / float(st->cfg.L);
+  return search_common(st, B, q_emb, q_prefix, ell, w_sem, k, out_score, out_id, stream);
+}
+
+fmoe_status fmoe_select_experts(const fmoe_store* st, int64_t B, const int64_t* map_id, const float* score, float delta,
+                                int32_t layer_begin, int32_t layer_end, uint64_t* out_mask, int32_t* out_count,
+                                void* stream) {
+  if (!st) return fail(FMOE_ERR_INVALID_ARG, "null store");
+  if (B < 0 || !map_id || !out_mask || !out_count) return fail(FMOE_ERR_INVALID_ARG, "null argument");
+  if (layer_begin < 0 || layer_begin >= layer_end || layer_end > st->cfg.L)
+    return fail(FMOE_ERR_INVALID_ARG, "need 0 <= layer_begin < layer_end <= L");
+  if (!(delta <= 1.f)) return fail(FMOE_ERR_INVALID_ARG, "delta must be <= 1 (negative = dynamic)");
+  if (delta < 0.f && !score) return fail(FMOE_ERR_INVALID_ARG, "dynamic delta needs score");
+  if (B == 0) return FMOE_OK;
+  const int T = layer_end - layer_begin;
+  DeviceGuard g(st->device);
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  Staging S(s, st->device);
+  const int64_t* did = S.in(map_id, size_t(B));
+  const float* dsc = delta < 0.f ? S.in(score, size_t(B)) : nullptr;
+  uint64_t* dm = S.out(out_mask, size_t(B) * T);
+  int32_t* dc = S.out(out_count, size_t(B) * T);
+  fmoe_status r = S.check();
+  if (r == FMOE_OK) {
+    cudaError_t e = launch_select(st->view(), int(B), did, dsc, delta, st->cfg.K, layer_begin, layer_end,
+                                  st->cfg.id_offset, st->n, dm, dc, s);
+    if (e != cudaSuccess) r = cuda_fail(e, "select launch");
+  }
+  return S.finish(r);
+}
+
+fmoe_status fmoe_topk_merge(int64_t B, int32_t n_lists, int32_t k_in, const float* scores, const int64_t* ids,
+                            int32_t k, float* out_score, int64_t* out_id, int device, void* stream) {
+  if (B < 0 || n_lists < 0 || k_in < 1 || k_in > FMOE_MAX_K || k < 1 || k > FMOE_MAX_K)
+    return fail(FMOE_ERR_INVALID_ARG, "sizes");
+  if ((n_lists > 0 && (!scores || !ids)) || !out_score || !out_id) return fail(FMOE_ERR_INVALID_ARG, "null argument");
+  if (B == 0) return FMOE_OK;
+  DeviceGuard g(device);
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  Staging S(s, device);
+  const size_t nin = size_t(n_lists) * B * k_in;
+  const float* dsc = S.in(scores, nin);
+  const int64_t* did = S.in(ids, nin);
+  float* ds = S.out(out_score, size_t(B) * k);
+  int64_t* di = S.out(out_id, size_t(B) * k);
+  fmoe_status r = S.check();
+  if (r == FMOE_OK) {
+    cudaError_t e = launch_merge_lists(int(B), n_lists, k_in, dsc, did, k, ds, di, s);
+    if (e != cudaSuccess) r = cuda_fail(e, "merge launch");
+  }
+  return S.finish(r);
+}
+
+}  // extern "C"

@@ -1,0 +1,260 @@
+"""GPU parity: the CUDA path through the C ABI vs the fp64 CPU oracle.
+
+Both sides get the same seeded fp32 inputs (fmoe_synth).  The oracle is fed the
+values the store holds -- inputs rounded to the store dtype with RNE
+(``O.quantize``, the "O-store" view of SURVEY §8(c) c8) -- and the comparison
+rules are DESIGN.md §"Parity contract":
+  * scores: |gpu - oracle| <= 1e-5 (absolute; |score| <= 1);
+  * ids: exact at every rank whose oracle score is separated from its
+    neighbours by more than 1e-5; elsewhere the returned id's oracle score
+    must be within 1e-5 of the oracle score at that rank;
+  * expert sets / counts / insert slots: bit-exact given the same (id, score).
+Sizes span many 32-row tiles, several blocks and a ragged tail.
+"""
+import numpy as np
+import pytest
+import torch
+
+import fmoe_synth as S
+from oracle import fmoe_oracle as O
+
+pytestmark = pytest.mark.gpu
+TOL = 1e-5
+
+SHAPES = {
+    "mixtral_tiny": S.Shape("mixtral-tiny", 32, 8, 2, 64, n_clusters=16),
+    "qwen_small": S.Shape("qwen-small", 24, 60, 4, 256, n_clusters=32),
+    "phi_small": S.Shape("phi-small", 32, 16, 2, 520, n_clusters=32),   # D not a multiple of 16 B
+}
+
+
+def make(lib, shape, N, dtype, cap=None, seed=1):
+    emb, maps, _ = S.store_rows(shape, seed, 0, N)
+    st = lib.ExpertMapStore(shape.L, shape.E, shape.K, shape.D, 3, cap or N, dtype)
+    for a in range(0, N, 4096):
+        st.insert(emb[a:a + 4096].cuda(), maps[a:a + 4096].cuda())
+    torch.cuda.synchronize()
+    return st, emb.numpy(), maps.numpy()
+
+
+def check_topk(gs, gi, ref, k, tol=TOL):
+    """ref: oracle B x N score matrix (O-store view)."""
+    gs = gs.cpu().numpy().astype(np.float64)
+    gi = gi.cpu().numpy()
+    rs, ri = O.topk(ref, k)
+    B = ref.shape[0]
+    for x in range(B):
+        if np.isnan(ref[x]).any():
+            assert np.isnan(gs[x]).all() and (gi[x] == -1).all()
+            continue
+        valid = ri[x] >= 0
+        assert np.array_equal(gi[x][~valid], ri[x][~valid])
+        assert np.all(np.isneginf(gs[x][~valid]))
+        assert np.all(np.abs(gs[x][valid] - rs[x][valid]) <= tol), (x, gs[x], rs[x])
+        ids = gi[x][valid]
+        assert len(set(ids.tolist())) == len(ids)
+        nv = int(valid.sum())
+        full = np.sort(ref[x])[::-1]          # all oracle scores, descending
+        for r in range(nv):
+            lo = full[r - 1] - full[r] if r > 0 else np.inf
+            hi = full[r] - full[r + 1] if r + 1 < full.shape[0] else np.inf
+            if min(lo, hi) > tol:
+                assert gi[x, r] == ri[x, r], (x, r, gi[x], ri[x])
+            else:
+                assert abs(ref[x, gi[x, r]] - rs[x, r]) <= tol
+
+
+@pytest.fixture(scope="module", params=[("mixtral_tiny", "f32"), ("mixtral_tiny", "bf16"), ("qwen_small", "bf16"),
+                                        ("qwen_small", "f32"), ("phi_small", "bf16")])
+def setup(request, lib):
+    name, dtype = request.param
+    shape = SHAPES[name]
+    N = 3001
+    st, emb, maps = make(lib, shape, N, dtype)
+    q_emb, q_maps, planted = S.queries(shape, 1, N, 6)   # seed of make()
+    Qe = O.quantize(emb, dtype)
+    Qm = O.quantize(maps, dtype)
+    yield dict(lib=lib, st=st, shape=shape, dtype=dtype, N=N, emb=emb, maps=maps, Qe=Qe, Qm=Qm,
+               q_emb=q_emb, q_maps=q_maps, planted=planted.numpy())
+    st.close()
+
+
+def test_store_holds_the_quantised_rows(setup):
+    e, m = setup["st"].read(0, 257)
+    assert np.array_equal(e.cpu().numpy().astype(np.float64), setup["Qe"][:257])
+    assert np.array_equal(m.cpu().numpy().astype(np.float64), setup["Qm"][:257])
+
+
+@pytest.mark.parametrize("B,k", [(1, 1), (3, 8), (6, 40)])
+def test_semantic(setup, B, k):
+    st, dt = setup["st"], setup["dtype"]
+    q = setup["q_emb"][:B]
+    gs, gi = st.search_semantic(q.cuda(), k)
+    ref = O.semantic_scores(O.quantize(q.numpy(), dt), setup["Qe"])
+    check_topk(gs, gi, ref, k)
+    # O-def view: within the bf16 contract of the unrounded definition
+    if dt == "bf16":
+        ref_def = O.semantic_scores(q.numpy(), setup["emb"])
+        rs, _ = O.topk(ref_def, k)
+        assert np.all(np.abs(gs.cpu().numpy() - rs) <= 2e-3)
+    pl = setup["planted"][:B]
+    for x in range(B):
+        if pl[x] >= 0:
+            assert gi[x, 0].item() == pl[x]
+
+
+@pytest.mark.parametrize("ell", [1, 2, 7, "L"])
+@pytest.mark.parametrize("B,k", [(1, 1), (4, 8), (5, 33)])
+def test_trajectory(setup, ell, B, k):
+    st, dt, sh = setup["st"], setup["dtype"], setup["shape"]
+    ell = sh.L if ell == "L" else ell
+    qp = setup["q_maps"][:B, :ell].contiguous()
+    gs, gi = st.search_trajectory(qp.cuda(), ell, k)
+    ref = O.trajectory_scores(O.quantize(qp.numpy(), dt), setup["Qm"], ell)
+    check_topk(gs, gi, ref, k)
+
+
+@pytest.mark.parametrize("w", [-1.0, 0.3])
+@pytest.mark.parametrize("B,ell", [(1, 5), (6, 31)])
+def test_blend(setup, w, B, ell):
+    st, dt, sh = setup["st"], setup["dtype"], setup["shape"]
+    ell = min(ell, sh.L)
+    w_eff = 3 / sh.L if w < 0 else w
+    qe, qp = setup["q_emb"][:B], setup["q_maps"][:B, :ell].contiguous()
+    gs, gi = st.search_blend(qe.cuda(), qp.cuda(), ell, w, 8)
+    sem = O.semantic_scores(O.quantize(qe.numpy(), dt), setup["Qe"])
+    trj = O.trajectory_scores(O.quantize(qp.numpy(), dt), setup["Qm"], ell)
+    check_topk(gs, gi, O.blend_scores(sem, trj, np.float64(np.float32(w_eff))), 8)
+
+
+def test_select_bit_exact(setup):
+    st, sh = setup["st"], setup["shape"]
+    rng = np.random.default_rng(7)
+    B = 300
+    ids = rng.integers(-1, setup["N"], B)
+    sc = rng.uniform(-1.2, 1.2, B).astype(np.float32)
+    sc[:5] = [1.0, -1.0, 0.0, np.nan, 0.7]
+    for delta in (-1.0, 0.9, 0.0, 1.0):
+        mask, cnt = st.select_experts(torch.from_numpy(ids).cuda(), torch.from_numpy(sc).cuda(), delta, 0, sh.L)
+        d32 = float(np.float32(delta))
+        om, oc = O.select_experts(setup["Qm"], ids.tolist(), sc.astype(np.float64).tolist(), d32,
+                                  list(range(sh.L)), sh.K)
+        gm = mask.cpu().numpy().view(np.uint64)
+        assert np.array_equal(gm, np.array(om, dtype=np.uint64)), delta
+        assert np.array_equal(cnt.cpu().numpy(), np.array(oc))
+
+
+def test_search_then_select_pipeline(setup):
+    """a6 -> a7: the matched map's first d layers (semantic path)."""
+    st, sh, dt = setup["st"], setup["shape"], setup["dtype"]
+    q = setup["q_emb"][:4].cuda()
+    gs, gi = st.search_semantic(q, 1)
+    mask, cnt = st.select_experts(gi[:, 0].contiguous(), gs[:, 0].contiguous(), -1.0, 0, 3)
+    om, oc = O.select_experts(setup["Qm"], gi[:, 0].cpu().tolist(), gs[:, 0].cpu().double().tolist(), -1.0,
+                              [0, 1, 2], sh.K)
+    assert np.array_equal(mask.cpu().numpy().view(np.uint64), np.array(om, dtype=np.uint64))
+
+
+def test_host_pointer_path(setup):
+    """Same call with CPU (host) tensors: staged + synchronised by the library."""
+    lib, st = setup["lib"], setup["st"]
+    q = setup["q_emb"][:3].contiguous()
+    s_h = torch.empty(3, 4)
+    i_h = torch.empty(3, 4, dtype=torch.int64)
+    lib.fmoe_search_semantic(st._h, q, 4, s_h, i_h)
+    s_d, i_d = st.search_semantic(q.cuda(), 4)
+    assert torch.equal(s_h, s_d.cpu()) and torch.equal(i_h, i_d.cpu())
+
+
+# ---------------------------------------------------------------- edge cases
+def test_edge_cases(lib):
+    sh = SHAPES["mixtral_tiny"]
+    st = lib.ExpertMapStore(sh.L, sh.E, sh.K, sh.D, 3, 50, "bf16")
+    q = torch.randn(2, sh.D, device="cuda")
+    s, i = st.search_semantic(q, 3)                     # empty store
+    assert (i == -1).all() and torch.isneginf(s).all()
+    emb, maps, _ = S.store_rows(sh, 3, 0, 5)
+    st.insert(emb.cuda(), maps.cuda())
+    s, i = st.search_semantic(q, 8)                     # k > |store|
+    assert (i[:, 5:] == -1).all() and torch.isneginf(s[:, 5:]).all() and (i[:, :5] >= 0).all()
+    q[1] = 0                                            # zero-norm query -> NaN, -1
+    s, i = st.search_semantic(q, 2)
+    assert torch.isnan(s[1]).all() and (i[1] == -1).all() and (i[0] >= 0).all()
+    # exact duplicate rows: bit-identical scores, the lowest id wins
+    dup_e = emb[2:3].repeat(3, 1) * torch.tensor([[1.0], [2.0], [0.5]])
+    dup_m = maps[2:3].repeat(3, 1, 1)
+    st.insert(dup_e.cuda(), dup_m.cuda())               # slots 5, 6, 7
+    s, i = st.search_semantic(emb[2:3].cuda(), 4)
+    assert i[0].tolist() == [2, 5, 6, 7]
+    s, i = st.search_trajectory(maps[2:3].cuda(), sh.L, 4)
+    assert i[0].tolist() == [2, 5, 6, 7] and abs(s[0, 0].item() - 1.0) < 1e-6
+    # argument errors are synchronous and typed
+    with pytest.raises(lib.FmoeError):
+        st.search_semantic(q, 65)
+    with pytest.raises(lib.FmoeError):
+        st.search_trajectory(maps[:1].cuda(), 0, 1)
+    with pytest.raises(lib.FmoeError):
+        st.select_experts(i[:, 0].contiguous(), s[:, 0].contiguous(), -1.0, 3, 3)
+    st.close()
+
+
+# ---------------------------------------------------------------- insert / dedup (a8)
+@pytest.mark.parametrize("dtype", ["f32", "bf16"])
+def test_insert_matches_oracle_store(lib, dtype):
+    sh = S.Shape("mix", 8, 8, 2, 48, n_clusters=4)
+    C = 700
+    emb, maps, _ = S.store_rows(sh, 11, 0, C + 400)
+    st = lib.ExpertMapStore(sh.L, sh.E, sh.K, sh.D, 3, C, dtype)
+    ref = O.Store(C, sh.L, sh.E, sh.D, 3)
+    Qe, Qm = O.quantize(emb.numpy(), dtype), O.quantize(maps.numpy(), dtype)
+    pos = 0
+    for B in (600, 64, 40, 1, 7, 33, 64):   # append, mixed batch (100 + ...), then replacements
+        e, m = emb[pos:pos + B], maps[pos:pos + B]
+        slot, rep = st.insert(e.cuda(), m.cuda())
+        rs, rr = ref.insert(Qe[pos:pos + B], Qm[pos:pos + B])
+        assert slot.cpu().tolist() == rs, (B, pos)
+        assert rep.cpu().tolist() == rr
+        pos += B
+        if pos + 64 > emb.shape[0]:
+            break
+    assert len(st) == ref.n == C
+    ge, gm = st.read(0, C)
+    assert np.array_equal(ge.cpu().numpy().astype(np.float64), ref.emb)
+    assert np.array_equal(gm.cpu().numpy().astype(np.float64), ref.maps)
+    st.close()
+
+
+def test_insert_duplicate_batch_distinct_victims(lib):
+    sh = S.Shape("mix", 8, 8, 2, 48, n_clusters=4)
+    emb, maps, _ = S.store_rows(sh, 12, 0, 100)
+    st = lib.ExpertMapStore(sh.L, sh.E, sh.K, sh.D, 3, 100, "bf16")
+    st.insert(emb.cuda(), maps.cuda())
+    # 5 identical copies of row 17: first replaces 17 (RDY=1), the rest take distinct next-best victims
+    slot, rep = st.insert(emb[17:18].repeat(5, 1).cuda(), maps[17:18].repeat(5, 1, 1).cuda())
+    s = slot.cpu().tolist()
+    assert s[0] == 17 and len(set(s)) == 5 and rep.cpu().tolist() == s
+    ref = O.Store(100, sh.L, sh.E, sh.D, 3)
+    ref.insert(O.quantize(emb.numpy(), "bf16"), O.quantize(maps.numpy(), "bf16"))
+    rs, _ = ref.insert(O.quantize(emb[17:18].repeat(5, 1).numpy(), "bf16"),
+                       O.quantize(maps[17:18].repeat(5, 1, 1).numpy(), "bf16"))
+    assert s == rs
+    with pytest.raises(lib.FmoeError):                  # > 64 replacements in one call
+        st.insert(emb[:65].cuda(), maps[:65].cuda())
+    st.close()
+
+
+def test_topk_merge_api(lib):
+    rng = np.random.default_rng(3)
+    G, B, kin, k = 4, 5, 8, 8
+    sc = np.round(rng.standard_normal((G, B, kin)), 2).astype(np.float32)
+    ids = rng.permutation(G * B * kin).reshape(G, B, kin).astype(np.int64)
+    ids[1, 2, 5:] = -1
+    sc[3, 4, 0] = np.nan
+    out_s = torch.empty(B, k, device="cuda")
+    out_i = torch.empty(B, k, dtype=torch.int64, device="cuda")
+    lib.fmoe_topk_merge(torch.from_numpy(sc).cuda(), torch.from_numpy(ids).cuda(), k, out_s, out_i)
+    ms, mi = O.merge_topk([sc[g].astype(np.float64) for g in range(G)], [ids[g] for g in range(G)], k)
+    valid = ~np.isnan(ms[:, 0])
+    assert np.array_equal(out_i.cpu().numpy()[valid], mi[valid])
+    assert np.array_equal(out_s.cpu().numpy()[valid], ms[valid].astype(np.float32))
+    assert (out_i.cpu().numpy()[~valid] == -1).all()
