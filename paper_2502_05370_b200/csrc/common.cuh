@@ -119,6 +119,29 @@ struct WarpTopK {
   }
 };
 
+// k == 1 specialisation: each lane keeps its own best key (one max per row,
+// no warp traffic); the warp maximum is formed only when read.
+template <>
+struct WarpTopK<0> {
+  uint64_t v[1];
+  __device__ __forceinline__ void init() { v[0] = 0ull; }
+  __device__ __forceinline__ void offer(uint64_t key, int) { v[0] = key > v[0] ? key : v[0]; }
+  __device__ __forceinline__ uint64_t get(int) const {
+    uint64_t m = v[0];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const uint64_t x = shfl_u64(m, (threadIdx.x & 31) ^ o);
+      m = x > m ? x : m;
+    }
+    return m;
+  }
+  __device__ __forceinline__ uint64_t kth(int) const { return get(0); }
+  __device__ __forceinline__ void store(uint64_t* dst, int) const {
+    const uint64_t m = get(0);
+    if ((threadIdx.x & 31) == 0) dst[0] = m;
+  }
+};
+
 // ---------------------------------------------------------------- bf16 / 16-byte chunks
 __device__ __forceinline__ void unpack8(const uint4& u, float (&f)[8], Bf16Tag) {
   f[0] = __uint_as_float(u.x << 16); f[1] = __uint_as_float(u.x & 0xffff0000u);
@@ -150,5 +173,70 @@ __device__ __forceinline__ float to_store_value(float x, Bf16Tag) {
   return __bfloat162float(__float2bfloat16_rn(x));
 }
 __device__ __forceinline__ float to_store_value(float x, F32Tag) { return x; }
+
+// ---------------------------------------------------------------- mbarrier + bulk async copy (TMA engine)
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_fence_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra WAIT_%=;\n}" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+// global -> shared bulk copy (TMA, non-tensor), completion counted on `bar`.
+// bytes and both addresses must be multiples of 16.
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, uint64_t* bar,
+                                         uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(policy)
+      : "memory");
+}
+__device__ __forceinline__ uint64_t policy_evict_first() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+
+// ---------------------------------------------------------------- device phase tracer
+// When a trace buffer is passed (fmoe_debug_trace, a debug entry point),
+// thread 0 of every block records %globaltimer at phase boundaries:
+// trace[block][phase].  Attributes a scan's time to launch, staging,
+// streaming and the merge tail.
+constexpr int kTraceBlocks = 4096;
+constexpr int kTracePhases = 8;
+__device__ __forceinline__ unsigned long long globaltimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+__device__ __forceinline__ void trace_mark(unsigned long long* trace, int phase) {
+  if (trace && threadIdx.x == 0 && blockIdx.x < kTraceBlocks)
+    trace[blockIdx.x * kTracePhases + phase] = globaltimer();
+}
+
+// ---------------------------------------------------------------- programmatic dependent launch
+// Every kernel of this library waits for the preceding grid on the stream
+// before touching global memory it may depend on, and lets the next grid
+// launch once its main loop is done (PDL, sm_90+).
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 
 }  // namespace fmoe

@@ -2,8 +2,28 @@
 #pragma once
 #include <cstdint>
 #include <cuda_runtime.h>
+#include <utility>
 
 namespace fmoe {
+
+// Launch with programmatic stream serialization (PDL): the grid may start
+// while the previous grid on the stream drains; kernels call pdl_wait()
+// before reading dependent memory.
+template <class... KArgs, class... Args>
+inline cudaError_t launch_pdl(void (*k)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+                              Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, k, std::forward<Args>(args)...);
+}
 
 // Device view of a store's HBM tiles.
 struct StoreView {
@@ -30,18 +50,33 @@ struct ScanArgs {
   uint32_t id_offset;        // global id of row 0
   uint64_t* cand;            // [B][grid][k] per-block candidate keys
   int grid;                  // blocks of the launch (cand stride)
-  float* qinfo;              // [B] 1 if the query is valid (non-zero norms), else 0
+  unsigned* counter;         // zeroed ticket counter of this pass (last block merges)
+  // outputs of the fused grid merge (queries q0..q0+nq): either (score, id) or raw keys
+  float* out_score;          // [B][k]
+  int64_t* out_id;           // [B][k]
+  uint64_t* out_keys;        // [B][k]
+  int check_valid;           // 1: zero-norm query -> (NaN, -1)
+  unsigned long long* trace; // debug phase tracer [kTraceBlocks][8] or null
+  unsigned long long* best;  // [B] zeroed keys for the k == 1 merge (reset by the last block)
 };
 
+// debug tracer buffer (null unless fmoe_debug_trace enabled it)
+unsigned long long* trace_buffer();
+
 // GEMV scan (B <= 4 per pass): bandwidth-bound warp-per-32-rows streaming.
-cudaError_t launch_scan_gemv(const ScanArgs& a, cudaStream_t s, int* grid_out);
+cudaError_t launch_scan_gemv(const ScanArgs& a, cudaStream_t s);
 int scan_gemv_grid(const ScanArgs& a);
 
-// Merge per-block candidate keys -> per-query top-k.
-//  keys [B][n_lists][k_in]; writes either (out_score,out_id) or out_keys [B][k].
+// Trajectory-only scan fed by a TMA bulk-copy ring (one CTA per SM).
+bool scan_tma_supported(const ScanArgs& a);
+int scan_tma_grid(const ScanArgs& a);
+cudaError_t launch_scan_tma(const ScanArgs& a, cudaStream_t s);
+
+// Merge per-list candidate keys -> per-query top-k (also fills an empty
+// result when n_lists == 0).  keys [B][n_lists][k_in]; writes (out_score,
+// out_id) and/or out_keys [B][k].
 cudaError_t launch_merge_keys(int B, int n_lists, int k_in, const uint64_t* keys, int k,
-                              const float* qinfo, float* out_score, int64_t* out_id,
-                              uint64_t* out_keys, cudaStream_t s);
+                              float* out_score, int64_t* out_id, uint64_t* out_keys, cudaStream_t s);
 // Merge (score, id) lists from an all-gather: [n_lists][B][k_in].
 cudaError_t launch_merge_lists(int B, int n_lists, int k_in, const float* scores,
                                const int64_t* ids, int k, float* out_score, int64_t* out_id,

@@ -19,8 +19,11 @@
 // warp's register-resident top-k lists (WarpTopK).  Queries are staged once
 // per block in shared memory as fp32 values of the store dtype.
 #include <cstdio>
+#include <mutex>
+#include <map>
 #include "common.cuh"
 #include "kernels.cuh"
+#include "merge.cuh"
 
 namespace fmoe {
 
@@ -53,14 +56,23 @@ __device__ __forceinline__ double warp_sum_d(double v) {
   return v;
 }
 
-template <class Tag, int NQ, int KPL, bool SEM, bool TRAJ>
-__global__ void __launch_bounds__(kScanThreads) scan_gemv_kernel(const ScanArgs a) {
+// TPI >= 1 (trajectory-only, 16-byte map rows): a warp streams TPI
+// consecutive 32-row tiles per iteration, LB = 16/TPI layers per load batch,
+// so each lane keeps 16 16-byte loads in flight at every prefix length (the
+// 8-deep generic path was latency-bound below ell ~ 16).  TPI = 0: generic.
+// Occupancy: the generic path needs >= 3 CTAs (24 warps) per SM to cover HBM
+// latency with 8 loads per lane; the multi-tile path keeps 16 loads per lane
+// and runs at 2 CTAs per SM.
+template <class Tag, int NQ, int KPL, bool SEM, bool TRAJ, int TPI>
+__global__ void __launch_bounds__(kScanThreads, TPI >= 1 ? 2 : 3) scan_gemv_kernel(const ScanArgs a) {
   using ST = StoreT<Tag>;
   constexpr int EP = ST::kElemsPer16B;
   constexpr int SB = ST::kBytes;
   extern __shared__ __align__(16) float smem[];
   __shared__ double red[kScanWarps][2 * NQ];
   __shared__ float rq[2][NQ];
+  __shared__ int s_valid[NQ];
+  __shared__ int s_last;
 
   const StoreView& st = a.st;
   const int Dp = st.Dp, Ep = st.Ep, E = st.E, D = st.D, ell = a.ell;
@@ -68,6 +80,9 @@ __global__ void __launch_bounds__(kScanThreads) scan_gemv_kernel(const ScanArgs 
   float* qsem = smem;                              // [NQ][Dp]
   float* qtraj = smem + (SEM ? NQ * Dp : 0);       // [NQ][ell][Ep]
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  trace_mark(a.trace, 0);
+  pdl_wait();
+  trace_mark(a.trace, 1);
 
   // ---- 1. stage the queries (quantised to the store dtype) + their norms
   double part[2 * NQ];
@@ -105,11 +120,11 @@ __global__ void __launch_bounds__(kScanThreads) scan_gemv_kernel(const ScanArgs 
     for (int w = 0; w < kScanWarps; ++w) { s0 += red[w][tid]; s1 += red[w][NQ + tid]; }
     rq[0][tid] = s0 > 0.0 ? float(1.0 / sqrt(s0)) : 0.f;
     rq[1][tid] = s1 > 0.0 ? float(1.0 / sqrt(s1)) : 0.f;
-    if (blockIdx.x == 0 && tid < a.nq && a.qinfo)
-      a.qinfo[a.q0 + tid] = ((!SEM || s0 > 0.0) && (!TRAJ || s1 > 0.0)) ? 1.f : 0.f;
+    s_valid[tid] = (!SEM || s0 > 0.0) && (!TRAJ || s1 > 0.0);
   }
   __syncthreads();
 
+  trace_mark(a.trace, 2);
   float rq0[NQ], rq1[NQ];
 #pragma unroll
   for (int q = 0; q < NQ; ++q) { rq0[q] = rq[0][q]; rq1[q] = rq[1][q]; }
@@ -119,9 +134,22 @@ __global__ void __launch_bounds__(kScanThreads) scan_gemv_kernel(const ScanArgs 
 #pragma unroll
   for (int q = 0; q < NQ; ++q) lists[q].init();
 
-  const int64_t n_rows = a.n_rows;
-  const int64_t ntiles = (n_rows + 31) / 32;
-  const int64_t wstride = int64_t(gridDim.x) * kScanWarps;
+  // Work partition: tiles of TS rows dealt round-robin over the nw warps
+  // (neighbouring warps stream neighbouring rows: DRAM-page friendly), and the
+  // rows left after the last full round split evenly into one partial tile per
+  // warp, so per-warp work differs by at most one row (plain round-robin left a
+  // 5-13% tail whenever the tile count was not a multiple of nw).
+  const int64_t nw = int64_t(gridDim.x) * kScanWarps;
+  const int64_t wg = int64_t(blockIdx.x) * kScanWarps + warp;
+  const int64_t TS = TPI >= 1 ? 32 * TPI : 32;
+  const int64_t full_rounds = a.n_rows / (nw * TS);
+  const int64_t rem_base = full_rounds * nw * TS, rem = a.n_rows - rem_base;
+  auto tile_of = [&](int64_t r, int64_t& y0, int64_t& y1) -> bool {
+    if (r < full_rounds) { y0 = (r * nw + wg) * TS; y1 = y0 + TS; return true; }
+    y0 = rem_base + rem * wg / nw;
+    y1 = rem_base + rem * (wg + 1) / nw;
+    return r == full_rounds && y0 < y1;
+  };
   const int CPR = Dp / EP;          // 16-byte chunks per embedding row
   const int GS = group_size(CPR);
   const int rpp = 32 / GS, sg = lane / GS, sgl = lane % GS;
@@ -134,8 +162,68 @@ __global__ void __launch_bounds__(kScanThreads) scan_gemv_kernel(const ScanArgs 
   const int64_t slab = st.cap * int64_t(Ep) * SB;
   const float w = a.w_sem, w1 = 1.f - a.w_sem;
 
-  for (int64_t t = int64_t(blockIdx.x) * kScanWarps + warp; t < ntiles; t += wstride) {
-    const int64_t y0 = t * 32;
+  if constexpr (TPI >= 1) {
+    // ---- 2a. trajectory-only, one 16-byte chunk per row-layer (GT == 1)
+    constexpr int LB = 16 / TPI;
+    int64_t y0, n_rows;
+    for (int64_t rr = 0; tile_of(rr, y0, n_rows); ++rr) {
+      float acc[TPI][NQ], sq[TPI];
+#pragma unroll
+      for (int i = 0; i < TPI; ++i) {
+        sq[i] = 0.f;
+#pragma unroll
+        for (int q = 0; q < NQ; ++q) acc[i][q] = 0.f;
+      }
+      for (int l0 = 0; l0 < ell; l0 += LB) {
+        uint4 buf[TPI][LB];
+#pragma unroll
+        for (int i = 0; i < TPI; ++i)
+#pragma unroll
+          for (int u = 0; u < LB; ++u) {
+            const int64_t row = y0 + i * 32 + lane;
+            buf[i][u] = (row < n_rows && l0 + u < ell) ? ld_stream(mapp + row * 16 + int64_t(l0 + u) * slab)
+                                                       : make_uint4(0u, 0u, 0u, 0u);
+          }
+#pragma unroll
+        for (int u = 0; u < LB; ++u) {
+          if (l0 + u < ell) {
+#pragma unroll
+            for (int i = 0; i < TPI; ++i) {
+              float x[8];
+              unpack_chunk<Tag>(buf[i][u], x);
+#pragma unroll
+              for (int e = 0; e < EP; ++e) sq[i] = fmaf(x[e], x[e], sq[i]);
+#pragma unroll
+              for (int q = 0; q < NQ; ++q) {
+                const float4* qp = reinterpret_cast<const float4*>(qtraj + q * tl + (l0 + u) * Ep);
+#pragma unroll
+                for (int e4 = 0; e4 < EP / 4; ++e4) {
+                  const float4 qv = qp[e4];
+                  acc[i][q] = fmaf(x[4 * e4 + 0], qv.x, acc[i][q]);
+                  acc[i][q] = fmaf(x[4 * e4 + 1], qv.y, acc[i][q]);
+                  acc[i][q] = fmaf(x[4 * e4 + 2], qv.z, acc[i][q]);
+                  acc[i][q] = fmaf(x[4 * e4 + 3], qv.w, acc[i][q]);
+                }
+              }
+            }
+          }
+        }
+      }
+#pragma unroll
+      for (int i = 0; i < TPI; ++i) {
+        const int64_t y = y0 + i * 32 + lane;
+        const bool ok = y < n_rows;
+        const float rm = sq[i] > 0.f ? rsqrtf(sq[i]) : 0.f;
+#pragma unroll
+        for (int q = 0; q < NQ; ++q) {
+          const float sc = fmaf(w1, acc[i][q] * rq1[q] * rm, 0.f);
+          lists[q].offer(ok ? pack_key(sc, a.id_offset + uint32_t(y)) : 0ull, a.k);
+        }
+      }
+    }
+  } else {
+  int64_t y0, n_rows;
+  for (int64_t rr = 0; tile_of(rr, y0, n_rows); ++rr) {
     float sem[NQ], trj[NQ], msq = 0.f;
 #pragma unroll
     for (int q = 0; q < NQ; ++q) { sem[q] = 0.f; trj[q] = 0.f; }
@@ -241,7 +329,7 @@ __global__ void __launch_bounds__(kScanThreads) scan_gemv_kernel(const ScanArgs 
     const int64_t y = y0 + lane;
     const bool ok = y < n_rows;
     const float re = (SEM && ok) ? st.r_e[y] : 0.f;
-    const float rm = (TRAJ && msq > 0.f) ? 1.f / sqrtf(msq) : 0.f;
+    const float rm = (TRAJ && msq > 0.f) ? rsqrtf(msq) : 0.f;
 #pragma unroll
     for (int q = 0; q < NQ; ++q) {
       float s = 0.f;
@@ -251,43 +339,48 @@ __global__ void __launch_bounds__(kScanThreads) scan_gemv_kernel(const ScanArgs 
       lists[q].offer(key, a.k);
     }
   }
+  }  // generic path
 
-  // ---- 3. block merge of the warps' lists, one warp per query
-  __syncthreads();
-  uint64_t* sk = reinterpret_cast<uint64_t*>(smem);  // [kScanWarps][NQ][k]
-  const int k = a.k;
-#pragma unroll
-  for (int q = 0; q < NQ; ++q) lists[q].store(sk + (warp * NQ + q) * k, k);
-  __syncthreads();
-  if (warp < a.nq) {
-    const int q = warp;
-    WarpTopK<KPL> m;
-#pragma unroll
-    for (int s = 0; s < KPL; ++s) {
-      const int j = s * 32 + lane;
-      m.v[s] = j < k ? sk[q * k + j] : 0ull;
-    }
-    for (int w2 = 1; w2 < kScanWarps; ++w2)
-      for (int j0 = 0; j0 < k; j0 += 32) {
-        const uint64_t key = (j0 + lane < k) ? sk[(w2 * NQ + q) * k + j0 + lane] : 0ull;
-        m.offer(key, k);
-      }
-    m.store(a.cand + (int64_t(a.q0 + q) * a.grid + blockIdx.x) * k, k);
-  }
+  // ---- 3. block merge + grid merge (last block)
+  trace_mark(a.trace, 3);
+  pdl_trigger();
+  finish_topk<NQ, KPL, kScanWarps>(lists, reinterpret_cast<uint64_t*>(smem), a, s_valid, &s_last);
 }
 
 // ------------------------------------------------------------------ host side
 using KernelFn = void (*)(const ScanArgs);
 
+// multi-tile trajectory path: trajectory-only, one 16-byte chunk per
+// row-layer; TPI*LB = 16 loads in flight per lane, TPI capped by registers.
+static int traj_tpi(const ScanArgs& a) {
+  const int esz = a.st.bf16 ? 2 : 4;
+  if (a.w_sem != 0.f || a.st.Ep * esz != 16) return 0;
+  const int cap = a.nq <= 1 ? 16 : (a.nq <= 2 ? 8 : 4);
+  int tpi = 1;
+  while (tpi * 2 <= cap && tpi * 2 * a.ell <= 16) tpi *= 2;
+  return tpi;
+}
+
 template <class Tag, int NQ, int KPL>
-static KernelFn pick_mode(float w) {
-  if (w == 1.f) return scan_gemv_kernel<Tag, NQ, KPL, true, false>;
-  if (w == 0.f) return scan_gemv_kernel<Tag, NQ, KPL, false, true>;
-  return scan_gemv_kernel<Tag, NQ, KPL, true, true>;
+static KernelFn pick_mode(const ScanArgs& a) {
+  if (a.w_sem == 1.f) return scan_gemv_kernel<Tag, NQ, KPL, true, false, 0>;
+  if (a.w_sem == 0.f) {
+    switch (traj_tpi(a)) {
+      case 16: if constexpr (NQ == 1) return scan_gemv_kernel<Tag, NQ, KPL, false, true, 16>; break;
+      case 8: if constexpr (NQ <= 2) return scan_gemv_kernel<Tag, NQ, KPL, false, true, 8>; break;
+      case 4: return scan_gemv_kernel<Tag, NQ, KPL, false, true, 4>;
+      case 2: return scan_gemv_kernel<Tag, NQ, KPL, false, true, 2>;
+      case 1: return scan_gemv_kernel<Tag, NQ, KPL, false, true, 1>;
+      default: break;
+    }
+    return scan_gemv_kernel<Tag, NQ, KPL, false, true, 0>;
+  }
+  return scan_gemv_kernel<Tag, NQ, KPL, true, true, 0>;
 }
 template <class Tag, int NQ>
 static KernelFn pick_kpl(const ScanArgs& a) {
-  return a.k <= 32 ? pick_mode<Tag, NQ, 1>(a.w_sem) : pick_mode<Tag, NQ, 2>(a.w_sem);
+  if (a.k == 1) return pick_mode<Tag, NQ, 0>(a);
+  return a.k <= 32 ? pick_mode<Tag, NQ, 1>(a) : pick_mode<Tag, NQ, 2>(a);
 }
 template <class Tag>
 static KernelFn pick_nq(const ScanArgs& a, int* NQ) {
@@ -319,33 +412,51 @@ static int sm_count() {
   return n;
 }
 
+// Per-kernel launch facts, computed once: the max dynamic smem attribute per
+// kernel and blocks/SM per (kernel, smem) (host-side cache; the ABI may be
+// called from several threads).
+static std::mutex g_info_mu;
+static std::map<const void*, size_t> g_smem_set;
+static std::map<std::pair<const void*, size_t>, int> g_occ;
+
+static int prepare(KernelFn fn, size_t smem) {
+  const void* f = reinterpret_cast<const void*>(fn);
+  std::lock_guard<std::mutex> lk(g_info_mu);
+  size_t& set = g_smem_set[f];
+  if (set < smem) {
+    cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    set = smem;
+  }
+  int& per_sm = g_occ[{f, smem}];
+  if (per_sm == 0) {
+    int v = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&v, f, kScanThreads, smem);
+    per_sm = v < 1 ? 1 : v;
+  }
+  return per_sm;
+}
+
 int scan_gemv_grid(const ScanArgs& a) {
   int NQ = 1;
   KernelFn fn = pick(a, &NQ);
   const size_t smem = scan_smem(a, NQ);
-  cudaFuncSetAttribute(reinterpret_cast<const void*>(fn), cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-  int per_sm = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, reinterpret_cast<const void*>(fn), kScanThreads, smem);
-  if (per_sm < 1) per_sm = 1;
-  const int64_t ntiles = (a.n_rows + 31) / 32;
-  int64_t want = (ntiles + kScanWarps - 1) / kScanWarps;
+  const int per_sm = prepare(fn, smem);
+  const int tpi = traj_tpi(a) > 0 ? traj_tpi(a) : 1;
+  const int64_t ntiles = (a.n_rows + 32 * tpi - 1) / (32 * tpi);
+  int64_t want = (ntiles + kScanWarps - 1) / kScanWarps;   // >= one tile per warp
   int64_t full = int64_t(per_sm) * sm_count();
   int64_t g = want < full ? want : full;
   return int(g < 1 ? 1 : g);
 }
 
-cudaError_t launch_scan_gemv(const ScanArgs& a, cudaStream_t s, int* grid_out) {
+cudaError_t launch_scan_gemv(const ScanArgs& a, cudaStream_t s) {
   int NQ = 1;
   KernelFn fn = pick(a, &NQ);
   const size_t smem = scan_smem(a, NQ);
   if (smem > 227 * 1024) return cudaErrorInvalidValue;
-  cudaError_t e = cudaFuncSetAttribute(reinterpret_cast<const void*>(fn),
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-  if (e != cudaSuccess) return e;
-  if (grid_out) *grid_out = a.grid;
-  fn<<<a.grid, kScanThreads, smem, s>>>(a);
+  prepare(fn, smem);
   count_launch();
-  return cudaGetLastError();
+  return launch_pdl(fn, dim3(a.grid), dim3(kScanThreads), smem, s, a);
 }
 
 }  // namespace fmoe

@@ -14,8 +14,9 @@ int64_t launch_count() { return g_launches.load(); }
 // One warp per query: stream the candidate keys through a WarpTopK.
 template <int KPL>
 __global__ void __launch_bounds__(32) merge_keys_kernel(int n_lists, int k_in, const uint64_t* __restrict__ keys,
-                                                        int k, const float* __restrict__ qinfo,
-                                                        float* out_score, int64_t* out_id, uint64_t* out_keys) {
+                                                        int k, float* out_score, int64_t* out_id,
+                                                        uint64_t* out_keys) {
+  pdl_wait();
   const int q = blockIdx.x, lane = threadIdx.x;
   WarpTopK<KPL> m;
   m.init();
@@ -25,7 +26,7 @@ __global__ void __launch_bounds__(32) merge_keys_kernel(int n_lists, int k_in, c
     const uint64_t key = (j0 + lane < total) ? src[j0 + lane] : 0ull;
     m.offer(key, k);
   }
-  const bool valid = qinfo ? (qinfo[q] != 0.f) : true;
+  const bool valid = true;
 #pragma unroll
   for (int s = 0; s < KPL; ++s) {
     const int j = s * 32 + lane;
@@ -38,13 +39,13 @@ __global__ void __launch_bounds__(32) merge_keys_kernel(int n_lists, int k_in, c
   }
 }
 
-cudaError_t launch_merge_keys(int B, int n_lists, int k_in, const uint64_t* keys, int k, const float* qinfo,
-                              float* out_score, int64_t* out_id, uint64_t* out_keys, cudaStream_t s) {
+cudaError_t launch_merge_keys(int B, int n_lists, int k_in, const uint64_t* keys, int k, float* out_score,
+                              int64_t* out_id, uint64_t* out_keys, cudaStream_t s) {
   if (B <= 0) return cudaSuccess;
   if (k <= 32)
-    merge_keys_kernel<1><<<B, 32, 0, s>>>(n_lists, k_in, keys, k, qinfo, out_score, out_id, out_keys);
+    return count_launch(), launch_pdl(merge_keys_kernel<1>, dim3(B), dim3(32), 0, s, n_lists, k_in, keys, k, out_score, out_id, out_keys);
   else
-    merge_keys_kernel<2><<<B, 32, 0, s>>>(n_lists, k_in, keys, k, qinfo, out_score, out_id, out_keys);
+    return count_launch(), launch_pdl(merge_keys_kernel<2>, dim3(B), dim3(32), 0, s, n_lists, k_in, keys, k, out_score, out_id, out_keys);
   count_launch();
   return cudaGetLastError();
 }
@@ -54,6 +55,7 @@ template <int KPL>
 __global__ void __launch_bounds__(32) merge_lists_kernel(int B, int n_lists, int k_in, const float* __restrict__ scores,
                                                          const int64_t* __restrict__ ids, int k, float* out_score,
                                                          int64_t* out_id) {
+  pdl_wait();
   const int q = blockIdx.x, lane = threadIdx.x;
   WarpTopK<KPL> m;
   m.init();
@@ -86,9 +88,9 @@ cudaError_t launch_merge_lists(int B, int n_lists, int k_in, const float* scores
                                float* out_score, int64_t* out_id, cudaStream_t s) {
   if (B <= 0) return cudaSuccess;
   if (k <= 32)
-    merge_lists_kernel<1><<<B, 32, 0, s>>>(B, n_lists, k_in, scores, ids, k, out_score, out_id);
+    return count_launch(), launch_pdl(merge_lists_kernel<1>, dim3(B), dim3(32), 0, s, B, n_lists, k_in, scores, ids, k, out_score, out_id);
   else
-    merge_lists_kernel<2><<<B, 32, 0, s>>>(B, n_lists, k_in, scores, ids, k, out_score, out_id);
+    return count_launch(), launch_pdl(merge_lists_kernel<2>, dim3(B), dim3(32), 0, s, B, n_lists, k_in, scores, ids, k, out_score, out_id);
   count_launch();
   return cudaGetLastError();
 }
@@ -116,6 +118,7 @@ __global__ void __launch_bounds__(kSelWarps * 32) select_kernel(StoreView st, in
                                                                 const float* __restrict__ score, float delta, int K,
                                                                 int lb, int T, int64_t id_offset, int64_t n_rows,
                                                                 uint64_t* out_mask, int32_t* out_count) {
+  pdl_wait();
   __shared__ float sp[kSelWarps][kMaxE];
   __shared__ int si[kSelWarps][kMaxE];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -180,11 +183,11 @@ cudaError_t launch_select(const StoreView& st, int B, const int64_t* map_id, con
   if (warps <= 0) return cudaSuccess;
   const int grid = int((warps + kSelWarps - 1) / kSelWarps);
   if (st.bf16)
-    select_kernel<Bf16Tag><<<grid, kSelWarps * 32, 0, s>>>(st, B, map_id, score, delta, K, layer_begin, T, id_offset,
-                                                           n_rows, out_mask, out_count);
+    return count_launch(), launch_pdl(select_kernel<Bf16Tag>, dim3(grid), dim3(kSelWarps * 32), 0, s, st, B, map_id, score,
+                                      delta, K, layer_begin, T, id_offset, n_rows, out_mask, out_count);
   else
-    select_kernel<F32Tag><<<grid, kSelWarps * 32, 0, s>>>(st, B, map_id, score, delta, K, layer_begin, T, id_offset,
-                                                          n_rows, out_mask, out_count);
+    return count_launch(), launch_pdl(select_kernel<F32Tag>, dim3(grid), dim3(kSelWarps * 32), 0, s, st, B, map_id, score,
+                                      delta, K, layer_begin, T, id_offset, n_rows, out_mask, out_count);
   count_launch();
   return cudaGetLastError();
 }
@@ -199,27 +202,35 @@ __device__ __forceinline__ double warp_sum_dbl(double v) {
   return v;
 }
 
+// One block per new row (rows are independent).  The embedding row is
+// quantised and its squared norm reduced in float64 (fixed order: per-thread
+// strided partials, then warp and block trees); each warp quantises whole
+// layers of the map, reduces each layer's squared norm, and one thread forms
+// the prefix sums -- deterministic, so r_e / psq are bit-reproducible.
+constexpr int kWriteThreads = 256;
+
 template <class Tag>
-__global__ void __launch_bounds__(256) write_rows_kernel(WriteArgs w) {
+__global__ void __launch_bounds__(kWriteThreads) write_rows_kernel(WriteArgs w) {
+  pdl_wait();
   using T = typename StoreT<Tag>::T;
-  const int lane = threadIdx.x & 31;
-  const int64_t x = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
-  if (x >= w.B) return;
+  __shared__ double red[kWriteThreads / 32];
+  __shared__ double lsum[256];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int64_t x = blockIdx.x;
   const int64_t slot = w.slots ? w.slots[x] : w.first_slot + x;
   if (slot < 0) return;
   T* emb = static_cast<T*>(w.emb);
   T* maps = static_cast<T*>(w.maps);
   double acc = 0.0;
-  for (int e = lane; e < w.Dp; e += 32) {
+  for (int e = tid; e < w.Dp; e += kWriteThreads) {
     const float v = e < w.D ? to_store_value(w.in_emb[x * w.D + e], Tag()) : 0.f;
     if constexpr (sizeof(T) == 2) emb[slot * w.Dp + e] = __float2bfloat16_rn(v);
     else emb[slot * w.Dp + e] = v;
     acc += double(v) * double(v);
   }
   acc = warp_sum_dbl(acc);
-  if (lane == 0) w.r_e[slot] = acc > 0.0 ? float(1.0 / sqrt(acc)) : 0.f;
-  double cum = 0.0;
-  for (int l = 0; l < w.L; ++l) {
+  if (lane == 0) red[warp] = acc;
+  for (int l = warp; l < w.L; l += kWriteThreads / 32) {
     double a = 0.0;
     for (int j = lane; j < w.Ep; j += 32) {
       const float v = j < w.E ? to_store_value(w.in_maps[(x * w.L + l) * w.E + j], Tag()) : 0.f;
@@ -228,17 +239,28 @@ __global__ void __launch_bounds__(256) write_rows_kernel(WriteArgs w) {
       else maps[o] = v;
       a += double(v) * double(v);
     }
-    cum += warp_sum_dbl(a);
-    if (lane == 0) w.psq[int64_t(l) * w.cap + slot] = float(cum);
+    a = warp_sum_dbl(a);
+    if (lane == 0) lsum[l] = a;
+  }
+  __syncthreads();
+  if (tid == 0) {
+    double t = 0.0;
+    for (int i = 0; i < kWriteThreads / 32; ++i) t += red[i];
+    w.r_e[slot] = t > 0.0 ? float(1.0 / sqrt(t)) : 0.f;
+    double cum = 0.0;
+    for (int l = 0; l < w.L; ++l) {
+      cum += lsum[l];
+      w.psq[int64_t(l) * w.cap + slot] = float(cum);
+    }
   }
 }
 
 cudaError_t launch_write_rows(const WriteArgs& w, cudaStream_t s) {
   if (w.B <= 0) return cudaSuccess;
-  const int64_t threads = int64_t(w.B) * 32;
-  const int grid = int((threads + 255) / 256);
-  if (w.bf16) write_rows_kernel<Bf16Tag><<<grid, 256, 0, s>>>(w);
-  else write_rows_kernel<F32Tag><<<grid, 256, 0, s>>>(w);
+  if (w.L > 256) return cudaErrorInvalidValue;
+  count_launch();
+  if (w.bf16) return launch_pdl(write_rows_kernel<Bf16Tag>, dim3(w.B), dim3(kWriteThreads), 0, s, w);
+  return launch_pdl(write_rows_kernel<F32Tag>, dim3(w.B), dim3(kWriteThreads), 0, s, w);
   count_launch();
   return cudaGetLastError();
 }
@@ -250,6 +272,7 @@ __global__ void __launch_bounds__(32) resolve_kernel(int nrep, int kk, const uin
                                                      uint32_t id_offset, int64_t* slots_all, int x0,
                                                      int64_t first_append_slot, int64_t* out_slot,
                                                      int64_t* out_replaced) {
+  pdl_wait();
   __shared__ int64_t claimed[kMaxK];
   const int lane = threadIdx.x;
   for (int x = lane; x < x0; x += 32) {
@@ -288,13 +311,16 @@ __global__ void __launch_bounds__(32) resolve_kernel(int nrep, int kk, const uin
 
 cudaError_t launch_resolve(int nrep, int kk, const uint64_t* keys, uint32_t id_offset, int64_t* slots_all, int x0,
                            int64_t first_append_slot, int64_t* out_slot, int64_t* out_replaced, cudaStream_t s) {
-  resolve_kernel<<<1, 32, 0, s>>>(nrep, kk, keys, id_offset, slots_all, x0, first_append_slot, out_slot, out_replaced);
+  count_launch();
+  return launch_pdl(resolve_kernel, dim3(1), dim3(32), 0, s, nrep, kk, keys, id_offset, slots_all, x0,
+                    first_append_slot, out_slot, out_replaced);
   count_launch();
   return cudaGetLastError();
 }
 
 __global__ void append_ids_kernel(int n, int64_t first_slot, uint32_t id_offset, int64_t* out_slot,
                                   int64_t* out_replaced) {
+  pdl_wait();
   const int x = blockIdx.x * blockDim.x + threadIdx.x;
   if (x >= n) return;
   if (out_slot) out_slot[x] = int64_t(id_offset) + first_slot + x;
@@ -304,7 +330,9 @@ __global__ void append_ids_kernel(int n, int64_t first_slot, uint32_t id_offset,
 cudaError_t launch_append_ids(int n, int64_t first_slot, uint32_t id_offset, int64_t* out_slot, int64_t* out_replaced,
                               cudaStream_t s) {
   if (n <= 0 || (!out_slot && !out_replaced)) return cudaSuccess;
-  append_ids_kernel<<<(n + 255) / 256, 256, 0, s>>>(n, first_slot, id_offset, out_slot, out_replaced);
+  count_launch();
+  return launch_pdl(append_ids_kernel, dim3((n + 255) / 256), dim3(256), 0, s, n, first_slot, id_offset, out_slot,
+                    out_replaced);
   count_launch();
   return cudaGetLastError();
 }
@@ -312,6 +340,7 @@ cudaError_t launch_append_ids(int n, int64_t first_slot, uint32_t id_offset, int
 // ------------------------------------------------------------------ read back
 template <class Tag>
 __global__ void read_rows_kernel(StoreView st, int64_t slot0, int64_t count, float* out_emb, float* out_maps) {
+  pdl_wait();
   using T = typename StoreT<Tag>::T;
   const T* emb = static_cast<const T*>(st.emb);
   const T* maps = static_cast<const T*>(st.maps);
@@ -341,3 +370,31 @@ cudaError_t launch_read_rows(const StoreView& st, int64_t slot0, int64_t count, 
 }
 
 }  // namespace fmoe
+
+// ------------------------------------------------------------------ debug: phase tracer
+namespace fmoe {
+static unsigned long long* g_trace_buf = nullptr;
+unsigned long long* trace_buffer() { return g_trace_buf; }
+}  // namespace fmoe
+
+// enable > 0: allocate + zero the buffer and trace subsequent scans; enable == 0:
+// stop tracing; enable < 0: leave as is.  out (host, [max_blocks][8] u64), if
+// given, receives the buffer (device-synchronous).  Not part of the product ABI.
+extern "C" int fmoe_debug_trace(int enable, unsigned long long* out, int max_blocks) {
+  using namespace fmoe;
+  const size_t bytes = size_t(kTraceBlocks) * kTracePhases * 8;
+  if (enable > 0) {
+    if (!g_trace_buf && cudaMalloc(&g_trace_buf, bytes) != cudaSuccess) return -1;
+    if (cudaMemset(g_trace_buf, 0, bytes) != cudaSuccess) return -1;
+  }
+  if (out && g_trace_buf) {
+    const int nb = max_blocks < kTraceBlocks ? max_blocks : kTraceBlocks;
+    if (cudaMemcpy(out, g_trace_buf, size_t(nb) * kTracePhases * 8, cudaMemcpyDeviceToHost) != cudaSuccess) return -1;
+  }
+  if (enable == 0 && g_trace_buf) {
+    cudaDeviceSynchronize();
+    cudaFree(g_trace_buf);
+    g_trace_buf = nullptr;
+  }
+  return 0;
+}

@@ -2,8 +2,11 @@
 // host/device staging, and dispatch of the sm_100a kernels.
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
+#include <mutex>
 #include <string>
+#include <unordered_map>
 #include <vector>
 
 #include "../../include/fmoe.h"
@@ -16,8 +19,22 @@ int64_t launch_count();
 
 using namespace fmoe;
 
+// Scratch reused by consecutive calls on one stream (stream-ordered, so no
+// hazard between them): per-block candidate lists and the scan's ticket
+// counters, which the last block of every scan resets to zero.
+struct StreamScratch {
+  char* buf = nullptr;
+  size_t bytes = 0;
+  unsigned* counters = nullptr;      // zero between calls
+  int ncounters = 0;
+  unsigned long long* best = nullptr;  // zero between calls (k == 1 merge)
+  int nbest = 0;
+};
+
 struct fmoe_store {
   fmoe_store_config cfg;
+  mutable std::mutex mu;
+  mutable std::unordered_map<cudaStream_t, StreamScratch> scratch;
   int device;
   int bf16, esz, Dp, Ep;
   void* emb = nullptr;
@@ -155,12 +172,55 @@ fmoe_status check_cfg(const fmoe_store_config* c) {
   return FMOE_OK;
 }
 
-// One scoring call: scan (passes of <= 4 queries) + merge.
+fmoe_status stream_scratch(const fmoe_store* st, cudaStream_t s, size_t bytes, int ncount, int nbest, char** buf,
+                           unsigned** ctr, unsigned long long** best) {
+  std::lock_guard<std::mutex> lk(st->mu);
+  StreamScratch& sc = st->scratch[s];
+  cudaError_t e;
+  if (sc.bytes < bytes) {
+    if (sc.buf) cudaFreeAsync(sc.buf, s);
+    sc.buf = nullptr;
+    sc.bytes = 0;
+    const size_t nb = bytes + bytes / 2 + 4096;
+    if ((e = cudaMallocAsync(reinterpret_cast<void**>(&sc.buf), nb, s)) != cudaSuccess) return cuda_fail(e, "scratch");
+    sc.bytes = nb;
+  }
+  if (sc.ncounters < ncount) {
+    if (sc.counters) cudaFreeAsync(sc.counters, s);
+    sc.counters = nullptr;
+    sc.ncounters = 0;
+    const int nc = ncount < 64 ? 64 : ncount;
+    if ((e = cudaMallocAsync(reinterpret_cast<void**>(&sc.counters), size_t(nc) * 4, s)) != cudaSuccess)
+      return cuda_fail(e, "counters");
+    if ((e = cudaMemsetAsync(sc.counters, 0, size_t(nc) * 4, s)) != cudaSuccess) return cuda_fail(e, "counters");
+    sc.ncounters = nc;
+  }
+  if (sc.nbest < nbest) {
+    if (sc.best) cudaFreeAsync(sc.best, s);
+    sc.best = nullptr;
+    sc.nbest = 0;
+    const int nb = nbest < 256 ? 256 : nbest;
+    if ((e = cudaMallocAsync(reinterpret_cast<void**>(&sc.best), size_t(nb) * 8, s)) != cudaSuccess)
+      return cuda_fail(e, "best keys");
+    if ((e = cudaMemsetAsync(sc.best, 0, size_t(nb) * 8, s)) != cudaSuccess) return cuda_fail(e, "best keys");
+    sc.nbest = nb;
+  }
+  *buf = sc.buf;
+  *ctr = sc.counters;
+  *best = sc.best;
+  return FMOE_OK;
+}
+
+size_t align_up(size_t x) { return (x + 255) & ~size_t(255); }
+
+// One scoring call: GEMV scan passes of <= 4 queries, each merging its
+// candidates in its last block.  `extra` bytes of scratch are reserved after
+// the candidate lists (returned in *extra_ptr) for the caller.
 fmoe_status run_search(const fmoe_store* st, int64_t B, const float* dq, const float* dp, int64_t q_stride, int ell,
-                       float w, int k, int64_t n_rows, uint32_t id_offset, Staging& S, cudaStream_t s,
-                       float* ds, int64_t* di, uint64_t* dkeys, bool check_queries) {
+                       float w, int k, int64_t n_rows, uint32_t id_offset, cudaStream_t s, float* ds, int64_t* di,
+                       uint64_t* dkeys, bool check_queries) {
   if (n_rows == 0) {
-    cudaError_t e = launch_merge_keys(int(B), 0, k, nullptr, k, nullptr, ds, di, dkeys, s);
+    cudaError_t e = launch_merge_keys(int(B), 0, k, nullptr, k, ds, di, dkeys, s);
     return e == cudaSuccess ? FMOE_OK : cuda_fail(e, "merge launch");
   }
   ScanArgs a{};
@@ -175,21 +235,33 @@ fmoe_status run_search(const fmoe_store* st, int64_t B, const float* dq, const f
   a.id_offset = id_offset;
   a.q0 = 0;
   a.nq = int(B < 4 ? B : 4);
-  a.grid = scan_gemv_grid(a);
-  uint64_t* cand = static_cast<uint64_t*>(S.scratch(size_t(B) * a.grid * k * 8));
-  float* qinfo = static_cast<float*>(S.scratch(size_t(B) * 4));
-  fmoe_status cs = S.check();
+  // The TMA bulk-copy ring (scan_tma.cu) measured slower than register
+  // streaming in steady state (5.4 vs 6.3 TB/s at ell = 31, K2t);
+  // it stays selectable for measurements with FMOE_TMA=1.
+  static const bool use_tma = getenv("FMOE_TMA") != nullptr;
+  const bool tma = use_tma && scan_tma_supported(a);
+  a.grid = tma ? scan_tma_grid(a) : scan_gemv_grid(a);
+  const int npass = int((B + 3) / 4);
+  char* buf = nullptr;
+  unsigned* counters = nullptr;
+  unsigned long long* best = nullptr;
+  fmoe_status cs = stream_scratch(st, s, size_t(B) * a.grid * k * 8, npass, int(B), &buf, &counters, &best);
   if (cs != FMOE_OK) return cs;
-  a.cand = cand;
-  a.qinfo = qinfo;
-  for (int64_t q0 = 0; q0 < B; q0 += 4) {
-    a.q0 = int(q0);
-    a.nq = int(B - q0 < 4 ? B - q0 : 4);
-    cudaError_t e = launch_scan_gemv(a, s, nullptr);
+  a.best = best;
+  a.cand = reinterpret_cast<uint64_t*>(buf);
+  a.out_score = ds;
+  a.out_id = di;
+  a.out_keys = dkeys;
+  a.check_valid = check_queries ? 1 : 0;
+  a.trace = trace_buffer();
+  for (int p = 0; p < npass; ++p) {
+    a.q0 = 4 * p;
+    a.nq = int(B - a.q0 < 4 ? B - a.q0 : 4);
+    a.counter = counters + p;
+    cudaError_t e = tma ? launch_scan_tma(a, s) : launch_scan_gemv(a, s);
     if (e != cudaSuccess) return cuda_fail(e, "scan launch");
   }
-  cudaError_t e = launch_merge_keys(int(B), a.grid, k, cand, k, check_queries ? qinfo : nullptr, ds, di, dkeys, s);
-  return e == cudaSuccess ? FMOE_OK : cuda_fail(e, "merge launch");
+  return FMOE_OK;
 }
 
 fmoe_status search_common(const fmoe_store* st, int64_t B, const float* q_emb, const float* q_prefix, int32_t ell,
@@ -213,8 +285,8 @@ fmoe_status search_common(const fmoe_store* st, int64_t B, const float* q_emb, c
   int64_t* di = S.out(out_id, size_t(B) * k);
   fmoe_status r = S.check();
   if (r == FMOE_OK)
-    r = run_search(st, B, dq, dp, int64_t(ell) * E, traj ? ell : 0, w, k, st->n, uint32_t(st->cfg.id_offset), S, s,
-                   ds, di, nullptr, true);
+    r = run_search(st, B, dq, dp, int64_t(ell) * E, traj ? ell : 0, w, k, st->n, uint32_t(st->cfg.id_offset), s, ds,
+                   di, nullptr, true);
   return S.finish(r);
 }
 
@@ -249,6 +321,15 @@ fmoe_status fmoe_store_create(const fmoe_store_config* cfg, int device, fmoe_sto
     return fail(FMOE_ERR_INVALID_ARG, "no such CUDA device");
   }
   DeviceGuard g(device);
+  {
+    // keep stream-ordered scratch cached in the pool across synchronisations
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+      uint64_t thr = ~0ull;
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    }
+    cudaGetLastError();
+  }
   fmoe_store* st = new fmoe_store();
   st->cfg = *cfg;
   st->device = device;
@@ -274,6 +355,11 @@ void fmoe_store_destroy(fmoe_store* st) {
   if (!st) return;
   DeviceGuard g(st->device);
   cudaDeviceSynchronize();
+  for (auto& kv : st->scratch) {
+    cudaFree(kv.second.buf);
+    cudaFree(kv.second.counters);
+    cudaFree(kv.second.best);
+  }
   cudaFree(st->emb);
   cudaFree(st->r_e);
   cudaFree(st->maps);
@@ -322,7 +408,7 @@ fmoe_status fmoe_store_insert(fmoe_store* st, int64_t B, const float* emb, const
       // RDY_{x,y} = d/L sem + (L-d)/L traj over full maps, against
       // the contexts present before this call: rows [0, n0).
       const float w = float(st->cfg.d) / float(L);
-      r = run_search(st, nrep, de + a * D, dm + a * int64_t(L) * E, int64_t(L) * E, L, w, kk, n0, 0u, S, s, nullptr,
+      r = run_search(st, nrep, de + a * D, dm + a * int64_t(L) * E, int64_t(L) * E, L, w, kk, n0, 0u, s, nullptr,
                      nullptr, keys, false);
     }
     if (r == FMOE_OK) {

@@ -103,7 +103,7 @@ def test_semantic(setup, B, k):
             assert gi[x, 0].item() == pl[x]
 
 
-@pytest.mark.parametrize("ell", [1, 2, 7, "L"])
+@pytest.mark.parametrize("ell", [1, 2, 3, 7, "L"])
 @pytest.mark.parametrize("B,k", [(1, 1), (4, 8), (5, 33)])
 def test_trajectory(setup, ell, B, k):
     st, dt, sh = setup["st"], setup["dtype"], setup["shape"]

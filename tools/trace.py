@@ -1,0 +1,75 @@
+"""Per-block phase timeline of one search call (device %globaltimer stamps).
+
+    python tools/trace.py [--ell 1] [--n 1000000] [--D 8] [--mode traj|sem]
+Phases: 0 block start, 1 after griddepcontrol.wait, 2 queries staged,
+3 main loop done, 4 block merge done, 5 (last block) grid merge start,
+6 (last block) end.  Prints µs relative to the earliest block start."""
+import argparse
+import ctypes
+import os
+import sys
+
+import numpy as np
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import fmoe_synth as S  # noqa: E402
+import paper_2502_05370_b200 as fm  # noqa: E402
+
+
+def main():
+    p = argparse.ArgumentParser()
+    p.add_argument("--n", type=int, default=1_000_000)
+    p.add_argument("--D", type=int, default=8)
+    p.add_argument("--E", type=int, default=8)
+    p.add_argument("--L", type=int, default=32)
+    p.add_argument("--ell", type=int, default=1)
+    p.add_argument("--mode", default="traj")
+    a = p.parse_args()
+    lib = fm._lib
+    lib.fmoe_debug_trace.restype = ctypes.c_int
+    lib.fmoe_debug_trace.argtypes = [ctypes.c_int, ctypes.c_void_p, ctypes.c_int]
+    sh = S.Shape("m", a.L, a.E, 2, a.D, 64)
+    st = fm.ExpertMapStore(sh.L, sh.E, sh.K, sh.D, 3, a.n, "bf16")
+    for s0 in range(0, a.n, 65536):
+        e, m, _ = S.store_rows(sh, 1, s0, min(65536, a.n - s0), device="cuda")
+        st.insert(e, m)
+    qe, qm, _ = S.queries(sh, 1, a.n, 1, device="cuda")
+    pre = qm[:, :a.ell].contiguous()
+    out_s = torch.empty(1, 1, device="cuda")
+    out_i = torch.empty(1, 1, dtype=torch.int64, device="cuda")
+
+    def call():
+        if a.mode == "traj":
+            fm.fmoe_search_trajectory(st._h, pre, a.ell, 1, out_s, out_i)
+        else:
+            fm.fmoe_search_semantic(st._h, qe, 1, out_s, out_i)
+    for _ in range(5):
+        call()
+    torch.cuda.synchronize()
+    lib.fmoe_debug_trace(1, None, 0)
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ev0.record()
+    call()
+    ev1.record()
+    torch.cuda.synchronize()
+    buf = np.zeros((4096, 8), dtype=np.uint64)
+    lib.fmoe_debug_trace(-1, buf.ctypes.data, 4096)
+    lib.fmoe_debug_trace(0, None, 0)
+    used = buf[:, 0] > 0
+    t = buf[used].astype(np.int64)
+    t0 = t[:, 0].min()
+    rel = (t - t0) / 1e3
+    rel[t == 0] = np.nan
+    print(f"mode={a.mode} ell={a.ell} blocks={used.sum()} event time {ev0.elapsed_time(ev1) * 1e3:.1f} us")
+    names = ["start", "pdl_wait", "staged", "loop_done", "blk_merge", "last_start", "last_end"]
+    for ph in range(7):
+        col = rel[:, ph]
+        col = col[~np.isnan(col)]
+        if col.size:
+            print(f"  {names[ph]:10s} n={col.size:4d} min {col.min():7.2f} med {np.median(col):7.2f} max {col.max():7.2f} us")
+    st.close()
+
+
+if __name__ == "__main__":
+    main()
