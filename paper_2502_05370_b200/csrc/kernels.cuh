@@ -74,9 +74,30 @@ cudaError_t launch_scan_tma(const ScanArgs& a, cudaStream_t s);
 
 // Merge per-list candidate keys -> per-query top-k (also fills an empty
 // result when n_lists == 0).  keys [B][n_lists][k_in]; writes (out_score,
-// out_id) and/or out_keys [B][k].
-cudaError_t launch_merge_keys(int B, int n_lists, int k_in, const uint64_t* keys, int k,
+// out_id) and/or out_keys [B][k]; valid (nullable) [B]: 0 -> (NaN, -1).
+cudaError_t launch_merge_keys(int B, int n_lists, int k_in, const uint64_t* keys, int k, const float* valid,
                               float* out_score, int64_t* out_id, uint64_t* out_keys, cudaStream_t s);
+
+// tcgen05 batched scan (scan_umma.cu)
+struct UmmaPlanIn {
+  int bf16, nq, k, D, Dp, E, Ep, L, ell;
+  float w_sem;
+  int64_t n_rows, cap;
+  uint32_t id_offset;
+  const void* emb; const void* maps; const float* r_e; const float* psq;
+};
+struct UmmaLaunch {
+  UmmaPlanIn in;
+  const float* q_emb; const float* q_prefix; int64_t q_stride;   // this pass's first query
+  void* scratch;               // umma_scratch_bytes(in)
+  float* valid;                // [nq] validity flags of this pass
+  uint64_t* cand; int cand_q0; int grid;
+  unsigned long long* trace;
+};
+bool umma_supported(const UmmaPlanIn& in);
+size_t umma_scratch_bytes(const UmmaPlanIn& in);
+int umma_grid(const UmmaPlanIn& in);
+cudaError_t launch_umma(const UmmaLaunch& L, cudaStream_t s);
 // Merge (score, id) lists from an all-gather: [n_lists][B][k_in].
 cudaError_t launch_merge_lists(int B, int n_lists, int k_in, const float* scores,
                                const int64_t* ids, int k, float* out_score, int64_t* out_id,

@@ -1,0 +1,503 @@
+// scan_umma.cu -- K3: batched scoring on the 5th-gen tensor cores (tcgen05),
+// fused with a per-query top-k epilogue.  bf16 stores, 5 <= B <= 128 queries
+// per pass.
+//
+// What it computes (Eq. 1, Eq. 2 and the RDY blend):
+//   S_sem [x][y] = (q~_x . e~_y) * r_q(x) * r_e[y]
+//   S_traj[x][y] = (q~_x[0:ell] . M~_y[0:ell]) * r_q(ell,x) / sqrt(psq[ell-1][y])
+//   S = w*S_sem + (1-w)*S_traj,  then the k best (score desc, id asc) per x.
+// The two dot products are real dense contractions once B >= 16: queries sit
+// on the UMMA M dimension (128 lanes of TMEM, zero-padded), store rows on N
+// (256 per tile), and K runs over D (64-element SW128 boxes) and over the
+// observed layers of the layer-major map slabs.
+//
+// Structure (one CTA per SM, persistent over 256-row tiles, round-robin):
+//   warp 0      TMA producer: cp.async.bulk.tensor boxes of the query and
+//               store tiles into an S-stage smem ring (mbarrier complete_tx)
+//   warp 1      MMA issuer: one elected thread issues tcgen05.mma kind::f16
+//               (bf16 x bf16 -> fp32 in TMEM), tcgen05.commit frees stages and
+//               publishes finished accumulators
+//   warp 2      TMEM allocator (512 columns)
+//   warps 4..7  epilogue: tcgen05.ld 32x32b (thread = query lane), scale,
+//               blend, and insert into a per-thread sorted top-k list in smem
+// Accumulators: 1 (semantic or trajectory) or 2 (blend) x 256 fp32 columns,
+// double-buffered in TMEM when they fit (512 columns).
+// Per-CTA lists go to cand[q][cta][k]; a tiny merge kernel (PDL) finishes.
+//
+// Trajectory K layout by map row width RB = Ep*2 bytes (SURVEY §8(a) layout
+// note): RB = 16 (Mixtral, E = 8): SWIZZLE_NONE core matrices, one K = 16 MMA
+// spans two layers (LBO = the layer stride inside the stage); RB = 32 (Phi):
+// SWIZZLE_32B, one MMA per layer; RB = 64: SWIZZLE_64B, 2 MMAs per layer;
+// RB = 128 (Qwen, E = 60 padded to 64): SWIZZLE_128B, 4 MMAs per layer.
+#include <cuda.h>
+
+#include <map>
+#include <mutex>
+
+#include "common.cuh"
+#include "kernels.cuh"
+
+namespace fmoe {
+
+constexpr int UM_M = 128;
+constexpr int UM_N = 256;
+constexpr int kUmThreads = 256;
+constexpr int kStageA = UM_M * 128;          // 16 KB
+constexpr int kStageB = UM_N * 128;          // 32 KB
+constexpr int kUmStageBytes = kStageA + kStageB;
+constexpr int kUmMaxStages = 4;
+
+// ------------------------------------------------------------------ PTX wrappers
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, int c0, int c1, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];" ::"r"(
+          smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1)
+      : "memory");
+}
+__device__ __forceinline__ void tma_prefetch(const CUtensorMap* map) {
+  asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(map)) : "memory");
+}
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
+               : "memory");
+}
+__device__ __forceinline__ void tc_mma(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(acc)
+      : "memory");
+}
+__device__ __forceinline__ void tc_ld32(uint32_t taddr, uint32_t (&r)[32]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]),
+        "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]), "=r"(r[16]),
+        "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]),
+        "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      : "r"(taddr));
+}
+__device__ __forceinline__ void tc_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+
+// UMMA shared-memory matrix descriptor (K-major), sm_100 "version 1".
+//  layout: 0 none (interleaved core matrices), 6 SW32, 4 SW64, 2 SW128
+__device__ __forceinline__ uint64_t umma_desc(const void* smem, uint32_t lbo_bytes, uint32_t sbo_bytes,
+                                              uint32_t layout) {
+  uint64_t d = 0;
+  d |= uint64_t((smem_u32(smem) >> 4) & 0x3fff);
+  d |= uint64_t((lbo_bytes >> 4) & 0x3fff) << 16;
+  d |= uint64_t((sbo_bytes >> 4) & 0x3fff) << 32;
+  d |= uint64_t(1) << 46;                      // version (Blackwell)
+  d |= uint64_t(layout & 7) << 61;
+  return d;
+}
+// kind::f16 instruction descriptor: bf16 x bf16 -> f32, both K-major.
+__host__ __device__ constexpr uint32_t umma_idesc(int M, int N) {
+  return (1u << 4) | (1u << 7) | (1u << 10) | (uint32_t(N >> 3) << 17) | (uint32_t(M >> 4) << 24);
+}
+
+struct UmmaParams {
+  int64_t n_rows;       // rows to scan
+  int n_tiles;
+  int k;                // list length
+  int nq;               // queries of this pass (<= 128)
+  float w;              // blend weight
+  int n_sem_kb;         // semantic k-blocks (64 elements), 0 if no semantic part
+  int n_traj_kb;        // trajectory k-blocks (stages)
+  int ell_pad;          // layers covered by trajectory k-blocks (ell, even for RB = 16)
+  int tmode;            // 0: RB 16, 1: RB 32, 2: RB 64, 3: RB 128
+  int lc;               // layers per trajectory stage
+  int stages;
+  int acc_stages;       // TMEM accumulator buffers (1 or 2)
+  int64_t cap;          // slab stride (rows) of the map tensor
+  uint32_t id_offset;
+  const float* rq_s;    // [128] query inverse norms (0 for padding rows)
+  const float* rq_t;
+  const float* r_e;     // [cap]
+  const float* psq;     // [cap] prefix squared norms at layer ell-1 (traj)
+  uint64_t* cand;       // [B][grid][k]
+  int cand_q0;          // query offset of this pass in cand
+  int grid;
+  unsigned long long* trace;
+};
+
+template <bool SEM, bool TRAJ>
+__global__ void __launch_bounds__(kUmThreads, 1)
+    scan_umma_kernel(const __grid_constant__ CUtensorMap tm_qs, const __grid_constant__ CUtensorMap tm_es,
+                     const __grid_constant__ CUtensorMap tm_qt, const __grid_constant__ CUtensorMap tm_mt,
+                     const UmmaParams p) {
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  __shared__ __align__(8) uint64_t full[kUmMaxStages], empty[kUmMaxStages], tfull[2], tempty[2];
+  __shared__ uint32_t tmem_base_sh;
+
+  // 1024-byte alignment for the SW128 atoms
+  unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* lists = reinterpret_cast<uint64_t*>(smem + size_t(p.stages) * kUmStageBytes);   // [k][128]
+
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  constexpr int NACC = (SEM ? 1 : 0) + (TRAJ ? 1 : 0);
+  const int S = p.stages, AS = p.acc_stages;
+
+  if (tid == 0) {
+    for (int s = 0; s < S; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
+    for (int a = 0; a < AS; ++a) { mbar_init(&tfull[a], 1); mbar_init(&tempty[a], 4); }
+    mbar_fence_init();
+  }
+  if (warp == 0 && lane == 0) {
+    if (SEM) { tma_prefetch(&tm_qs); tma_prefetch(&tm_es); }
+    if (TRAJ) { tma_prefetch(&tm_qt); tma_prefetch(&tm_mt); }
+  }
+  if (warp == 2) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(&tmem_base_sh))
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  // empty top-k lists
+  for (int i = tid; i < p.k * UM_M; i += kUmThreads) lists[i] = 0ull;
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = tmem_base_sh;
+  trace_mark(p.trace, 0);
+  pdl_wait();
+  trace_mark(p.trace, 1);
+
+  const int n_kb = p.n_sem_kb + p.n_traj_kb;
+  const int RB = 16 << p.tmode;                        // trajectory row bytes
+
+  if (warp == 0) {
+    // ---------------------------------------------------------------- TMA producer
+    if (lane == 0) {
+      unsigned u = 0;
+      for (int t = blockIdx.x; t < p.n_tiles; t += gridDim.x) {
+        const int y0 = t * UM_N;
+        for (int kb = 0; kb < n_kb; ++kb, ++u) {
+          const int s = int(u % unsigned(S));
+          mbar_wait(&empty[s], ((u / unsigned(S)) & 1u) ^ 1u);
+          unsigned char* sa = smem + size_t(s) * kUmStageBytes;
+          unsigned char* sb = sa + kStageA;
+          if (SEM && kb < p.n_sem_kb) {
+            mbar_arrive_expect_tx(&full[s], kUmStageBytes);
+            tma_load_2d(sa, &tm_qs, kb * 64, 0, &full[s]);
+            tma_load_2d(sb, &tm_es, kb * 64, y0, &full[s]);
+          } else {
+            const int j = kb - p.n_sem_kb;
+            const int l0 = j * p.lc;
+            const int nl = p.ell_pad - l0 < p.lc ? p.ell_pad - l0 : p.lc;
+            mbar_arrive_expect_tx(&full[s], unsigned(nl * (UM_M + UM_N) * RB));
+            for (int l = 0; l < nl; ++l) {
+              tma_load_2d(sa + l * UM_M * RB, &tm_qt, 0, (l0 + l) * UM_M, &full[s]);
+              tma_load_2d(sb + l * UM_N * RB, &tm_mt, 0, int((l0 + l) * p.cap + y0), &full[s]);
+            }
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ---------------------------------------------------------------- MMA issuer
+    if (lane == 0) {
+      constexpr uint32_t idesc = umma_idesc(UM_M, UM_N);
+      unsigned u = 0, ti = 0;
+      for (int t = blockIdx.x; t < p.n_tiles; t += gridDim.x, ++ti) {
+        const int as = int(ti % unsigned(AS));
+        mbar_wait(&tempty[as], ((ti / unsigned(AS)) & 1u) ^ 1u);
+        tc_fence_after();
+        const uint32_t d_sem = tmem_base + uint32_t(as * NACC * UM_N);
+        const uint32_t d_trj = d_sem + (SEM ? UM_N : 0);
+        for (int kb = 0; kb < n_kb; ++kb, ++u) {
+          const int s = int(u % unsigned(S));
+          mbar_wait(&full[s], (u / unsigned(S)) & 1u);
+          tc_fence_after();
+          const unsigned char* sa = smem + size_t(s) * kUmStageBytes;
+          const unsigned char* sb = sa + kStageA;
+          if (SEM && kb < p.n_sem_kb) {
+#pragma unroll
+            for (int kk = 0; kk < 4; ++kk)
+              tc_mma(d_sem, umma_desc(sa + kk * 32, 16, 1024, 2), umma_desc(sb + kk * 32, 16, 1024, 2), idesc,
+                     (kb | kk) ? 1u : 0u);
+          } else {
+            const int j = kb - p.n_sem_kb;
+            const int l0 = j * p.lc;
+            const int nl = p.ell_pad - l0 < p.lc ? p.ell_pad - l0 : p.lc;
+            const bool first = (j == 0);
+            if (p.tmode == 0) {
+              // two 16-byte layers per K=16 MMA: LBO = the layer stride
+              for (int l = 0; l < nl; l += 2)
+                tc_mma(d_trj, umma_desc(sa + l * UM_M * 16, UM_M * 16, 128, 0),
+                       umma_desc(sb + l * UM_N * 16, UM_N * 16, 128, 0), idesc, (first && l == 0) ? 0u : 1u);
+            } else {
+              const uint32_t layout = p.tmode == 1 ? 6u : (p.tmode == 2 ? 4u : 2u);
+              const int ksteps = RB / 32;
+              for (int l = 0; l < nl; ++l)
+                for (int kk = 0; kk < ksteps; ++kk)
+                  tc_mma(d_trj, umma_desc(sa + l * UM_M * RB + kk * 32, 16, 8 * RB, layout),
+                         umma_desc(sb + l * UM_N * RB + kk * 32, 16, 8 * RB, layout), idesc,
+                         (first && l == 0 && kk == 0) ? 0u : 1u);
+            }
+          }
+          tc_commit(&empty[s]);            // stage s may be refilled once these MMAs retire
+        }
+        tc_commit(&tfull[as]);             // accumulators of tile t complete
+      }
+    }
+  } else if (warp >= 4) {
+    // ---------------------------------------------------------------- epilogue
+    const int qd = warp - 4;                      // TMEM lane quadrant of this warp
+    const int q = qd * 32 + lane;                 // query of this thread
+    const bool live = q < p.nq;
+    const float rqs = (SEM && live) ? p.rq_s[q] : 0.f;
+    const float rqt = (TRAJ && live) ? p.rq_t[q] : 0.f;
+    const float w = p.w, w1 = 1.f - p.w;
+    const int k = p.k;
+    uint64_t thr = 0ull;                          // current k-th key of this thread's list
+    unsigned ti = 0;
+    for (int t = blockIdx.x; t < p.n_tiles; t += gridDim.x, ++ti) {
+      const int as = int(ti % unsigned(AS));
+      mbar_wait(&tfull[as], (ti / unsigned(AS)) & 1u);
+      tc_fence_after();
+      const int y0 = t * UM_N;
+      const uint32_t lane_addr = uint32_t(qd * 32) << 16;
+      const uint32_t c_sem = tmem_base + lane_addr + uint32_t(as * NACC * UM_N);
+      const uint32_t c_trj = c_sem + (SEM ? UM_N : 0);
+      for (int c = 0; c < UM_N; c += 32) {
+        uint32_t vs[32], vt[32];
+        if (SEM) tc_ld32(c_sem + c, vs);
+        if (TRAJ) tc_ld32(c_trj + c, vt);
+        const int64_t yl = int64_t(y0) + c + lane;
+        const bool yok = yl < p.n_rows;
+        const float re_l = (SEM && yok) ? __ldg(p.r_e + yl) : 0.f;
+        const float ps_l = (TRAJ && yok) ? __ldg(p.psq + yl) : 0.f;
+        const float rm_l = ps_l > 0.f ? rsqrtf(ps_l) : 0.f;
+        tc_wait_ld();
+#pragma unroll
+        for (int j = 0; j < 32; ++j) {
+          const float re = __shfl_sync(0xffffffffu, re_l, j);
+          const float rm = __shfl_sync(0xffffffffu, rm_l, j);
+          float s = 0.f;
+          if (SEM) s = w * (__uint_as_float(vs[j]) * rqs * re);
+          if (TRAJ) s = fmaf(w1, __uint_as_float(vt[j]) * rqt * rm, s);
+          const int64_t y = int64_t(y0) + c + j;
+          const uint64_t key = (live && y < p.n_rows) ? pack_key(s, p.id_offset + uint32_t(y)) : 0ull;
+          if (key > thr) {
+            // sorted insert into this thread's list (column-major: entry i at lists[i*128 + q])
+            int pos = k - 1;
+            while (pos > 0) {
+              const uint64_t prev = lists[(pos - 1) * UM_M + q];
+              if (prev >= key) break;
+              lists[pos * UM_M + q] = prev;
+              --pos;
+            }
+            lists[pos * UM_M + q] = key;
+            thr = lists[(k - 1) * UM_M + q];
+          }
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tempty[as]);
+    }
+    trace_mark(p.trace, 3);
+    if (live) {
+      uint64_t* dst = p.cand + (int64_t(p.cand_q0 + q) * p.grid + blockIdx.x) * k;
+      for (int i = 0; i < k; ++i) dst[i] = lists[i * UM_M + q];
+    }
+  }
+  pdl_trigger();
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 2) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem_base) : "memory");
+  }
+  trace_mark(p.trace, 6);
+}
+
+// ------------------------------------------------------------------ query preparation
+// Quantises the batch to bf16 in the UMMA operand layouts (zero padding to
+// 128 rows, to Dp columns and to ell_pad layers) and computes the inverse norms
+// of the quantised rows (float64 sums) and the validity flags.
+__global__ void __launch_bounds__(256) umma_prep_kernel(const float* __restrict__ q_emb, const float* __restrict__ q_prefix,
+                                                        int64_t q_stride, int nq, int D, int Dp, int E, int Ep, int ell,
+                                                        int ell_pad, __nv_bfloat16* qs, __nv_bfloat16* qt, float* rq_s,
+                                                        float* rq_t, float* valid, int sem, int traj) {
+  pdl_wait();
+  __shared__ double red[2][8];
+  const int q = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const bool live = q < nq;
+  double a = 0.0, b = 0.0;
+  if (sem) {
+    for (int e = tid; e < Dp; e += 256) {
+      const float v = (live && e < D) ? __bfloat162float(__float2bfloat16_rn(q_emb[int64_t(q) * D + e])) : 0.f;
+      qs[int64_t(q) * Dp + e] = __float2bfloat16_rn(v);
+      a += double(v) * double(v);
+    }
+  }
+  if (traj) {
+    for (int i = tid; i < ell_pad * Ep; i += 256) {
+      const int l = i / Ep, j = i - l * Ep;
+      const float v = (live && l < ell && j < E)
+                          ? __bfloat162float(__float2bfloat16_rn(q_prefix[int64_t(q) * q_stride + l * E + j]))
+                          : 0.f;
+      qt[(int64_t(l) * UM_M + q) * Ep + j] = __float2bfloat16_rn(v);
+      b += double(v) * double(v);
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    a += __shfl_xor_sync(0xffffffffu, a, o);
+    b += __shfl_xor_sync(0xffffffffu, b, o);
+  }
+  if (lane == 0) { red[0][warp] = a; red[1][warp] = b; }
+  __syncthreads();
+  if (tid == 0) {
+    double sa = 0.0, sb = 0.0;
+    for (int w = 0; w < 8; ++w) { sa += red[0][w]; sb += red[1][w]; }
+    rq_s[q] = sa > 0.0 ? float(1.0 / sqrt(sa)) : 0.f;
+    rq_t[q] = sb > 0.0 ? float(1.0 / sqrt(sb)) : 0.f;
+    if (live) valid[q] = ((!sem || sa > 0.0) && (!traj || sb > 0.0)) ? 1.f : 0.f;
+  }
+}
+
+// ------------------------------------------------------------------ host side
+using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*, const cuuint64_t*,
+                              const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                              CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+static EncodeFn encoder() {
+  static EncodeFn fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeFn>(p);
+  });
+  return fn;
+}
+
+// 2-D bf16 tensor map: inner dim `cols` (contiguous), outer `rows`, box {bc, br}
+static bool make_map(CUtensorMap* m, const void* base, uint64_t cols, uint64_t rows, uint32_t bc, uint32_t br,
+                     CUtensorMapSwizzle sw) {
+  EncodeFn enc = encoder();
+  if (!enc) return false;
+  cuuint64_t dims[2] = {cols, rows};
+  cuuint64_t strides[1] = {cols * 2};
+  cuuint32_t box[2] = {bc, br};
+  cuuint32_t es[2] = {1, 1};
+  return enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box, es,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, sw, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+static int tmode_of(int rb) { return rb == 16 ? 0 : rb == 32 ? 1 : rb == 64 ? 2 : rb == 128 ? 3 : -1; }
+
+bool umma_supported(const UmmaPlanIn& in) {
+  if (!in.bf16 || in.nq < 1 || in.nq > UM_M || in.k < 1 || in.k > kMaxK) return false;
+  if (in.w_sem != 1.f && tmode_of(in.Ep * 2) < 0) return false;
+  if (!encoder()) return false;
+  return true;
+}
+
+// scratch layout: qs [128][Dp] bf16 | qt [ell+2][128][Ep] bf16 | rq_s, rq_t [128] f32
+static size_t qt_offset(const UmmaPlanIn& in) { return size_t(UM_M) * in.Dp * 2; }
+static size_t rq_offset(const UmmaPlanIn& in) { return qt_offset(in) + size_t(in.ell + 2) * UM_M * in.Ep * 2; }
+size_t umma_scratch_bytes(const UmmaPlanIn& in) { return rq_offset(in) + 2 * UM_M * 4 + 256; }
+
+int umma_grid(const UmmaPlanIn& in) {
+  static int sms = 0;
+  if (!sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  }
+  const int64_t tiles = (in.n_rows + UM_N - 1) / UM_N;
+  return int(tiles < sms ? (tiles < 1 ? 1 : tiles) : sms);
+}
+
+cudaError_t launch_umma(const UmmaLaunch& L, cudaStream_t s) {
+  const UmmaPlanIn& in = L.in;
+  const bool sem = in.w_sem != 0.f, traj = in.w_sem != 1.f;
+  const int ell_pad = traj ? in.ell + ((in.Ep * 2 == 16) ? (in.ell & 1) : 0) : 0;
+  char* scr = static_cast<char*>(L.scratch);
+  __nv_bfloat16* qs = reinterpret_cast<__nv_bfloat16*>(scr);
+  __nv_bfloat16* qt = reinterpret_cast<__nv_bfloat16*>(scr + qt_offset(in));
+  float* rq_s = reinterpret_cast<float*>(scr + rq_offset(in));
+  float* rq_t = rq_s + UM_M;
+  // 1. query preparation
+  count_launch();
+  cudaError_t e = launch_pdl(umma_prep_kernel, dim3(UM_M), dim3(256), 0, s, L.q_emb, L.q_prefix, L.q_stride, in.nq,
+                             in.D, in.Dp, in.E, in.Ep, in.ell, ell_pad, qs, qt, rq_s, rq_t, L.valid, sem ? 1 : 0,
+                             traj ? 1 : 0);
+  if (e != cudaSuccess) return e;
+  // 2. tensor maps
+  CUtensorMap tq_s{}, te_s{}, tq_t{}, tm_t{};
+  if (sem) {
+    if (!make_map(&tq_s, qs, in.Dp, UM_M, 64, UM_M, CU_TENSOR_MAP_SWIZZLE_128B) ||
+        !make_map(&te_s, in.emb, in.Dp, in.cap, 64, UM_N, CU_TENSOR_MAP_SWIZZLE_128B))
+      return cudaErrorInvalidValue;
+  }
+  int tmode = 0, lc = 0, n_traj_kb = 0;
+  if (traj) {
+    const int rb = in.Ep * 2;
+    tmode = tmode_of(rb);
+    const CUtensorMapSwizzle sw = tmode == 0   ? CU_TENSOR_MAP_SWIZZLE_NONE
+                                  : tmode == 1 ? CU_TENSOR_MAP_SWIZZLE_32B
+                                  : tmode == 2 ? CU_TENSOR_MAP_SWIZZLE_64B
+                                               : CU_TENSOR_MAP_SWIZZLE_128B;
+    if (!make_map(&tq_t, qt, in.Ep, uint64_t(ell_pad) * UM_M, in.Ep, UM_M, sw) ||
+        !make_map(&tm_t, in.maps, in.Ep, uint64_t(in.L) * in.cap, in.Ep, UM_N, sw))
+      return cudaErrorInvalidValue;
+    lc = kStageA / (UM_M * rb);
+    n_traj_kb = (ell_pad + lc - 1) / lc;
+  }
+  UmmaParams p{};
+  p.n_rows = in.n_rows;
+  p.n_tiles = int((in.n_rows + UM_N - 1) / UM_N);
+  p.k = in.k;
+  p.nq = in.nq;
+  p.w = in.w_sem;
+  p.n_sem_kb = sem ? (in.Dp + 63) / 64 : 0;
+  p.n_traj_kb = n_traj_kb;
+  p.ell_pad = ell_pad;
+  p.tmode = tmode;
+  p.lc = lc;
+  const size_t lists = size_t(in.k) * UM_M * 8;
+  int S = int((225 * 1024 - 1024 - lists) / kUmStageBytes);
+  p.stages = S > kUmMaxStages ? kUmMaxStages : S;
+  if (p.stages < 2) return cudaErrorInvalidValue;
+  p.acc_stages = (sem && traj) ? 1 : 2;
+  p.cap = in.cap;
+  p.id_offset = in.id_offset;
+  p.rq_s = rq_s;
+  p.rq_t = rq_t;
+  p.r_e = in.r_e;
+  p.psq = traj ? in.psq + int64_t(in.ell - 1) * in.cap : in.psq;
+  p.cand = L.cand;
+  p.cand_q0 = L.cand_q0;
+  p.grid = L.grid;
+  p.trace = L.trace;
+  const size_t smem = 1024 + size_t(p.stages) * kUmStageBytes + lists;
+  void (*fn)(const CUtensorMap, const CUtensorMap, const CUtensorMap, const CUtensorMap, const UmmaParams) =
+      sem && traj ? scan_umma_kernel<true, true> : sem ? scan_umma_kernel<true, false> : scan_umma_kernel<false, true>;
+  {
+    static std::mutex mu;
+    static std::map<const void*, size_t> set;
+    std::lock_guard<std::mutex> lk(mu);
+    size_t& cur = set[reinterpret_cast<const void*>(fn)];
+    if (cur < smem) {
+      e = cudaFuncSetAttribute(reinterpret_cast<const void*>(fn), cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               int(smem));
+      if (e != cudaSuccess) return e;
+      cur = smem;
+    }
+  }
+  count_launch();
+  return launch_pdl(fn, dim3(L.grid), dim3(kUmThreads), smem, s, tq_s, te_s, tq_t, tm_t, p);
+}
+
+}  // namespace fmoe

@@ -14,8 +14,8 @@ int64_t launch_count() { return g_launches.load(); }
 // One warp per query: stream the candidate keys through a WarpTopK.
 template <int KPL>
 __global__ void __launch_bounds__(32) merge_keys_kernel(int n_lists, int k_in, const uint64_t* __restrict__ keys,
-                                                        int k, float* out_score, int64_t* out_id,
-                                                        uint64_t* out_keys) {
+                                                        int k, const float* __restrict__ valid_q,
+                                                        float* out_score, int64_t* out_id, uint64_t* out_keys) {
   pdl_wait();
   const int q = blockIdx.x, lane = threadIdx.x;
   WarpTopK<KPL> m;
@@ -26,7 +26,7 @@ __global__ void __launch_bounds__(32) merge_keys_kernel(int n_lists, int k_in, c
     const uint64_t key = (j0 + lane < total) ? src[j0 + lane] : 0ull;
     m.offer(key, k);
   }
-  const bool valid = true;
+  const bool valid = valid_q ? valid_q[q] != 0.f : true;
 #pragma unroll
   for (int s = 0; s < KPL; ++s) {
     const int j = s * 32 + lane;
@@ -39,13 +39,13 @@ __global__ void __launch_bounds__(32) merge_keys_kernel(int n_lists, int k_in, c
   }
 }
 
-cudaError_t launch_merge_keys(int B, int n_lists, int k_in, const uint64_t* keys, int k, float* out_score,
-                              int64_t* out_id, uint64_t* out_keys, cudaStream_t s) {
+cudaError_t launch_merge_keys(int B, int n_lists, int k_in, const uint64_t* keys, int k, const float* valid,
+                              float* out_score, int64_t* out_id, uint64_t* out_keys, cudaStream_t s) {
   if (B <= 0) return cudaSuccess;
   if (k <= 32)
-    return count_launch(), launch_pdl(merge_keys_kernel<1>, dim3(B), dim3(32), 0, s, n_lists, k_in, keys, k, out_score, out_id, out_keys);
+    return count_launch(), launch_pdl(merge_keys_kernel<1>, dim3(B), dim3(32), 0, s, n_lists, k_in, keys, k, valid, out_score, out_id, out_keys);
   else
-    return count_launch(), launch_pdl(merge_keys_kernel<2>, dim3(B), dim3(32), 0, s, n_lists, k_in, keys, k, out_score, out_id, out_keys);
+    return count_launch(), launch_pdl(merge_keys_kernel<2>, dim3(B), dim3(32), 0, s, n_lists, k_in, keys, k, valid, out_score, out_id, out_keys);
   count_launch();
   return cudaGetLastError();
 }

@@ -213,6 +213,42 @@ fmoe_status stream_scratch(const fmoe_store* st, cudaStream_t s, size_t bytes, i
 
 size_t align_up(size_t x) { return (x + 255) & ~size_t(255); }
 
+// Batched call on the tensor cores: passes of <= 128 queries, per-CTA lists,
+// then one merge kernel over all passes.
+fmoe_status run_search_umma(const fmoe_store* st, UmmaPlanIn in, int64_t B, const float* dq, const float* dp,
+                            int64_t q_stride, cudaStream_t s, float* ds, int64_t* di, uint64_t* dkeys,
+                            bool check_queries) {
+  const int grid = umma_grid(in);
+  const size_t cand_b = align_up(size_t(B) * grid * in.k * 8);
+  const size_t valid_b = align_up(size_t(B) * 4);
+  const size_t prep_b = align_up(umma_scratch_bytes(in));
+  char* buf = nullptr;
+  unsigned* counters = nullptr;
+  unsigned long long* best = nullptr;
+  fmoe_status cs = stream_scratch(st, s, cand_b + valid_b + prep_b, 1, 1, &buf, &counters, &best);
+  if (cs != FMOE_OK) return cs;
+  uint64_t* cand = reinterpret_cast<uint64_t*>(buf);
+  float* valid = reinterpret_cast<float*>(buf + cand_b);
+  for (int64_t q0 = 0; q0 < B; q0 += 128) {
+    UmmaLaunch L{};
+    L.in = in;
+    L.in.nq = int(B - q0 < 128 ? B - q0 : 128);
+    L.q_emb = dq ? dq + q0 * in.D : nullptr;
+    L.q_prefix = dp ? dp + q0 * q_stride : nullptr;
+    L.q_stride = q_stride;
+    L.scratch = buf + cand_b + valid_b;
+    L.valid = valid + q0;
+    L.cand = cand;
+    L.cand_q0 = int(q0);
+    L.grid = grid;
+    L.trace = trace_buffer();
+    cudaError_t e = launch_umma(L, s);
+    if (e != cudaSuccess) return cuda_fail(e, "umma scan launch");
+  }
+  cudaError_t e = launch_merge_keys(int(B), grid, in.k, cand, in.k, check_queries ? valid : nullptr, ds, di, dkeys, s);
+  return e == cudaSuccess ? FMOE_OK : cuda_fail(e, "merge launch");
+}
+
 // One scoring call: GEMV scan passes of <= 4 queries, each merging its
 // candidates in its last block.  `extra` bytes of scratch are reserved after
 // the candidate lists (returned in *extra_ptr) for the caller.
@@ -220,8 +256,16 @@ fmoe_status run_search(const fmoe_store* st, int64_t B, const float* dq, const f
                        float w, int k, int64_t n_rows, uint32_t id_offset, cudaStream_t s, float* ds, int64_t* di,
                        uint64_t* dkeys, bool check_queries) {
   if (n_rows == 0) {
-    cudaError_t e = launch_merge_keys(int(B), 0, k, nullptr, k, ds, di, dkeys, s);
+    cudaError_t e = launch_merge_keys(int(B), 0, k, nullptr, k, nullptr, ds, di, dkeys, s);
     return e == cudaSuccess ? FMOE_OK : cuda_fail(e, "merge launch");
+  }
+  static const int umma_min_b = getenv("FMOE_UMMA_MIN_B") ? atoi(getenv("FMOE_UMMA_MIN_B")) : 5;
+  if (st->bf16 && B >= umma_min_b) {
+    UmmaPlanIn in{};
+    in.bf16 = 1; in.nq = int(B < 128 ? B : 128); in.k = k; in.D = st->cfg.D; in.Dp = st->Dp; in.E = st->cfg.E;
+    in.Ep = st->Ep; in.L = st->cfg.L; in.ell = ell; in.w_sem = w; in.n_rows = n_rows; in.cap = st->cfg.capacity;
+    in.id_offset = id_offset; in.emb = st->emb; in.maps = st->maps; in.r_e = st->r_e; in.psq = st->psq;
+    if (umma_supported(in)) return run_search_umma(st, in, B, dq, dp, q_stride, s, ds, di, dkeys, check_queries);
   }
   ScanArgs a{};
   a.st = st->view();

@@ -258,3 +258,29 @@ def test_topk_merge_api(lib):
     assert np.array_equal(out_i.cpu().numpy()[valid], mi[valid])
     assert np.array_equal(out_s.cpu().numpy()[valid], ms[valid].astype(np.float32))
     assert (out_i.cpu().numpy()[~valid] == -1).all()
+
+
+# ---------------------------------------------------------------- batched (tcgen05 path, B >= 5, bf16)
+@pytest.mark.parametrize("B,k", [(16, 1), (64, 8), (130, 64)])
+@pytest.mark.parametrize("mode", ["sem", "traj3", "trajL", "blend"])
+def test_batched_tcgen05(setup, B, k, mode):
+    if setup["dtype"] != "bf16":
+        pytest.skip("tensor-core path is bf16")
+    st, dt, sh = setup["st"], setup["dtype"], setup["shape"]
+    q_emb, q_maps, _ = S.queries(sh, 1, setup["N"], B)
+    if mode == "sem":
+        gs, gi = st.search_semantic(q_emb.cuda(), k)
+        ref = O.semantic_scores(O.quantize(q_emb.numpy(), dt), setup["Qe"])
+    elif mode.startswith("traj"):
+        ell = 3 if mode == "traj3" else sh.L
+        qp = q_maps[:, :ell].contiguous()
+        gs, gi = st.search_trajectory(qp.cuda(), ell, k)
+        ref = O.trajectory_scores(O.quantize(qp.numpy(), dt), setup["Qm"], ell)
+    else:
+        ell = 5
+        qp = q_maps[:, :ell].contiguous()
+        gs, gi = st.search_blend(q_emb.cuda(), qp.cuda(), ell, -1.0, k)
+        sem = O.semantic_scores(O.quantize(q_emb.numpy(), dt), setup["Qe"])
+        trj = O.trajectory_scores(O.quantize(qp.numpy(), dt), setup["Qm"], ell)
+        ref = O.blend_scores(sem, trj, np.float64(np.float32(3 / sh.L)))
+    check_topk(gs, gi, ref, k)
