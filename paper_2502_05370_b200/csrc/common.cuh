@@ -227,6 +227,10 @@ __device__ __forceinline__ unsigned long long globaltimer() {
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
   return t;
 }
+// same, from whichever single thread calls it
+__device__ __forceinline__ void trace_mark_here(unsigned long long* trace, int phase) {
+  if (trace && blockIdx.x < kTraceBlocks) trace[blockIdx.x * kTracePhases + phase] = globaltimer();
+}
 __device__ __forceinline__ void trace_mark(unsigned long long* trace, int phase) {
   if (trace && threadIdx.x == 0 && blockIdx.x < kTraceBlocks)
     trace[blockIdx.x * kTracePhases + phase] = globaltimer();

@@ -18,11 +18,15 @@
 //               (bf16 x bf16 -> fp32 in TMEM), tcgen05.commit frees stages and
 //               publishes finished accumulators
 //   warp 2      TMEM allocator (512 columns)
-//   warps 4..7  epilogue: tcgen05.ld 32x32b (thread = query lane), scale,
-//               blend, and insert into a per-thread sorted top-k list in smem
+//   warps 4..11 epilogue: tcgen05.ld 32x32b (thread = query lane, warp pair
+//               = two column halves), scale, blend, threshold test against the
+//               thread's k-th key; the rare winners go into a per-thread sorted
+//               list in shared memory (out-of-line insert keeps the hot loop
+//               small: a fully unrolled version thrashed the instruction cache)
 // Accumulators: 1 (semantic or trajectory) or 2 (blend) x 256 fp32 columns,
 // double-buffered in TMEM when they fit (512 columns).
-// Per-CTA lists go to cand[q][cta][k]; a tiny merge kernel (PDL) finishes.
+// Per-CTA lists (one per column half) go to cand[q][2*cta+half][k]; a tiny
+// merge kernel (PDL) finishes.
 //
 // Trajectory K layout by map row width RB = Ep*2 bytes (SURVEY §8(a) layout
 // note): RB = 16 (Mixtral, E = 8): SWIZZLE_NONE core matrices, one K = 16 MMA
@@ -41,7 +45,8 @@ namespace fmoe {
 
 constexpr int UM_M = 128;
 constexpr int UM_N = 256;
-constexpr int kUmThreads = 256;
+constexpr int kUmEpiWarps = 8;               // 2 per SM sub-partition: two column halves
+constexpr int kUmThreads = (4 + kUmEpiWarps) * 32;
 constexpr int kStageA = UM_M * 128;          // 16 KB
 constexpr int kStageB = UM_N * 128;          // 32 KB
 constexpr int kUmStageBytes = kStageA + kStageB;
@@ -80,6 +85,10 @@ __device__ __forceinline__ void tc_ld32(uint32_t taddr, uint32_t (&r)[32]) {
         "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]),
         "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
       : "r"(taddr));
+}
+// per-tile role timeline of CTA 0 (debug tracer): flat slot 8192 + role*256 + tile
+__device__ __forceinline__ void tile_mark(unsigned long long* trace, int role, unsigned ti) {
+  if (trace && blockIdx.x == 0 && ti < 256) trace[8192 + role * 256 + ti] = globaltimer();
 }
 __device__ __forceinline__ void tc_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
 
@@ -125,6 +134,31 @@ struct UmmaParams {
   unsigned long long* trace;
 };
 
+// Sorted insert into a per-thread list in shared memory (entry i at
+// l[i*stride]); called rarely (only for keys beating the k-th), kept out of
+// line so the hot epilogue loop stays small enough for the instruction cache.
+__device__ __forceinline__ uint64_t lds64(uint32_t a) {
+  uint64_t v;
+  asm volatile("ld.shared.u64 %0, [%1];" : "=l"(v) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ void sts64(uint32_t a, uint64_t v) {
+  asm volatile("st.shared.u64 [%0], %1;" ::"r"(a), "l"(v) : "memory");
+}
+// l: shared-memory address of entry 0, entries `stride` bytes apart.  Returns
+// the new k-th key.
+__device__ __noinline__ uint64_t list_insert(uint32_t l, uint32_t stride, int k, uint64_t key) {
+  int pos = k - 1;
+  while (pos > 0) {
+    const uint64_t prev = lds64(l + uint32_t(pos - 1) * stride);
+    if (prev >= key) break;
+    sts64(l + uint32_t(pos) * stride, prev);
+    --pos;
+  }
+  sts64(l + uint32_t(pos) * stride, key);
+  return lds64(l + uint32_t(k - 1) * stride);
+}
+
 template <bool SEM, bool TRAJ>
 __global__ void __launch_bounds__(kUmThreads, 1)
     scan_umma_kernel(const __grid_constant__ CUtensorMap tm_qs, const __grid_constant__ CUtensorMap tm_es,
@@ -136,7 +170,7 @@ __global__ void __launch_bounds__(kUmThreads, 1)
 
   // 1024-byte alignment for the SW128 atoms
   unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint64_t* lists = reinterpret_cast<uint64_t*>(smem + size_t(p.stages) * kUmStageBytes);   // [k][128]
+  uint64_t* lists = reinterpret_cast<uint64_t*>(smem + size_t(p.stages) * kUmStageBytes);   // [2][k][128] (KR == 0)
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   constexpr int NACC = (SEM ? 1 : 0) + (TRAJ ? 1 : 0);
@@ -144,7 +178,7 @@ __global__ void __launch_bounds__(kUmThreads, 1)
 
   if (tid == 0) {
     for (int s = 0; s < S; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
-    for (int a = 0; a < AS; ++a) { mbar_init(&tfull[a], 1); mbar_init(&tempty[a], 4); }
+    for (int a = 0; a < AS; ++a) { mbar_init(&tfull[a], 1); mbar_init(&tempty[a], kUmEpiWarps); }
     mbar_fence_init();
   }
   if (warp == 0 && lane == 0) {
@@ -157,14 +191,13 @@ __global__ void __launch_bounds__(kUmThreads, 1)
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
   }
   // empty top-k lists
-  for (int i = tid; i < p.k * UM_M; i += kUmThreads) lists[i] = 0ull;
+  for (int i = tid; i < 2 * p.k * UM_M; i += kUmThreads) lists[i] = 0ull;
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = tmem_base_sh;
   trace_mark(p.trace, 0);
   pdl_wait();
-  trace_mark(p.trace, 1);
 
   const int n_kb = p.n_sem_kb + p.n_traj_kb;
   const int RB = 16 << p.tmode;                        // trajectory row bytes
@@ -195,7 +228,9 @@ __global__ void __launch_bounds__(kUmThreads, 1)
             }
           }
         }
+        tile_mark(p.trace, 0, unsigned((t - int(blockIdx.x)) / int(gridDim.x)));
       }
+      trace_mark_here(p.trace, 5);
     }
   } else if (warp == 1) {
     // ---------------------------------------------------------------- MMA issuer
@@ -242,68 +277,105 @@ __global__ void __launch_bounds__(kUmThreads, 1)
           tc_commit(&empty[s]);            // stage s may be refilled once these MMAs retire
         }
         tc_commit(&tfull[as]);             // accumulators of tile t complete
+        tile_mark(p.trace, 1, ti);
       }
+      trace_mark_here(p.trace, 7);
     }
   } else if (warp >= 4) {
     // ---------------------------------------------------------------- epilogue
-    const int qd = warp - 4;                      // TMEM lane quadrant of this warp
+    // warp 4+e: TMEM lane quadrant e%4 (a warp may only read its own
+    // quadrant), column half e/4.  Thread = (query, half): its own top-k list.
+    const int e = warp - 4, qd = e & 3, half = e >> 2;
     const int q = qd * 32 + lane;                 // query of this thread
     const bool live = q < p.nq;
     const float rqs = (SEM && live) ? p.rq_s[q] : 0.f;
     const float rqt = (TRAJ && live) ? p.rq_t[q] : 0.f;
     const float w = p.w, w1 = 1.f - p.w;
     const int k = p.k;
-    uint64_t thr = 0ull;                          // current k-th key of this thread's list
+    constexpr int HC = UM_N / 2;                  // columns per half
+    uint64_t* ml = lists + size_t(half) * k * UM_M + q;   // this thread's list: entry i at ml[i*128]
+    const uint32_t ml_s = smem_u32(ml);
+    uint64_t thr = 0ull;                          // current k-th key
+    float thr_s = -__int_as_float(0x7f800000);    // its score (fast-path filter: score >= thr_s)
     unsigned ti = 0;
+    // per-row scales of the next half tile, loaded one tile ahead
+    float re_n[HC / 32], rm_n[HC / 32];
+    auto fetch = [&](int t) {
+#pragma unroll
+      for (int c = 0; c < HC / 32; ++c) {
+        const int64_t yl = int64_t(t) * UM_N + half * HC + c * 32 + lane;
+        const bool yok = t < p.n_tiles && yl < p.n_rows;
+        re_n[c] = (SEM && yok) ? __ldg(p.r_e + yl) : 0.f;
+        rm_n[c] = (TRAJ && yok) ? __ldg(p.psq + yl) : 0.f;
+      }
+    };
+    fetch(blockIdx.x);
     for (int t = blockIdx.x; t < p.n_tiles; t += gridDim.x, ++ti) {
       const int as = int(ti % unsigned(AS));
+      const int ybase = t * UM_N + half * HC;
+      float re_l[HC / 32], rm_l[HC / 32];
+#pragma unroll
+      for (int c = 0; c < HC / 32; ++c) {
+        re_l[c] = re_n[c];
+        rm_l[c] = rm_n[c] > 0.f ? rsqrtf(rm_n[c]) : 0.f;
+      }
+      fetch(t + gridDim.x);
+      if (ti == 0 && tid == 128) trace_mark_here(p.trace, 2);
       mbar_wait(&tfull[as], (ti / unsigned(AS)) & 1u);
+      if (ti == 0 && tid == 128) trace_mark_here(p.trace, 4);
+      if (tid == 128) tile_mark(p.trace, 2, ti);
       tc_fence_after();
-      const int y0 = t * UM_N;
       const uint32_t lane_addr = uint32_t(qd * 32) << 16;
-      const uint32_t c_sem = tmem_base + lane_addr + uint32_t(as * NACC * UM_N);
+      const uint32_t c_sem = tmem_base + lane_addr + uint32_t(as * NACC * UM_N + half * HC);
       const uint32_t c_trj = c_sem + (SEM ? UM_N : 0);
-      for (int c = 0; c < UM_N; c += 32) {
+#pragma unroll 1
+      for (int c = 0; c < HC / 32; ++c) {
         uint32_t vs[32], vt[32];
-        if (SEM) tc_ld32(c_sem + c, vs);
-        if (TRAJ) tc_ld32(c_trj + c, vt);
-        const int64_t yl = int64_t(y0) + c + lane;
-        const bool yok = yl < p.n_rows;
-        const float re_l = (SEM && yok) ? __ldg(p.r_e + yl) : 0.f;
-        const float ps_l = (TRAJ && yok) ? __ldg(p.psq + yl) : 0.f;
-        const float rm_l = ps_l > 0.f ? rsqrtf(ps_l) : 0.f;
+        if (SEM) tc_ld32(c_sem + c * 32, vs);
+        if (TRAJ) tc_ld32(c_trj + c * 32, vt);
+        const float rec = c == 0 ? re_l[0] : c == 1 ? re_l[1] : c == 2 ? re_l[2] : re_l[3];
+        const float rmc = c == 0 ? rm_l[0] : c == 1 ? rm_l[1] : c == 2 ? rm_l[2] : rm_l[3];
+        const int64_t yc = int64_t(ybase) + c * 32;
+        const int64_t left = p.n_rows - yc;
+        const unsigned vmask = !live ? 0u : (left >= 32 ? 0xffffffffu : (left <= 0 ? 0u : ((1u << left) - 1u)));
         tc_wait_ld();
+        // fast path: 32 scores, a float compare each against the k-th score
+        float sc[32];
+        unsigned m = 0;
 #pragma unroll
         for (int j = 0; j < 32; ++j) {
-          const float re = __shfl_sync(0xffffffffu, re_l, j);
-          const float rm = __shfl_sync(0xffffffffu, rm_l, j);
-          float s = 0.f;
-          if (SEM) s = w * (__uint_as_float(vs[j]) * rqs * re);
-          if (TRAJ) s = fmaf(w1, __uint_as_float(vt[j]) * rqt * rm, s);
-          const int64_t y = int64_t(y0) + c + j;
-          const uint64_t key = (live && y < p.n_rows) ? pack_key(s, p.id_offset + uint32_t(y)) : 0ull;
+          float v = 0.f;
+          if (SEM) v = w * (__uint_as_float(vs[j]) * rqs * __shfl_sync(0xffffffffu, rec, j));
+          if (TRAJ) v = fmaf(w1, __uint_as_float(vt[j]) * rqt * __shfl_sync(0xffffffffu, rmc, j), v);
+          sc[j] = v;
+          m |= (v >= thr_s ? 1u : 0u) << j;
+        }
+        m &= vmask;
+        // rare path: exact key order (score desc, id asc) for the candidates
+        while (m) {
+          const int j = __ffs(m) - 1;
+          m &= m - 1;
+          float v = sc[0];
+#pragma unroll
+          for (int jj = 1; jj < 32; ++jj)
+            if (jj == j) v = sc[jj];
+          const uint64_t key = pack_key(v, p.id_offset + uint32_t(yc + j));
           if (key > thr) {
-            // sorted insert into this thread's list (column-major: entry i at lists[i*128 + q])
-            int pos = k - 1;
-            while (pos > 0) {
-              const uint64_t prev = lists[(pos - 1) * UM_M + q];
-              if (prev >= key) break;
-              lists[pos * UM_M + q] = prev;
-              --pos;
-            }
-            lists[pos * UM_M + q] = key;
-            thr = lists[(k - 1) * UM_M + q];
+            thr = list_insert(ml_s, UM_M * 8, k, key);
+            thr_s = key_score(thr);
           }
         }
       }
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&tempty[as]);
+      if (ti == 0 && tid == 128) trace_mark_here(p.trace, 1);
+      if (tid == 128) tile_mark(p.trace, 3, ti);
     }
     trace_mark(p.trace, 3);
     if (live) {
-      uint64_t* dst = p.cand + (int64_t(p.cand_q0 + q) * p.grid + blockIdx.x) * k;
-      for (int i = 0; i < k; ++i) dst[i] = lists[i * UM_M + q];
+      uint64_t* dst = p.cand + (int64_t(p.cand_q0 + q) * (2 * p.grid) + 2 * blockIdx.x + half) * k;
+      for (int i = 0; i < k; ++i) dst[i] = ml[i * UM_M];
     }
   }
   pdl_trigger();
@@ -466,7 +538,7 @@ cudaError_t launch_umma(const UmmaLaunch& L, cudaStream_t s) {
   p.ell_pad = ell_pad;
   p.tmode = tmode;
   p.lc = lc;
-  const size_t lists = size_t(in.k) * UM_M * 8;
+  const size_t lists = size_t(2) * in.k * UM_M * 8;
   int S = int((225 * 1024 - 1024 - lists) / kUmStageBytes);
   p.stages = S > kUmMaxStages ? kUmMaxStages : S;
   if (p.stages < 2) return cudaErrorInvalidValue;
@@ -482,8 +554,9 @@ cudaError_t launch_umma(const UmmaLaunch& L, cudaStream_t s) {
   p.grid = L.grid;
   p.trace = L.trace;
   const size_t smem = 1024 + size_t(p.stages) * kUmStageBytes + lists;
-  void (*fn)(const CUtensorMap, const CUtensorMap, const CUtensorMap, const CUtensorMap, const UmmaParams) =
-      sem && traj ? scan_umma_kernel<true, true> : sem ? scan_umma_kernel<true, false> : scan_umma_kernel<false, true>;
+  using Fn = void (*)(const CUtensorMap, const CUtensorMap, const CUtensorMap, const CUtensorMap, const UmmaParams);
+  const Fn fn = sem && traj ? scan_umma_kernel<true, true> : sem ? scan_umma_kernel<true, false>
+                                                               : scan_umma_kernel<false, true>;
   {
     static std::mutex mu;
     static std::map<const void*, size_t> set;

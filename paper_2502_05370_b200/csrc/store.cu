@@ -219,7 +219,8 @@ fmoe_status run_search_umma(const fmoe_store* st, UmmaPlanIn in, int64_t B, cons
                             int64_t q_stride, cudaStream_t s, float* ds, int64_t* di, uint64_t* dkeys,
                             bool check_queries) {
   const int grid = umma_grid(in);
-  const size_t cand_b = align_up(size_t(B) * grid * in.k * 8);
+  const int n_lists = 2 * grid;                       // one list per (CTA, column half)
+  const size_t cand_b = align_up(size_t(B) * n_lists * in.k * 8);
   const size_t valid_b = align_up(size_t(B) * 4);
   const size_t prep_b = align_up(umma_scratch_bytes(in));
   char* buf = nullptr;
@@ -245,7 +246,7 @@ fmoe_status run_search_umma(const fmoe_store* st, UmmaPlanIn in, int64_t B, cons
     cudaError_t e = launch_umma(L, s);
     if (e != cudaSuccess) return cuda_fail(e, "umma scan launch");
   }
-  cudaError_t e = launch_merge_keys(int(B), grid, in.k, cand, in.k, check_queries ? valid : nullptr, ds, di, dkeys, s);
+  cudaError_t e = launch_merge_keys(int(B), n_lists, in.k, cand, in.k, check_queries ? valid : nullptr, ds, di, dkeys, s);
   return e == cudaSuccess ? FMOE_OK : cuda_fail(e, "merge launch");
 }
 

@@ -25,6 +25,8 @@ def main():
     p.add_argument("--L", type=int, default=32)
     p.add_argument("--ell", type=int, default=1)
     p.add_argument("--mode", default="traj")
+    p.add_argument("--B", type=int, default=1)
+    p.add_argument("--k", type=int, default=1)
     a = p.parse_args()
     lib = fm._lib
     lib.fmoe_debug_trace.restype = ctypes.c_int
@@ -34,16 +36,16 @@ def main():
     for s0 in range(0, a.n, 65536):
         e, m, _ = S.store_rows(sh, 1, s0, min(65536, a.n - s0), device="cuda")
         st.insert(e, m)
-    qe, qm, _ = S.queries(sh, 1, a.n, 1, device="cuda")
+    qe, qm, _ = S.queries(sh, 1, a.n, a.B, device="cuda")
     pre = qm[:, :a.ell].contiguous()
-    out_s = torch.empty(1, 1, device="cuda")
-    out_i = torch.empty(1, 1, dtype=torch.int64, device="cuda")
+    out_s = torch.empty(a.B, a.k, device="cuda")
+    out_i = torch.empty(a.B, a.k, dtype=torch.int64, device="cuda")
 
     def call():
         if a.mode == "traj":
-            fm.fmoe_search_trajectory(st._h, pre, a.ell, 1, out_s, out_i)
+            fm.fmoe_search_trajectory(st._h, pre, a.ell, a.k, out_s, out_i)
         else:
-            fm.fmoe_search_semantic(st._h, qe, 1, out_s, out_i)
+            fm.fmoe_search_semantic(st._h, qe, a.k, out_s, out_i)
     for _ in range(5):
         call()
     torch.cuda.synchronize()
@@ -62,12 +64,21 @@ def main():
     rel = (t - t0) / 1e3
     rel[t == 0] = np.nan
     print(f"mode={a.mode} ell={a.ell} blocks={used.sum()} event time {ev0.elapsed_time(ev1) * 1e3:.1f} us")
-    names = ["start", "pdl_wait", "staged", "loop_done", "blk_merge", "last_start", "last_end"]
-    for ph in range(7):
+    names = ["start", "pdl_wait", "staged", "loop_done", "blk_merge", "last_start", "last_end", "ph7"]
+    if a.B >= 5:
+        names = ["start", "epi_tile0_done", "epi_wait0", "epi_all_done", "epi_tile0_ready", "tma_done", "end", "mma_done"]
+    for ph in range(8):
         col = rel[:, ph]
         col = col[~np.isnan(col)]
         if col.size:
             print(f"  {names[ph]:10s} n={col.size:4d} min {col.min():7.2f} med {np.median(col):7.2f} max {col.max():7.2f} us")
+    flat = buf.reshape(-1)
+    if a.B >= 5:
+        roles = flat[8192:8192 + 4 * 256].reshape(4, 256).astype(np.int64)
+        ntile = int((roles[0] > 0).sum())
+        print("  CTA 0 per-tile timeline (us from kernel start): tile | tma_issued | mma_committed | epi_got | epi_done")
+        for i in range(min(ntile, 12)):
+            print("   ", i, " ".join(f"{(roles[r, i] - t0) / 1e3:8.2f}" for r in range(4)))
     st.close()
 
 
