@@ -110,6 +110,15 @@ fmoe_status fmoe_store_get_config(const fmoe_store* store, fmoe_store_config* ou
 fmoe_status fmoe_store_insert(fmoe_store* store, int64_t B, const float* emb, const float* maps,
                               int64_t* out_slot, int64_t* out_replaced, void* stream);
 
+/* Overwrite existing contexts at explicit slots (the write half of an insert;
+ * used by the sharded insert, SURVEY §8(e), and to restore a snapshot).
+ * emb [B][D], maps [B][L][E] fp32, slot [B] int64 GLOBAL ids.  Rows whose slot
+ * is -1 or lies outside [id_offset, id_offset + size) are skipped (that is how
+ * each shard ignores the other shards' rows); appends go through
+ * fmoe_store_insert.  Rows are quantised exactly as by fmoe_store_insert. */
+fmoe_status fmoe_store_write(fmoe_store* store, int64_t B, const float* emb, const float* maps,
+                             const int64_t* slot, void* stream);
+
 /* Read back `count` slots from `slot_begin` as the fp32 values the store holds
  * (the quantised rows): out_emb [count][D], out_maps [count][L][E]; either
  * may be NULL.  (SPEC snapshot.) */
@@ -166,6 +175,14 @@ fmoe_status fmoe_select_experts(const fmoe_store* store, int64_t B, const int64_
 fmoe_status fmoe_topk_merge(int64_t B, int32_t n_lists, int32_t k_in, const float* scores,
                             const int64_t* ids, int32_t k, float* out_score, int64_t* out_id,
                             int device, void* stream);
+
+/* Victim resolution of the RDY insert (Reading R8): ids [B][k] are
+ * each new row's candidate old contexts, best first (e.g. the merged output of
+ * per-shard RDY searches).  Row j, in batch order, takes its first id not taken
+ * by an earlier row; -1 if none.  out_victim [B].  1 <= k <= FMOE_MAX_K,
+ * B <= FMOE_MAX_K. */
+fmoe_status fmoe_resolve_victims(int64_t B, int32_t k, const int64_t* ids, int64_t* out_victim,
+                                 int device, void* stream);
 
 /* ---- diagnostics --------------------------------------------------------- */
 const char* fmoe_status_string(fmoe_status s);

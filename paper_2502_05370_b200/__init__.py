@@ -50,6 +50,8 @@ def _load():
         "fmoe_store_get_config": (I32, [P, ctypes.POINTER(fmoe_store_config)]),
         "fmoe_store_insert": (I32, [P, I64, P, P, P, P, P]),
         "fmoe_store_read": (I32, [P, I64, I64, P, P, P]),
+        "fmoe_store_write": (I32, [P, I64, P, P, P, P]),
+        "fmoe_resolve_victims": (I32, [I64, I32, P, P, ctypes.c_int, P]),
         "fmoe_search_semantic": (I32, [P, I64, P, I32, P, P, P]),
         "fmoe_search_trajectory": (I32, [P, I64, P, I32, I32, P, P, P]),
         "fmoe_search_blend": (I32, [P, I64, P, P, I32, F, I32, P, P, P]),
@@ -68,7 +70,7 @@ def _load():
 
 _lib = _load()
 ABI_SYMBOLS = ("fmoe_store_create", "fmoe_store_destroy", "fmoe_store_size", "fmoe_store_get_config",
-               "fmoe_store_insert", "fmoe_store_read", "fmoe_search_semantic", "fmoe_search_trajectory",
+               "fmoe_store_insert", "fmoe_store_read", "fmoe_store_write", "fmoe_resolve_victims", "fmoe_search_semantic", "fmoe_search_trajectory",
                "fmoe_search_blend", "fmoe_select_experts", "fmoe_topk_merge", "fmoe_status_string",
                "fmoe_last_error", "fmoe_kernel_launch_count")
 
@@ -120,6 +122,15 @@ def fmoe_store_size(h) -> int:
 def fmoe_store_insert(h, emb, maps, out_slot=None, out_replaced=None, stream=None):
     _check(_lib.fmoe_store_insert(h, emb.shape[0], _ptr(_f32(emb)), _ptr(_f32(maps)), _ptr(out_slot),
                                   _ptr(out_replaced), _stream(stream)))
+
+
+def fmoe_store_write(h, emb, maps, slot, stream=None):
+    _check(_lib.fmoe_store_write(h, emb.shape[0], _ptr(_f32(emb)), _ptr(_f32(maps)), _ptr(slot), _stream(stream)))
+
+
+def fmoe_resolve_victims(ids, out_victim, device=0, stream=None):
+    B, k = ids.shape
+    _check(_lib.fmoe_resolve_victims(B, k, _ptr(ids), _ptr(out_victim), int(device), _stream(stream)))
 
 
 def fmoe_store_read(h, slot_begin, count, out_emb=None, out_maps=None, stream=None):

@@ -1,6 +1,6 @@
 """Build the sm_100a shared library libfmoe_b200.so in-tree with nvcc.
 
-    python -m paper_2502_05370_b200.build [--force]
+    python paper_2502_05370_b200/build.py [--force]      (or __graft_entry__.build())
 
 Every .cu under csrc/ is compiled with -gencode arch=compute_100a,code=sm_100a
 (no other architecture), -O3 -lineinfo, in parallel, then linked against the

@@ -116,6 +116,8 @@ struct WriteArgs {
   const float* in_emb; const float* in_maps;   // [B][D], [B][L][E]
   int B;
   const int64_t* slots; int64_t first_slot;
+  int64_t slot_offset;   // slots[] hold global ids: local = slot - slot_offset
+  int64_t slot_limit;    // rows whose local slot is outside [0, slot_limit) are skipped
 };
 cudaError_t launch_write_rows(const WriteArgs& w, cudaStream_t s);
 
@@ -126,6 +128,8 @@ cudaError_t launch_write_rows(const WriteArgs& w, cudaStream_t s);
 cudaError_t launch_resolve(int nrep, int kk, const uint64_t* keys, uint32_t id_offset,
                            int64_t* victims, int x0, int64_t first_append_slot,
                            int64_t* out_slot, int64_t* out_replaced, cudaStream_t s);
+// Victim resolution from merged candidate ids [B][k] (best first).
+cudaError_t launch_resolve_ids(int B, int k, const int64_t* ids, int64_t* out_victim, cudaStream_t s);
 cudaError_t launch_append_ids(int n, int64_t first_slot, uint32_t id_offset, int64_t* out_slot,
                               int64_t* out_replaced, cudaStream_t s);
 

@@ -217,8 +217,8 @@ __global__ void __launch_bounds__(kWriteThreads) write_rows_kernel(WriteArgs w) 
   __shared__ double lsum[256];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int64_t x = blockIdx.x;
-  const int64_t slot = w.slots ? w.slots[x] : w.first_slot + x;
-  if (slot < 0) return;
+  const int64_t slot = w.slots ? w.slots[x] - w.slot_offset : w.first_slot + x;
+  if (slot < 0 || slot >= w.slot_limit) return;
   T* emb = static_cast<T*>(w.emb);
   T* maps = static_cast<T*>(w.maps);
   double acc = 0.0;
@@ -316,6 +316,42 @@ cudaError_t launch_resolve(int nrep, int kk, const uint64_t* keys, uint32_t id_o
                     first_append_slot, out_slot, out_replaced);
   count_launch();
   return cudaGetLastError();
+}
+
+__global__ void __launch_bounds__(32) resolve_ids_kernel(int B, int k, const int64_t* __restrict__ ids,
+                                                         int64_t* out_victim) {
+  pdl_wait();
+  __shared__ int64_t claimed[kMaxK];
+  const int lane = threadIdx.x;
+  for (int j = 0; j < B; ++j) {
+    int64_t best = -1;
+    for (int c0 = 0; c0 < k; c0 += 32) {
+      const int c = c0 + lane;
+      int64_t id = -1;
+      if (c < k) {
+        id = ids[int64_t(j) * k + c];
+        if (id >= 0)
+          for (int i = 0; i < j; ++i)
+            if (claimed[i] == id) { id = -1; break; }
+      }
+      const unsigned m = __ballot_sync(0xffffffffu, id >= 0);
+      if (m) {
+        best = __shfl_sync(0xffffffffu, id, __ffs(m) - 1);
+        break;
+      }
+    }
+    if (lane == 0) {
+      claimed[j] = best >= 0 ? best : -2;
+      out_victim[j] = best;
+    }
+    __syncwarp();
+  }
+}
+
+cudaError_t launch_resolve_ids(int B, int k, const int64_t* ids, int64_t* out_victim, cudaStream_t s) {
+  if (B <= 0) return cudaSuccess;
+  count_launch();
+  return launch_pdl(resolve_ids_kernel, dim3(1), dim3(32), 0, s, B, k, ids, out_victim);
 }
 
 __global__ void append_ids_kernel(int n, int64_t first_slot, uint32_t id_offset, int64_t* out_slot,

@@ -472,10 +472,59 @@ fmoe_status fmoe_store_insert(fmoe_store* st, int64_t B, const float* emb, const
     w.B = int(nrep > 0 ? B : a);
     w.slots = slots_all;
     w.first_slot = n0;
+    w.slot_offset = 0;
+    w.slot_limit = cap;
     cudaError_t e = launch_write_rows(w, s);
     if (e != cudaSuccess) r = cuda_fail(e, "write launch");
   }
   if (r == FMOE_OK) st->n = n0 + a;
+  return S.finish(r);
+}
+
+fmoe_status fmoe_store_write(fmoe_store* st, int64_t B, const float* emb, const float* maps, const int64_t* slot,
+                             void* stream) {
+  if (!st) return fail(FMOE_ERR_INVALID_ARG, "null store");
+  if (B < 0) return fail(FMOE_ERR_INVALID_ARG, "B");
+  if (B == 0) return FMOE_OK;
+  if (!emb || !maps || !slot) return fail(FMOE_ERR_INVALID_ARG, "null argument");
+  const int L = st->cfg.L, E = st->cfg.E, D = st->cfg.D;
+  DeviceGuard g(st->device);
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  Staging S(s, st->device);
+  const float* de = S.in(emb, size_t(B) * D);
+  const float* dm = S.in(maps, size_t(B) * L * E);
+  const int64_t* dsl = S.in(slot, size_t(B));
+  fmoe_status r = S.check();
+  if (r == FMOE_OK) {
+    WriteArgs w{};
+    w.emb = st->emb; w.r_e = st->r_e; w.maps = st->maps; w.psq = st->psq;
+    w.cap = st->cfg.capacity; w.L = L; w.E = E; w.D = D; w.Dp = st->Dp; w.Ep = st->Ep; w.bf16 = st->bf16;
+    w.in_emb = de; w.in_maps = dm;
+    w.B = int(B);
+    w.slots = dsl;
+    w.slot_offset = st->cfg.id_offset;
+    w.slot_limit = st->n;
+    cudaError_t e = launch_write_rows(w, s);
+    if (e != cudaSuccess) r = cuda_fail(e, "write launch");
+  }
+  return S.finish(r);
+}
+
+fmoe_status fmoe_resolve_victims(int64_t B, int32_t k, const int64_t* ids, int64_t* out_victim, int device,
+                                 void* stream) {
+  if (B < 0 || k < 1 || k > FMOE_MAX_K || B > FMOE_MAX_K) return fail(FMOE_ERR_INVALID_ARG, "sizes");
+  if (!ids || !out_victim) return fail(FMOE_ERR_INVALID_ARG, "null argument");
+  if (B == 0) return FMOE_OK;
+  DeviceGuard g(device);
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  Staging S(s, device);
+  const int64_t* di = S.in(ids, size_t(B) * k);
+  int64_t* dv = S.out(out_victim, size_t(B));
+  fmoe_status r = S.check();
+  if (r == FMOE_OK) {
+    cudaError_t e = launch_resolve_ids(int(B), k, di, dv, s);
+    if (e != cudaSuccess) r = cuda_fail(e, "resolve launch");
+  }
   return S.finish(r);
 }
 

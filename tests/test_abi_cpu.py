@@ -19,8 +19,8 @@ def declared_functions():
 
 @pytest.fixture(scope="module")
 def libpath():
-    from paper_2502_05370_b200 import build
-    return build.build()
+    import __graft_entry__
+    return __graft_entry__._builder().build()
 
 
 def test_header_declares_the_north_star_calls():
