@@ -51,10 +51,14 @@ WORKLOADS = {
 def parse():
     p = argparse.ArgumentParser()
     p.add_argument("--gpus", type=int, default=1)
-    p.add_argument("--steps", type=int, default=60)
+    p.add_argument("--steps", type=int, default=200)
     p.add_argument("--warmup", type=int, default=3)
     p.add_argument("--config", default="C2", choices=sorted(WORKLOADS))
     p.add_argument("--impl", default="fmoe", choices=["fmoe", "reference"])
+    p.add_argument("--traj", default="session", choices=["session", "stateless"],
+                   help="trajectory sweep: incremental session (SURVEY §8(f) #1) or one stateless search per prefix")
+    p.add_argument("--no-graph", dest="graph", action="store_false",
+                   help="time eager launches instead of a CUDA-graph replay of the step")
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--seed", type=int, default=S.BASE_SEED + 1)
@@ -70,12 +74,18 @@ def step_counts(cfg):
     return searches, n_traj
 
 
-def algorithmic_bytes(cfg, N):
-    """bytes a scan must stream per launch (store tiles only)."""
+def algorithmic_bytes(cfg, N, traj_mode="stateless"):
+    """bytes a scan must stream per launch (store tiles only).
+    Session step ell: slab ell-1, the prefix-norm row, and the per-query running
+    dot product (read from step 2 on, written every step)."""
     sh = cfg["shape"]
     s = 2 if cfg["dtype"] == "bf16" else 4
     sem = N * sh.D * s
-    traj = {ell: N * ell * sh.E * s for ell in range(1, sh.L)}
+    B = cfg["B"]
+    if traj_mode == "session":
+        traj = {ell: N * (sh.E * s + 4 + 4 * B * (2 if ell > 1 else 1)) for ell in range(1, sh.L)}
+    else:
+        traj = {ell: N * ell * sh.E * s for ell in range(1, sh.L)}
     rdy = N * (sh.D * s + sh.L * sh.E * s)
     return sem, traj, rdy
 
@@ -135,9 +145,10 @@ def build_store(fm, cfg, N_local, offset, dev, seed):
 class Step:
     """One matcher iteration (see module docstring) on a (possibly sharded) store."""
 
-    def __init__(self, fm, st, cfg, dist_ctx=None):
-        self.fm, self.st, self.cfg, self.dist = fm, st, cfg, dist_ctx
+    def __init__(self, fm, st, cfg, traj_mode="stateless"):
+        self.fm, self.st, self.cfg = fm, st, cfg
         self.sh = cfg["shape"]
+        self.sess = fm.fmoe_traj_session_create(st._h, cfg["B"]) if traj_mode == "session" else None
 
     def run(self, q_emb, q_maps, new_emb, new_maps, ev=None):
         """ev: optional dict kind -> list of (start, end) CUDA events around the searches."""
@@ -168,9 +179,14 @@ class Step:
         fm.fmoe_select_experts(h, top_i, top_s, cfg["delta"], 0, d, mask, cnt)
         m1 = torch.empty(B, 1, dtype=torch.int64, device=dev)
         c1 = torch.empty(B, 1, dtype=torch.int32, device=dev)
+        if self.sess is not None:
+            fm.fmoe_traj_session_reset(self.sess)        # the store changed at the last insert
         for ell in range(1, L):
-            pre = q_maps[ell - 1]
-            rec(f"traj{ell}", lambda: fm.fmoe_search_trajectory(h, pre, ell, k, out_s, out_i))
+            pre, lay = q_maps[ell - 1]
+            if self.sess is not None:
+                rec(f"traj{ell}", lambda: fm.fmoe_traj_session_step(self.sess, lay, k, out_s, out_i))
+            else:
+                rec(f"traj{ell}", lambda: fm.fmoe_search_trajectory(h, pre, ell, k, out_s, out_i))
             tgt = ell - 1 + d
             if tgt < L:
                 top_i = out_i[:, 0].contiguous()
@@ -183,8 +199,8 @@ class HostStep(Step):
     """The same step through the C ABI with host (pinned) buffers: the library
     stages inputs H2D and outputs D2H inside the timed region."""
 
-    def __init__(self, fm, st, cfg):
-        super().__init__(fm, st, cfg)
+    def __init__(self, fm, st, cfg, traj_mode="stateless"):
+        super().__init__(fm, st, cfg, traj_mode)
         B, k, d = cfg["B"], cfg["k"], 3
         pin = lambda *shape, dtype=torch.float32: torch.empty(*shape, dtype=dtype).pin_memory()
         self.out_s, self.out_i = pin(B, k), pin(B, k, dtype=torch.int64)
@@ -200,8 +216,14 @@ class HostStep(Step):
         fm.fmoe_search_semantic(h, q_emb, k, out_s, out_i)
         top_s.copy_(out_s[:, 0]); top_i.copy_(out_i[:, 0])
         fm.fmoe_select_experts(h, top_i, top_s, cfg["delta"], 0, d, self.mask, self.cnt)
+        if self.sess is not None:
+            fm.fmoe_traj_session_reset(self.sess)
         for ell in range(1, L):
-            fm.fmoe_search_trajectory(h, q_maps[ell - 1], ell, k, out_s, out_i)
+            pre, lay = q_maps[ell - 1]
+            if self.sess is not None:
+                fm.fmoe_traj_session_step(self.sess, lay, k, out_s, out_i)
+            else:
+                fm.fmoe_search_trajectory(h, pre, ell, k, out_s, out_i)
             tgt = ell - 1 + d
             if tgt < L:
                 top_s.copy_(out_s[:, 0]); top_i.copy_(out_i[:, 0])
@@ -210,9 +232,10 @@ class HostStep(Step):
         return float(out_s[0, 0])
 
     @staticmethod
-    def bytes_per_step(cfg, B):
+    def bytes_per_step(cfg, B, traj_mode="stateless"):
         sh, k, d, L = cfg["shape"], cfg["k"], 3, cfg["shape"].L
-        h2d = B * sh.D * 4 + sum(B * ell * sh.E * 4 for ell in range(1, L)) + B * (sh.D + L * sh.E) * 4
+        traj_in = sum(B * (1 if traj_mode == "session" else ell) * sh.E * 4 for ell in range(1, L))
+        h2d = B * sh.D * 4 + traj_in + B * (sh.D + L * sh.E) * 4
         n_sel = 1 + sum(1 for ell in range(1, L) if ell - 1 + d < L)
         h2d += n_sel * B * (8 + 4)                                  # map ids + scores into select
         d2h = (L) * B * k * (4 + 8)                                 # search outputs
@@ -226,7 +249,7 @@ def make_queries(cfg, N, pool, seed, dev):
     qs = []
     for p in range(pool):
         qe, qm, _ = S.queries(sh, seed + 101 * p, N, B, device=dev)
-        pre = [qm[:, :ell].contiguous() for ell in range(1, sh.L)]
+        pre = [(qm[:, :ell].contiguous(), qm[:, ell - 1].contiguous()) for ell in range(1, sh.L)]
         ne, nm, _ = S.store_rows(sh, seed + 7, N + p * B, B, device=dev)   # the iteration's new contexts
         qs.append((qe.contiguous(), pre, ne.contiguous(), nm.contiguous()))
     return qs
@@ -258,7 +281,7 @@ class ShardedStep(Step):
         s, i = out["r"]
         sst.select_experts(i[:, 0].contiguous(), s[:, 0].contiguous(), cfg["delta"], 0, d)
         for ell in range(1, L):
-            pre = q_maps[ell - 1]
+            pre, _ = q_maps[ell - 1]
             rec(f"traj{ell}", lambda: sst.search_trajectory(pre, ell, k))
             tgt = ell - 1 + d
             if tgt < L:
@@ -294,30 +317,67 @@ def run_fmoe(args, cfg, rank, world, local_rank):
     else:
         N_local = N_total
         st = build_store(fm, cfg, N_local, 0, dev, args.seed)
-        step = Step(fm, st, cfg)
+        if cfg["B"] > 4:
+            args.traj = "stateless"    # the session kernel is the B <= 4 streaming path; batches use tcgen05
+        step = Step(fm, st, cfg, args.traj)
     pool = 4
     qs = make_queries(cfg, N_total, pool, args.seed, dev)
     searches, n_traj = step_counts(cfg)
-    sem_b, traj_b, rdy_b = algorithmic_bytes(cfg, N_local)
+    sem_b, traj_b, rdy_b = algorithmic_bytes(cfg, N_local, args.traj if world == 1 else "stateless")
 
-    for w in range(args.warmup):
-        step.run(*qs[w % pool])
+    use_graph = args.graph and world == 1
+    run_stream = torch.cuda.Stream(device=dev) if use_graph else torch.cuda.current_stream(dev)
+    with torch.cuda.stream(run_stream):
+        for w in range(args.warmup):               # also creates this stream's scratch
+            step.run(*qs[w % pool])
     torch.cuda.synchronize()
     if world > 1:
         torch.distributed.barrier()
-    l0 = fm.kernel_launch_count()
-    clk = ClockSampler(local_rank) if rank == 0 else None
     ev = {}
+    # 1. eager timed pass: CUDA events around every search call (roofline source)
+    l0 = fm.kernel_launch_count()
     t0 = torch.cuda.Event(enable_timing=True)
     t1 = torch.cuda.Event(enable_timing=True)
+    eager_steps = args.steps
+    with torch.cuda.stream(run_stream):
+        t0.record()
+        for i in range(eager_steps):
+            step.run(*qs[i % pool], ev=ev)
+        t1.record()
     torch.cuda.synchronize()
-    t0.record()
-    for i in range(args.steps):
-        step.run(*qs[i % pool], ev=ev)
-    t1.record()
-    torch.cuda.synchronize()
-    ms = t0.elapsed_time(t1)
-    launches = fm.kernel_launch_count() - l0
+    ms_eager = t0.elapsed_time(t1)
+    launches_per_step = (fm.kernel_launch_count() - l0) / eager_steps
+    graphs = []
+    if use_graph:
+        # 2. the step captured once per query set as a CUDA graph (no host launch
+        #    overhead between the ~100 kernels of a step); the timed region replays it
+        for p_ in range(pool):
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g, stream=run_stream):
+                step.run(*qs[p_])
+            graphs.append(g)
+        with torch.cuda.stream(run_stream):
+            for p_ in range(pool):
+                graphs[p_].replay()
+        torch.cuda.synchronize()
+    clk = ClockSampler(local_rank) if rank == 0 else None
+    if graphs:
+        with torch.cuda.stream(run_stream):
+            t0.record()
+            for i in range(args.steps):
+                graphs[i % pool].replay()
+            t1.record()
+        torch.cuda.synchronize()
+        ms = t0.elapsed_time(t1)
+    else:
+        with torch.cuda.stream(run_stream):
+            t0.record()
+            for i in range(args.steps):
+                step.run(*qs[i % pool])
+            t1.record()
+        torch.cuda.synchronize()
+        ms = t0.elapsed_time(t1)
+    launches = int(round(launches_per_step * args.steps))
     clocks = clk.stop() if clk else None
     if world > 1:
         t = torch.tensor([ms], device=dev)
@@ -327,7 +387,7 @@ def run_fmoe(args, cfg, rank, world, local_rank):
     ms_step = ms / args.steps
 
     # per-kind search durations (events on the launching stream, inside the timed region)
-    kind_ms = {kk: sum(a.elapsed_time(b) for a, b in v) / args.steps for kk, v in ev.items()}
+    kind_ms = {kk: sum(a.elapsed_time(b) for a, b in v) / eager_steps for kk, v in ev.items()}
     traj_ms = sum(v for kk, v in kind_ms.items() if kk.startswith("traj"))
     scan_ms = kind_ms.get("semantic", 0) + traj_ms + kind_ms.get("rdy_insert", 0)
     scan_bytes = sem_b + sum(traj_b.values()) + rdy_b
@@ -335,7 +395,8 @@ def run_fmoe(args, cfg, rank, world, local_rank):
     achieved = scan_bytes / (scan_ms * 1e-3) / 1e9
     roofline = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peaks["hbm_gbs"], "unit": "GB/s",
                 "frac": round(achieved / peaks["hbm_gbs"], 4), "traffic": None,
-                "kernel": "scan_gemv_kernel (all 33 search launches of a step; events around each search call)",
+                "kernel": "the scan kernels of a step (all 33 searches; CUDA events around each search call, eager pass)",
+                "eager_ms_per_step": round(ms_eager / eager_steps, 4),
                 "peak_source": peaks["source"],
                 "breakdown": {
                     "semantic": {"ms": round(kind_ms.get("semantic", 0), 4), "GBps": round(sem_b / kind_ms.get("semantic", 1) / 1e6, 1)},
@@ -351,9 +412,9 @@ def run_fmoe(args, cfg, rank, world, local_rank):
     if not args.no_e2e and world == 1:
         hq = []
         for qe, pre, ne, nm in qs:
-            hq.append((qe.cpu().pin_memory(), [p.cpu().pin_memory() for p in pre], ne.cpu().pin_memory(),
-                       nm.cpu().pin_memory()))
-        hstep = HostStep(fm, st, cfg)
+            hq.append((qe.cpu().pin_memory(), [(p.cpu().pin_memory(), l.cpu().pin_memory()) for p, l in pre],
+                       ne.cpu().pin_memory(), nm.cpu().pin_memory()))
+        hstep = HostStep(fm, st, cfg, args.traj)
         for w in range(2):
             hstep.run(*hq[w % pool])
         torch.cuda.synchronize()
@@ -363,10 +424,13 @@ def run_fmoe(args, cfg, rank, world, local_rank):
             hstep.run(*hq[i % pool])
         torch.cuda.synchronize()
         e_ms = (time.perf_counter() - t0h) * 1e3 / e_steps
-        h2d, d2h = HostStep.bytes_per_step(cfg, cfg["B"])
+        h2d, d2h = HostStep.bytes_per_step(cfg, cfg["B"], args.traj)
         e2e = {"value": round(searches / (e_ms * 1e-3), 2), "unit": "searches/s", "ms_per_step": round(e_ms, 4),
                "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                "note": "host pinned buffers through the C ABI; library stages + synchronises per call"}
+    for obj in (step, locals().get("hstep")):
+        if obj is not None and getattr(obj, "sess", None) is not None:
+            fm.fmoe_traj_session_destroy(obj.sess)
     st.close()
     return dict(value=value, ms_step=ms_step, roofline=roofline, e2e=e2e, clocks=clocks, launches=launches,
                 N_local=N_local)
@@ -448,7 +512,11 @@ def main():
                                f"batch {cfg['B']}, semantic + trajectory ell=1..{sh.L - 1} + select + RDY insert at "
                                f"full capacity", "N": cfg["N"], "L": sh.L, "E": sh.E, "D": sh.D, "B": cfg["B"],
                    "k": cfg["k"], "store_dtype": cfg["dtype"], "searches_per_step": searches,
-                   "l2": "inputs larger than L2 (store >> 126 MB), no flush"}
+                   "trajectory": ("incremental session: step ell reads slab ell + running dots (SURVEY §8(f) #1)"
+                                  if args.traj == "session" and world == 1 and cfg["B"] <= 4 else
+                                  "stateless: one search over the whole prefix per ell"),
+                   "l2": "inputs larger than L2 (store >> 126 MB), no flush",
+                   "launch": "CUDA graph replay of the step (1 GPU)" if (args.graph and world == 1) else "eager"}
 
     if args.impl == "reference":
         if rank != 0:

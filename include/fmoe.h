@@ -148,6 +148,26 @@ fmoe_status fmoe_search_blend(const fmoe_store* store, int64_t B, const float* q
                               const float* q_prefix, int32_t ell, float w_sem, int32_t k,
                               float* out_score, int64_t* out_id, void* stream);
 
+/* ---- incremental trajectory search ---------------- */
+
+/* A session follows B requests through the layers of one inference iteration:
+ * step t (t = 0, 1, ...) consumes layer t of each query and returns the
+ * trajectory search (Eq. 2) at prefix ell = t+1 -- the same result as
+ * fmoe_search_trajectory on the prefix (summation order aside), but step t
+ * reads only slab t of the store plus a running per-row dot product
+ * (4 bytes per query and row, kept in the session), instead of t+1 slabs.
+ * The session owns B*capacity*4 bytes of device memory.  Any insert/write to
+ * the store invalidates it (the next step returns INVALID_ARG until reset).
+ * 1 <= B <= 64. */
+typedef struct fmoe_traj_session fmoe_traj_session;
+fmoe_status fmoe_traj_session_create(const fmoe_store* store, int64_t B, fmoe_traj_session** out);
+/* q_layer [B][E] fp32: layer t of every query.  Outputs as fmoe_search_trajectory. */
+fmoe_status fmoe_traj_session_step(fmoe_traj_session* session, const float* q_layer, int32_t k,
+                                   float* out_score, int64_t* out_id, void* stream);
+/* Start a new prefix (next step consumes layer 0); re-validates against the store. */
+fmoe_status fmoe_traj_session_reset(fmoe_traj_session* session);
+void fmoe_traj_session_destroy(fmoe_traj_session* session);
+
 /* ---- similarity-aware expert selection ----------------------- */
 
 /* For each query x with matched context map_id[x] (-1 = none) and its score:

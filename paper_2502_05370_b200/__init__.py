@@ -56,6 +56,10 @@ def _load():
         "fmoe_search_trajectory": (I32, [P, I64, P, I32, I32, P, P, P]),
         "fmoe_search_blend": (I32, [P, I64, P, P, I32, F, I32, P, P, P]),
         "fmoe_select_experts": (I32, [P, I64, P, P, F, I32, I32, P, P, P]),
+        "fmoe_traj_session_create": (I32, [P, I64, ctypes.POINTER(P)]),
+        "fmoe_traj_session_step": (I32, [P, P, I32, P, P, P]),
+        "fmoe_traj_session_reset": (I32, [P]),
+        "fmoe_traj_session_destroy": (None, [P]),
         "fmoe_topk_merge": (I32, [I64, I32, I32, P, P, I32, P, P, ctypes.c_int, P]),
         "fmoe_status_string": (ctypes.c_char_p, [I32]),
         "fmoe_last_error": (ctypes.c_char_p, []),
@@ -71,7 +75,8 @@ def _load():
 _lib = _load()
 ABI_SYMBOLS = ("fmoe_store_create", "fmoe_store_destroy", "fmoe_store_size", "fmoe_store_get_config",
                "fmoe_store_insert", "fmoe_store_read", "fmoe_store_write", "fmoe_resolve_victims", "fmoe_search_semantic", "fmoe_search_trajectory",
-               "fmoe_search_blend", "fmoe_select_experts", "fmoe_topk_merge", "fmoe_status_string",
+               "fmoe_search_blend", "fmoe_select_experts", "fmoe_traj_session_create", "fmoe_traj_session_step",
+               "fmoe_traj_session_reset", "fmoe_traj_session_destroy", "fmoe_topk_merge", "fmoe_status_string",
                "fmoe_last_error", "fmoe_kernel_launch_count")
 
 
@@ -157,6 +162,24 @@ def fmoe_select_experts(h, map_id, score, delta, layer_begin, layer_end, out_mas
                                     _ptr(out_mask), _ptr(out_count), _stream(stream)))
 
 
+def fmoe_traj_session_create(h, B):
+    s = ctypes.c_void_p()
+    _check(_lib.fmoe_traj_session_create(h, B, ctypes.byref(s)))
+    return s
+
+
+def fmoe_traj_session_step(s, q_layer, k, out_score, out_id, stream=None):
+    _check(_lib.fmoe_traj_session_step(s, _ptr(_f32(q_layer)), k, _ptr(out_score), _ptr(out_id), _stream(stream)))
+
+
+def fmoe_traj_session_reset(s):
+    _check(_lib.fmoe_traj_session_reset(s))
+
+
+def fmoe_traj_session_destroy(s):
+    _lib.fmoe_traj_session_destroy(s)
+
+
 def fmoe_topk_merge(scores, ids, k, out_score, out_id, device=0, stream=None):
     n_lists, B, k_in = scores.shape
     _check(_lib.fmoe_topk_merge(B, n_lists, k_in, _ptr(scores), _ptr(ids), k, _ptr(out_score), _ptr(out_id),
@@ -222,6 +245,9 @@ class ExpertMapStore:
         fmoe_search_blend(self._h, q_emb, q_prefix, ell, w_sem, k, s, i, stream)
         return s, i
 
+    def trajectory_session(self, B):
+        return TrajectorySession(self, B)
+
     def select_experts(self, map_id, score, delta=-1.0, layer_begin=0, layer_end=None, stream=None):
         layer_end = self.L if layer_end is None else layer_end
         B, T = map_id.shape[0], layer_end - layer_begin
@@ -230,3 +256,31 @@ class ExpertMapStore:
         fmoe_select_experts(self._h, map_id.contiguous(), None if score is None else score.contiguous(), delta,
                             layer_begin, layer_end, mask, cnt, stream)
         return mask, cnt
+
+
+class TrajectorySession:
+    """Incremental trajectory search: step() consumes the next layer of each query."""
+
+    def __init__(self, store, B):
+        self.store, self.B = store, B
+        self._s = fmoe_traj_session_create(store._h, B)
+
+    def step(self, q_layer, k=1, stream=None):
+        s = torch.empty(self.B, k, dtype=torch.float32, device=self.store.device)
+        i = torch.empty(self.B, k, dtype=torch.int64, device=self.store.device)
+        fmoe_traj_session_step(self._s, q_layer.contiguous(), k, s, i, stream)
+        return s, i
+
+    def reset(self):
+        fmoe_traj_session_reset(self._s)
+
+    def close(self):
+        if self._s is not None:
+            fmoe_traj_session_destroy(self._s)
+            self._s = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

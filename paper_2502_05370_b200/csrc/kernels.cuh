@@ -78,6 +78,18 @@ cudaError_t launch_scan_tma(const ScanArgs& a, cudaStream_t s);
 cudaError_t launch_merge_keys(int B, int n_lists, int k_in, const uint64_t* keys, int k, const float* valid,
                               float* out_score, int64_t* out_id, uint64_t* out_keys, cudaStream_t s);
 
+// Incremental trajectory session (traj_session.cu): step `layer` consumes one
+// layer of each query; acc [B][cap] running dots; qn [2][B] running norms.
+struct SessionArgs {
+  const float* q_layer;   // [B][E] fp32, this step's layer
+  int layer;              // 0-based layer consumed by this step
+  float* acc;             // [B][cap]
+  const double* qn_prev;  // [B]
+  double* qn_next;        // [B]
+};
+cudaError_t launch_traj_session(const ScanArgs& a, const SessionArgs& s, cudaStream_t stream);
+int traj_session_grid(const ScanArgs& a);
+
 // tcgen05 batched scan (scan_umma.cu)
 struct UmmaPlanIn {
   int bf16, nq, k, D, Dp, E, Ep, L, ell;

@@ -20,8 +20,8 @@
 //   warp 2      TMEM allocator (512 columns)
 //   warps 4..11 epilogue: tcgen05.ld 32x32b (thread = query lane, warp pair
 //               = two column halves), scale, blend, threshold test against the
-//               thread's k-th key; the rare winners go into a per-thread sorted
-//               list in shared memory (out-of-line insert keeps the hot loop
+//               thread's k-th key; the rare winners go into a per-thread min-heap
+//               in shared memory (out-of-line replace-root keeps the hot loop
 //               small: a fully unrolled version thrashed the instruction cache)
 // Accumulators: 1 (semantic or trajectory) or 2 (blend) x 256 fp32 columns,
 // double-buffered in TMEM when they fit (512 columns).
@@ -122,6 +122,8 @@ struct UmmaParams {
   int lc;               // layers per trajectory stage
   int stages;
   int acc_stages;       // TMEM accumulator buffers (1 or 2)
+  int split_kb;         // semantic-only: k-blocks >= split_kb accumulate into a second TMEM
+                        // accumulator, summed in fp32 by the epilogue (0 = no split)
   int64_t cap;          // slab stride (rows) of the map tensor
   uint32_t id_offset;
   const float* rq_s;    // [128] query inverse norms (0 for padding rows)
@@ -145,18 +147,29 @@ __device__ __forceinline__ uint64_t lds64(uint32_t a) {
 __device__ __forceinline__ void sts64(uint32_t a, uint64_t v) {
   asm volatile("st.shared.u64 [%0], %1;" ::"r"(a), "l"(v) : "memory");
 }
-// l: shared-memory address of entry 0, entries `stride` bytes apart.  Returns
-// the new k-th key.
-__device__ __noinline__ uint64_t list_insert(uint32_t l, uint32_t stride, int k, uint64_t key) {
-  int pos = k - 1;
-  while (pos > 0) {
-    const uint64_t prev = lds64(l + uint32_t(pos - 1) * stride);
-    if (prev >= key) break;
-    sts64(l + uint32_t(pos) * stride, prev);
-    --pos;
+// Per-thread top-k list in shared memory kept as a binary MIN-heap of k keys
+// (entry i at l + i*stride; empty entries are key 0): the root is the current
+// k-th best key, a better key replaces it and sifts down (log2 k levels, no
+// shifting -- the sorted-array insert cost O(k) smem moves and dominated the
+// k = 64 RDY scan).  The merge kernel takes the lists unsorted.  Called only
+// for keys beating the root, out of line.  Returns the new root.
+__device__ __noinline__ uint64_t heap_replace_root(uint32_t l, uint32_t stride, int k, uint64_t key) {
+  int i = 0;
+  while (true) {
+    const int c1 = 2 * i + 1;
+    if (c1 >= k) break;
+    int c = c1;
+    uint64_t vc = lds64(l + uint32_t(c1) * stride);
+    if (c1 + 1 < k) {
+      const uint64_t v2 = lds64(l + uint32_t(c1 + 1) * stride);
+      if (v2 < vc) { vc = v2; c = c1 + 1; }
+    }
+    if (vc >= key) break;
+    sts64(l + uint32_t(i) * stride, vc);
+    i = c;
   }
-  sts64(l + uint32_t(pos) * stride, key);
-  return lds64(l + uint32_t(k - 1) * stride);
+  sts64(l + uint32_t(i) * stride, key);
+  return lds64(l);
 }
 
 template <bool SEM, bool TRAJ>
@@ -173,7 +186,9 @@ __global__ void __launch_bounds__(kUmThreads, 1)
   uint64_t* lists = reinterpret_cast<uint64_t*>(smem + size_t(p.stages) * kUmStageBytes);   // [2][k][128] (KR == 0)
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  constexpr int NACC = (SEM ? 1 : 0) + (TRAJ ? 1 : 0);
+  // accumulators per tile: semantic + trajectory, or semantic K-halves when
+  // split_kb > 0 (second slot), else one
+  const int NACC = ((SEM && TRAJ) || p.split_kb > 0) ? 2 : 1;
   const int S = p.stages, AS = p.acc_stages;
 
   if (tid == 0) {
@@ -242,7 +257,7 @@ __global__ void __launch_bounds__(kUmThreads, 1)
         mbar_wait(&tempty[as], ((ti / unsigned(AS)) & 1u) ^ 1u);
         tc_fence_after();
         const uint32_t d_sem = tmem_base + uint32_t(as * NACC * UM_N);
-        const uint32_t d_trj = d_sem + (SEM ? UM_N : 0);
+        const uint32_t d_trj = d_sem + (NACC == 2 ? UM_N : 0);
         for (int kb = 0; kb < n_kb; ++kb, ++u) {
           const int s = int(u % unsigned(S));
           mbar_wait(&full[s], (u / unsigned(S)) & 1u);
@@ -250,10 +265,13 @@ __global__ void __launch_bounds__(kUmThreads, 1)
           const unsigned char* sa = smem + size_t(s) * kUmStageBytes;
           const unsigned char* sb = sa + kStageA;
           if (SEM && kb < p.n_sem_kb) {
+            const bool hi = !TRAJ && p.split_kb > 0 && kb >= p.split_kb;
+            const uint32_t d = hi ? d_trj : d_sem;
+            const int kb0 = hi ? p.split_kb : 0;
 #pragma unroll
             for (int kk = 0; kk < 4; ++kk)
-              tc_mma(d_sem, umma_desc(sa + kk * 32, 16, 1024, 2), umma_desc(sb + kk * 32, 16, 1024, 2), idesc,
-                     (kb | kk) ? 1u : 0u);
+              tc_mma(d, umma_desc(sa + kk * 32, 16, 1024, 2), umma_desc(sb + kk * 32, 16, 1024, 2), idesc,
+                     (kb != kb0 || kk) ? 1u : 0u);
           } else {
             const int j = kb - p.n_sem_kb;
             const int l0 = j * p.lc;
@@ -292,6 +310,7 @@ __global__ void __launch_bounds__(kUmThreads, 1)
     const float rqt = (TRAJ && live) ? p.rq_t[q] : 0.f;
     const float w = p.w, w1 = 1.f - p.w;
     const int k = p.k;
+    const bool split = p.split_kb > 0;
     constexpr int HC = UM_N / 2;                  // columns per half
     uint64_t* ml = lists + size_t(half) * k * UM_M + q;   // this thread's list: entry i at ml[i*128]
     const uint32_t ml_s = smem_u32(ml);
@@ -327,12 +346,12 @@ __global__ void __launch_bounds__(kUmThreads, 1)
       tc_fence_after();
       const uint32_t lane_addr = uint32_t(qd * 32) << 16;
       const uint32_t c_sem = tmem_base + lane_addr + uint32_t(as * NACC * UM_N + half * HC);
-      const uint32_t c_trj = c_sem + (SEM ? UM_N : 0);
+      const uint32_t c_trj = c_sem + (NACC == 2 ? UM_N : 0);
 #pragma unroll 1
       for (int c = 0; c < HC / 32; ++c) {
         uint32_t vs[32], vt[32];
         if (SEM) tc_ld32(c_sem + c * 32, vs);
-        if (TRAJ) tc_ld32(c_trj + c * 32, vt);
+        if (TRAJ || p.split_kb > 0) tc_ld32(c_trj + c * 32, vt);
         const float rec = c == 0 ? re_l[0] : c == 1 ? re_l[1] : c == 2 ? re_l[2] : re_l[3];
         const float rmc = c == 0 ? rm_l[0] : c == 1 ? rm_l[1] : c == 2 ? rm_l[2] : rm_l[3];
         const int64_t yc = int64_t(ybase) + c * 32;
@@ -345,7 +364,10 @@ __global__ void __launch_bounds__(kUmThreads, 1)
 #pragma unroll
         for (int j = 0; j < 32; ++j) {
           float v = 0.f;
-          if (SEM) v = w * (__uint_as_float(vs[j]) * rqs * __shfl_sync(0xffffffffu, rec, j));
+          if (SEM) {
+            const float dot = (!TRAJ && split) ? __uint_as_float(vs[j]) + __uint_as_float(vt[j]) : __uint_as_float(vs[j]);
+            v = w * (dot * rqs * __shfl_sync(0xffffffffu, rec, j));
+          }
           if (TRAJ) v = fmaf(w1, __uint_as_float(vt[j]) * rqt * __shfl_sync(0xffffffffu, rmc, j), v);
           sc[j] = v;
           m |= (v >= thr_s ? 1u : 0u) << j;
@@ -361,7 +383,7 @@ __global__ void __launch_bounds__(kUmThreads, 1)
             if (jj == j) v = sc[jj];
           const uint64_t key = pack_key(v, p.id_offset + uint32_t(yc + j));
           if (key > thr) {
-            thr = list_insert(ml_s, UM_M * 8, k, key);
+            thr = heap_replace_root(ml_s, UM_M * 8, k, key);
             thr_s = key_score(thr);
           }
         }
@@ -542,7 +564,13 @@ cudaError_t launch_umma(const UmmaLaunch& L, cudaStream_t s) {
   int S = int((225 * 1024 - 1024 - lists) / kUmStageBytes);
   p.stages = S > kUmMaxStages ? kUmMaxStages : S;
   if (p.stages < 2) return cudaErrorInvalidValue;
-  p.acc_stages = (sem && traj) ? 1 : 2;
+  // tcgen05 fp32 accumulation is not round-to-nearest per step: over D/16 = 256
+  // MMAs (D = 4096) the semantic dot drifted by ~1.4e-5 relative (measured,
+  // C5).  Splitting K over two accumulators halves the chain; the epilogue adds
+  // them in IEEE fp32.  (Blends weight the semantic part by d/L and their
+  // trajectory K is short, so they keep one accumulator per part.)
+  p.split_kb = (sem && !traj && p.n_sem_kb >= 16) ? p.n_sem_kb / 2 : 0;
+  p.acc_stages = (sem && traj) || p.split_kb > 0 ? 1 : 2;
   p.cap = in.cap;
   p.id_offset = in.id_offset;
   p.rq_s = rq_s;

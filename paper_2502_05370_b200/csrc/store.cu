@@ -42,6 +42,7 @@ struct fmoe_store {
   void* maps = nullptr;
   float* psq = nullptr;
   int64_t n = 0;
+  uint64_t gen = 0;       // bumped by every insert/write (invalidates trajectory sessions)
 
   StoreView view() const {
     StoreView v;
@@ -478,6 +479,7 @@ fmoe_status fmoe_store_insert(fmoe_store* st, int64_t B, const float* emb, const
     if (e != cudaSuccess) r = cuda_fail(e, "write launch");
   }
   if (r == FMOE_OK) st->n = n0 + a;
+  ++st->gen;
   return S.finish(r);
 }
 
@@ -506,6 +508,114 @@ fmoe_status fmoe_store_write(fmoe_store* st, int64_t B, const float* emb, const 
     w.slot_limit = st->n;
     cudaError_t e = launch_write_rows(w, s);
     if (e != cudaSuccess) r = cuda_fail(e, "write launch");
+  }
+  ++st->gen;
+  return S.finish(r);
+}
+
+}  // extern "C"
+
+struct fmoe_traj_session {
+  const fmoe_store* st;
+  int64_t B;
+  float* acc = nullptr;      // [B][cap]
+  double* qn = nullptr;      // [2][B]
+  int layer = 0;
+  uint64_t gen = 0;
+};
+
+extern "C" {
+
+fmoe_status fmoe_traj_session_create(const fmoe_store* st, int64_t B, fmoe_traj_session** out) {
+  if (!st || !out) return fail(FMOE_ERR_INVALID_ARG, "null argument");
+  if (B < 1 || B > FMOE_MAX_K) return fail(FMOE_ERR_INVALID_ARG, "1 <= B <= 64");
+  *out = nullptr;
+  DeviceGuard g(st->device);
+  fmoe_traj_session* s = new fmoe_traj_session();
+  s->st = st;
+  s->B = B;
+  s->gen = st->gen;
+  cudaError_t e;
+  if ((e = cudaMalloc(&s->acc, size_t(B) * st->cfg.capacity * 4)) != cudaSuccess ||
+      (e = cudaMalloc(&s->qn, size_t(2) * B * 8)) != cudaSuccess) {
+    fmoe_traj_session_destroy(s);
+    return cuda_fail(e, "session memory");
+  }
+  *out = s;
+  return FMOE_OK;
+}
+
+void fmoe_traj_session_destroy(fmoe_traj_session* s) {
+  if (!s) return;
+  DeviceGuard g(s->st->device);
+  cudaDeviceSynchronize();
+  cudaFree(s->acc);
+  cudaFree(s->qn);
+  delete s;
+}
+
+fmoe_status fmoe_traj_session_reset(fmoe_traj_session* s) {
+  if (!s) return fail(FMOE_ERR_INVALID_ARG, "null session");
+  s->layer = 0;
+  s->gen = s->st->gen;
+  return FMOE_OK;
+}
+
+fmoe_status fmoe_traj_session_step(fmoe_traj_session* ss, const float* q_layer, int32_t k, float* out_score,
+                                   int64_t* out_id, void* stream) {
+  if (!ss || !q_layer) return fail(FMOE_ERR_INVALID_ARG, "null argument");
+  const fmoe_store* st = ss->st;
+  if (ss->gen != st->gen) return fail(FMOE_ERR_INVALID_ARG, "store changed since the session was reset");
+  if (ss->layer >= st->cfg.L) return fail(FMOE_ERR_INVALID_ARG, "all L layers consumed; reset the session");
+  if (k < 1 || k > FMOE_MAX_K) return fail(FMOE_ERR_INVALID_ARG, "k must be in [1, 64]");
+  if (!out_score && !out_id) return fail(FMOE_ERR_INVALID_ARG, "no output");
+  const int64_t B = ss->B;
+  DeviceGuard g(st->device);
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  Staging S(s, st->device);
+  const float* dq = S.in(q_layer, size_t(B) * st->cfg.E);
+  float* ds = S.out(out_score, size_t(B) * k);
+  int64_t* di = S.out(out_id, size_t(B) * k);
+  fmoe_status r = S.check();
+  if (r == FMOE_OK && st->n == 0) {
+    cudaError_t e = launch_merge_keys(int(B), 0, k, nullptr, k, nullptr, ds, di, nullptr, s);
+    if (e != cudaSuccess) r = cuda_fail(e, "merge launch");
+  } else if (r == FMOE_OK) {
+    ScanArgs a{};
+    a.st = st->view();
+    a.n_rows = st->n;
+    a.ell = ss->layer + 1;
+    a.k = k;
+    a.id_offset = uint32_t(st->cfg.id_offset);
+    a.nq = int(B < 4 ? B : 4);
+    a.grid = traj_session_grid(a);
+    const int npass = int((B + 3) / 4);
+    char* buf = nullptr;
+    unsigned* counters = nullptr;
+    unsigned long long* best = nullptr;
+    r = stream_scratch(st, s, size_t(B) * a.grid * k * 8, npass, int(B), &buf, &counters, &best);
+    if (r == FMOE_OK) {
+      a.cand = reinterpret_cast<uint64_t*>(buf);
+      a.best = best;
+      a.out_score = ds;
+      a.out_id = di;
+      a.check_valid = 1;
+      a.trace = trace_buffer();
+      SessionArgs sa{};
+      sa.q_layer = dq;
+      sa.layer = ss->layer;
+      sa.acc = ss->acc;
+      sa.qn_prev = ss->qn + (ss->layer & 1) * B;
+      sa.qn_next = ss->qn + ((ss->layer + 1) & 1) * B;
+      for (int p = 0; p < npass && r == FMOE_OK; ++p) {
+        a.q0 = 4 * p;
+        a.nq = int(B - a.q0 < 4 ? B - a.q0 : 4);
+        a.counter = counters + p;
+        cudaError_t e = launch_traj_session(a, sa, s);
+        if (e != cudaSuccess) r = cuda_fail(e, "session launch");
+      }
+      if (r == FMOE_OK) ++ss->layer;
+    }
   }
   return S.finish(r);
 }

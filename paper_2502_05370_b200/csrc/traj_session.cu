@@ -1,0 +1,192 @@
+// traj_session.cu -- incremental trajectory search.
+//
+// A request observes its gate distributions layer by layer; after layer ell
+// the trajectory search (Eq. 2) scores the prefix 1..ell.  The
+// stateless call re-reads ell slabs per row; a session keeps, per query and
+// per stored row, the running dot product  acc[q][y] = sum_{l<ell} q_l . M_y,l
+// (fp32, the same sequential accumulation order as the stateless GEMV), so
+// step ell reads one 16..256-byte slab row + 4 bytes of accumulator per query
+// and writes the accumulator back:
+//   score = acc * r_q(ell) / sqrt(psq[ell-1][y])
+// with r_q(ell) from a running float64 sum of the query's squared entries and
+// psq the store's prefix squared-norm table.  The result is Eq. 2 at prefix ell
+// (summation order differs only in the prefix norm, taken from the table).
+//
+// Mapping: GT lanes per row (GT = 16-byte chunks per slab row, power of two),
+// 32/GT rows per pass, PASSES passes per warp iteration so a lane keeps 8
+// slab loads in flight; fused top-k via merge.cuh.
+#include "common.cuh"
+#include "kernels.cuh"
+#include "merge.cuh"
+
+namespace fmoe {
+
+constexpr int kSessThreads = 256;
+constexpr int kSessWarps = kSessThreads / 32;
+constexpr int kPasses = 8;
+
+template <class Tag>
+__device__ __forceinline__ void unpack_sess(const uint4& u, float (&x)[8]) {
+  if constexpr (StoreT<Tag>::kBytes == 2) {
+    unpack8(u, x, Bf16Tag());
+  } else {
+    x[0] = __uint_as_float(u.x); x[1] = __uint_as_float(u.y);
+    x[2] = __uint_as_float(u.z); x[3] = __uint_as_float(u.w);
+    x[4] = x[5] = x[6] = x[7] = 0.f;
+  }
+}
+
+__device__ __forceinline__ int pow2_at_least(int c) {
+  int g = 1;
+  while (g < c) g <<= 1;
+  return g;
+}
+
+template <class Tag, int NQ, int KPL>
+__global__ void __launch_bounds__(kSessThreads, NQ == 1 ? 4 : 2) traj_session_kernel(const ScanArgs a, SessionArgs s) {
+  using ST = StoreT<Tag>;
+  constexpr int EP = ST::kElemsPer16B;
+  constexpr int SB = ST::kBytes;
+  __shared__ __align__(16) float qs[NQ][kMaxE];   // layer ell-1 of the queries (store dtype values)
+  __shared__ double red[kSessWarps][NQ];
+  __shared__ float rq[NQ];
+  __shared__ int s_valid[NQ];
+  __shared__ int s_last;
+  __shared__ __align__(16) uint64_t sk[kSessWarps * NQ * kMaxK];
+
+  const StoreView& st = a.st;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int Ep = st.Ep, E = st.E, layer = s.layer;   // 0-based layer consumed by this step
+  trace_mark(a.trace, 0);
+  pdl_wait();
+  trace_mark(a.trace, 1);
+
+  // ---- the new layer of each query, and the running query norm
+  double part[NQ];
+#pragma unroll
+  for (int q = 0; q < NQ; ++q) {
+    part[q] = 0.0;
+    for (int j = tid; j < kMaxE; j += kSessThreads) {
+      float v = 0.f;
+      if (q < a.nq && j < E) v = to_store_value(s.q_layer[int64_t(a.q0 + q) * E + j], Tag());
+      qs[q][j] = v;
+      part[q] += double(v) * double(v);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) part[q] += __shfl_xor_sync(0xffffffffu, part[q], o);
+    if (lane == 0) red[warp][q] = part[q];
+  }
+  __syncthreads();
+  if (tid < NQ) {
+    double t = layer > 0 ? s.qn_prev[a.q0 + tid] : 0.0;
+    for (int w = 0; w < kSessWarps; ++w) t += red[w][tid];
+    rq[tid] = t > 0.0 ? float(1.0 / sqrt(t)) : 0.f;
+    s_valid[tid] = t > 0.0;
+    if (blockIdx.x == 0 && tid < a.nq) s.qn_next[a.q0 + tid] = t;   // double-buffered: others read qn_prev
+  }
+  __syncthreads();
+  trace_mark(a.trace, 2);
+  float rq_r[NQ];
+#pragma unroll
+  for (int q = 0; q < NQ; ++q) rq_r[q] = rq[q];
+
+  WarpTopK<KPL> lists[NQ];
+#pragma unroll
+  for (int q = 0; q < NQ; ++q) lists[q].init();
+
+  const int CPY = Ep / EP;                      // 16-byte chunks per slab row
+  const int GT = pow2_at_least(CPY);
+  const int rpp = 32 / GT, g = lane / GT, cl = lane % GT;
+  const bool lead = cl == 0;
+  const int64_t n = a.n_rows, cap = st.cap;
+  const char* slab = static_cast<const char*>(st.maps) + int64_t(layer) * cap * Ep * SB;
+  const float* psq = st.psq + int64_t(layer) * cap;
+  const int64_t rows_per_iter = int64_t(rpp) * kPasses;
+  const int64_t nw = int64_t(gridDim.x) * kSessWarps;
+  const int64_t wg = int64_t(blockIdx.x) * kSessWarps + warp;
+
+  for (int64_t base = wg * rows_per_iter; base < n; base += nw * rows_per_iter) {
+    uint4 buf[kPasses];
+#pragma unroll
+    for (int p = 0; p < kPasses; ++p) {
+      const int64_t row = base + p * rpp + g;
+      buf[p] = (row < n && cl < CPY) ? ld_stream(slab + row * Ep * SB + cl * 16) : make_uint4(0u, 0u, 0u, 0u);
+    }
+    float accv[kPasses][NQ], ps[kPasses];
+#pragma unroll
+    for (int p = 0; p < kPasses; ++p) {
+      const int64_t row = base + p * rpp + g;
+      const bool ok = lead && row < n;
+      ps[p] = ok ? __ldcs(psq + row) : 0.f;
+#pragma unroll
+      for (int q = 0; q < NQ; ++q)
+        accv[p][q] = (ok && layer > 0 && q < a.nq) ? __ldcs(s.acc + int64_t(a.q0 + q) * cap + row) : 0.f;
+    }
+#pragma unroll
+    for (int p = 0; p < kPasses; ++p) {
+      float x[8];
+      unpack_sess<Tag>(buf[p], x);
+      float d[NQ];
+#pragma unroll
+      for (int q = 0; q < NQ; ++q) {
+        d[q] = 0.f;
+        if (cl < CPY) {
+#pragma unroll
+          for (int e = 0; e < EP; ++e) d[q] = fmaf(x[e], qs[q][cl * EP + e], d[q]);
+        }
+        for (int o = GT >> 1; o > 0; o >>= 1) d[q] += __shfl_xor_sync(0xffffffffu, d[q], o);
+      }
+      const int64_t row = base + p * rpp + g;
+      const bool ok = lead && row < n;
+      const float rm = ps[p] > 0.f ? rsqrtf(ps[p]) : 0.f;
+#pragma unroll
+      for (int q = 0; q < NQ; ++q) {
+        const float acc = accv[p][q] + d[q];
+        if (ok && q < a.nq) __stcs(s.acc + int64_t(a.q0 + q) * cap + row, acc);
+        const float sc = acc * rq_r[q] * rm;
+        lists[q].offer(ok ? pack_key(sc, a.id_offset + uint32_t(row)) : 0ull, a.k);
+      }
+    }
+  }
+  trace_mark(a.trace, 3);
+  pdl_trigger();
+  finish_topk<NQ, KPL, kSessWarps>(lists, sk, a, s_valid, &s_last);
+}
+
+cudaError_t launch_traj_session(const ScanArgs& a, const SessionArgs& s, cudaStream_t stream) {
+  using Fn = void (*)(const ScanArgs, SessionArgs);
+  Fn fn;
+  const int NQ = a.nq <= 1 ? 1 : (a.nq <= 2 ? 2 : 4);
+  const int kp = a.k == 1 ? 0 : (a.k <= 32 ? 1 : 2);
+#define FMOE_SESS_PICK(TAG)                                                                          \
+  if (NQ == 1) fn = kp == 0 ? traj_session_kernel<TAG, 1, 0> : kp == 1 ? traj_session_kernel<TAG, 1, 1> \
+                                                                        : traj_session_kernel<TAG, 1, 2>; \
+  else if (NQ == 2) fn = kp == 0 ? traj_session_kernel<TAG, 2, 0> : kp == 1 ? traj_session_kernel<TAG, 2, 1> \
+                                                                             : traj_session_kernel<TAG, 2, 2>; \
+  else fn = kp == 0 ? traj_session_kernel<TAG, 4, 0> : kp == 1 ? traj_session_kernel<TAG, 4, 1>           \
+                                                              : traj_session_kernel<TAG, 4, 2>;
+  if (a.st.bf16) { FMOE_SESS_PICK(Bf16Tag) } else { FMOE_SESS_PICK(F32Tag) }
+#undef FMOE_SESS_PICK
+  count_launch();
+  return launch_pdl(fn, dim3(a.grid), dim3(kSessThreads), 0, stream, a, s);
+}
+
+int traj_session_grid(const ScanArgs& a) {
+  static int sms = 0;
+  if (!sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  }
+  const int esz = a.st.bf16 ? 2 : 4;
+  int cpy = a.st.Ep * esz / 16, gt = 1;
+  while (gt < cpy) gt <<= 1;
+  const int64_t rows_per_iter = int64_t(32 / gt) * kPasses;
+  const int64_t want = (a.n_rows + rows_per_iter * kSessWarps - 1) / (rows_per_iter * kSessWarps);
+  // one wave, and (N = 1M, B = 1) about one iteration per warp: 4 CTAs/SM
+  const int64_t full = int64_t(a.nq <= 1 ? 4 : 2) * sms;
+  const int64_t gsz = want < full ? want : full;
+  return int(gsz < 1 ? 1 : gsz);
+}
+
+}  // namespace fmoe

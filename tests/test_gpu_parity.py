@@ -284,3 +284,41 @@ def test_batched_tcgen05(setup, B, k, mode):
         trj = O.trajectory_scores(O.quantize(qp.numpy(), dt), setup["Qm"], ell)
         ref = O.blend_scores(sem, trj, np.float64(np.float32(3 / sh.L)))
     check_topk(gs, gi, ref, k)
+
+
+# ---------------------------------------------------------------- incremental trajectory session
+@pytest.mark.parametrize("B,k", [(1, 1), (3, 8), (6, 33)])
+def test_trajectory_session_equals_eq2_at_every_prefix(setup, B, k):
+    st, dt, sh = setup["st"], setup["dtype"], setup["shape"]
+    qm = setup["q_maps"][:B]
+    sess = st.trajectory_session(B)
+    try:
+        for ell in range(1, sh.L + 1):
+            gs, gi = sess.step(qm[:, ell - 1].contiguous().cuda(), k)
+            if ell in (1, 2, 3, 8, sh.L) or ell % 7 == 0:
+                ref = O.trajectory_scores(O.quantize(qm[:, :ell].numpy(), dt), setup["Qm"], ell)
+                check_topk(gs, gi, ref, k)
+        with pytest.raises(setup["lib"].FmoeError):          # all L layers consumed
+            sess.step(qm[:, 0].contiguous().cuda(), k)
+        sess.reset()
+        gs, gi = sess.step(qm[:, 0].contiguous().cuda(), k)   # prefix 1 again
+        check_topk(gs, gi, O.trajectory_scores(O.quantize(qm[:, :1].numpy(), dt), setup["Qm"], 1), k)
+    finally:
+        sess.close()
+
+
+def test_trajectory_session_invalidated_by_insert(lib):
+    sh = SHAPES["mixtral_tiny"]
+    emb, maps, _ = S.store_rows(sh, 3, 0, 40)
+    st = lib.ExpertMapStore(sh.L, sh.E, sh.K, sh.D, 3, 64, "bf16")
+    st.insert(emb[:30].cuda(), maps[:30].cuda())
+    sess = st.trajectory_session(1)
+    sess.step(maps[:1, 0].contiguous().cuda(), 1)
+    st.insert(emb[30:].cuda(), maps[30:].cuda())
+    with pytest.raises(lib.FmoeError):
+        sess.step(maps[:1, 1].contiguous().cuda(), 1)
+    sess.reset()
+    s, i = sess.step(maps[35:36, 0].contiguous().cuda(), 1)
+    assert i.item() in range(40)
+    sess.close()
+    st.close()

@@ -80,6 +80,16 @@ def main():
         pre = qm[:, :ell].contiguous()
         us = timeit(lambda: fm.fmoe_search_trajectory(st._h, pre, ell, a.k, out_s, out_i))
         print(f"traj ell={ell:2d}: {us:8.2f} us  {a.n * ell * a.E * s / us / 1e3:8.1f} GB/s  host {getattr(timeit, 'host_us', 0):.1f} us/call")
+    sess = fm.fmoe_traj_session_create(st._h, a.B)
+    lay = qm[:, 0].contiguous()
+
+    def sweep():
+        fm.fmoe_traj_session_reset(sess)
+        for ell in range(1, a.L):
+            fm.fmoe_traj_session_step(sess, lay, a.k, out_s, out_i)
+    us = timeit(sweep, reps=5, warm=2)
+    print(f"session sweep ell=1..{a.L - 1}: {us:8.2f} us ({us / (a.L - 1):.2f} us/step)")
+    fm.fmoe_traj_session_destroy(sess)
     us = timeit(lambda: fm.fmoe_search_semantic(st._h, qe, a.k, out_s, out_i), reps=50)
     print(f"semantic   : {us:8.2f} us  {a.n * a.D * s / us / 1e3:8.1f} GB/s")
     pre = qm.contiguous()

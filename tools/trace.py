@@ -41,7 +41,20 @@ def main():
     out_s = torch.empty(a.B, a.k, device="cuda")
     out_i = torch.empty(a.B, a.k, dtype=torch.int64, device="cuda")
 
+    sess = fm.fmoe_traj_session_create(st._h, a.B) if a.mode == "session" else None
+    lay = qm[:, 0].contiguous()
+
     def call():
+        if a.mode == "session":
+            fm.fmoe_traj_session_reset(sess)
+            for _ in range(a.ell - 1):
+                fm.fmoe_traj_session_step(sess, lay, a.k, out_s, out_i)
+            torch.cuda.synchronize()
+            if lib.fmoe_debug_trace(-1, None, 0) == 0 and getattr(call, "arm", False):
+                lib.fmoe_debug_trace(1, None, 0)
+                ev0.record()
+            fm.fmoe_traj_session_step(sess, lay, a.k, out_s, out_i)
+            return
         if a.mode == "traj":
             fm.fmoe_search_trajectory(st._h, pre, a.ell, a.k, out_s, out_i)
         else:
@@ -49,9 +62,12 @@ def main():
     for _ in range(5):
         call()
     torch.cuda.synchronize()
-    lib.fmoe_debug_trace(1, None, 0)
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    ev0.record()
+    if a.mode == "session":
+        call.arm = True
+    else:
+        lib.fmoe_debug_trace(1, None, 0)
+        ev0.record()
     call()
     ev1.record()
     torch.cuda.synchronize()
