@@ -41,8 +41,13 @@ WORKLOADS = {
     "C2": dict(shape=S.MIXTRAL, N=1_000_000, B=1, k=1, dtype="bf16", delta=-1.0),
     # configs[2]: Qwen1.5-MoE shape, N = 1M, batch 64, top-8
     "C3": dict(shape=S.QWEN, N=1_000_000, B=64, k=8, dtype="bf16", delta=-1.0),
-    # configs[3]: Phi-3.5-MoE shape, N = 4M, blend + insert at full capacity (B = 64)
-    "C4": dict(shape=S.PHI, N=4_000_000, B=64, k=8, dtype="bf16", delta=-1.0),
+    # configs[3]: Phi-3.5-MoE shape, N = 4M, blended searches (ell = 16, 31; SURVEY §8 C4
+    # proposal) + insert of the batch at full capacity (B = 64)
+    "C4": dict(shape=S.PHI, N=4_000_000, B=64, k=8, dtype="bf16", delta=-1.0, kind="blend", ells=(16, 31),
+               insert=64),
+    # configs[4] at 1 GPU: Mixtral shape, N = 16M, B = 256, blend at ell = 31, insert of 64 contexts
+    "C5": dict(shape=S.MIXTRAL, N=16_000_000, B=256, k=8, dtype="bf16", delta=-1.0, kind="blend", ells=(31,),
+               insert=64),
     # configs[0]: tiny Mixtral-shaped store (correctness config)
     "C1": dict(shape=S.TINY, N=1000, B=1, k=1, dtype="f32", delta=0.9),
 }
@@ -59,6 +64,8 @@ def parse():
                    help="trajectory sweep: incremental session (SURVEY §8(f) #1) or one stateless search per prefix")
     p.add_argument("--no-graph", dest="graph", action="store_false",
                    help="time eager launches instead of a CUDA-graph replay of the step")
+    p.add_argument("--no-cos", dest="cos", action="store_false",
+                   help="insert with a full RDY scan instead of reusing the semantic search's cosines")
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--seed", type=int, default=S.BASE_SEED + 1)
@@ -69,12 +76,15 @@ def parse():
 def step_counts(cfg):
     sh = cfg["shape"]
     B = cfg["B"]
+    if cfg.get("kind") == "blend":
+        n_traj = len(cfg["ells"])
+        return B * (1 + n_traj) + cfg["insert"], n_traj
     n_traj = sh.L - 1
     searches = B * (1 + n_traj + 1)
     return searches, n_traj
 
 
-def algorithmic_bytes(cfg, N, traj_mode="stateless"):
+def algorithmic_bytes(cfg, N, traj_mode="stateless", use_cos=False):
     """bytes a scan must stream per launch (store tiles only).
     Session step ell: slab ell-1, the prefix-norm row, and the per-query running
     dot product (read from step 2 on, written every step)."""
@@ -82,11 +92,19 @@ def algorithmic_bytes(cfg, N, traj_mode="stateless"):
     s = 2 if cfg["dtype"] == "bf16" else 4
     sem = N * sh.D * s
     B = cfg["B"]
-    if traj_mode == "session":
+    if cfg.get("kind") == "blend":
+        traj = {ell: N * (sh.D + ell * sh.E) * s for ell in cfg["ells"]}
+    elif traj_mode == "session":
         traj = {ell: N * (sh.E * s + 4 + 4 * B * (2 if ell > 1 else 1)) for ell in range(1, sh.L)}
     else:
         traj = {ell: N * ell * sh.E * s for ell in range(1, sh.L)}
     rdy = N * (sh.D * s + sh.L * sh.E * s)
+    if use_cos:
+        # the semantic search also writes its B cosines per row; the RDY scan reads
+        # the maps and the inserted rows' cosines instead of the embeddings
+        nb = cfg.get("insert", B)
+        sem += N * 4 * B
+        rdy = N * (sh.L * sh.E * s + 4 * nb)
     return sem, traj, rdy
 
 
@@ -145,10 +163,28 @@ def build_store(fm, cfg, N_local, offset, dev, seed):
 class Step:
     """One matcher iteration (see module docstring) on a (possibly sharded) store."""
 
-    def __init__(self, fm, st, cfg, traj_mode="stateless"):
+    def __init__(self, fm, st, cfg, traj_mode="stateless", use_cos=True):
         self.fm, self.st, self.cfg = fm, st, cfg
         self.sh = cfg["shape"]
         self.sess = fm.fmoe_traj_session_create(st._h, cfg["B"]) if traj_mode == "session" else None
+        # semantic cosines kept on the device for the RDY insert (fmoe_store_insert_cos):
+        # the iteration's new context carries the embedding its semantic search used
+        n = len(st)
+        self.stride = (n + 3) // 4 * 4
+        self.cos = (torch.empty(cfg["B"], self.stride, device=st.device)
+                    if use_cos and cfg["B"] * self.stride * 4 <= (4 << 30) else None)
+
+    def semantic(self, h, q_emb, k, out_s, out_i):
+        if self.cos is not None:
+            self.fm.fmoe_search_semantic_cos(h, q_emb, k, out_s, out_i, self.cos, self.stride)
+        else:
+            self.fm.fmoe_search_semantic(h, q_emb, k, out_s, out_i)
+
+    def insert(self, h, ne, nm):
+        if self.cos is not None:
+            self.fm.fmoe_store_insert_cos(h, ne, nm, self.cos, self.stride, None, None)
+        else:
+            self.fm.fmoe_store_insert(h, ne, nm, None, None)
 
     def run(self, q_emb, q_maps, new_emb, new_maps, ev=None):
         """ev: optional dict kind -> list of (start, end) CUDA events around the searches."""
@@ -173,12 +209,25 @@ class Step:
             b.record()
             ev.setdefault(kind, []).append((a, b))
 
-        rec("semantic", lambda: fm.fmoe_search_semantic(h, q_emb, k, out_s, out_i))
+        rec("semantic", lambda: self.semantic(h, q_emb, k, out_s, out_i))
         top_i = out_i[:, 0].contiguous()
         top_s = out_s[:, 0].contiguous()
         fm.fmoe_select_experts(h, top_i, top_s, cfg["delta"], 0, d, mask, cnt)
         m1 = torch.empty(B, 1, dtype=torch.int64, device=dev)
         c1 = torch.empty(B, 1, dtype=torch.int32, device=dev)
+        if cfg.get("kind") == "blend":
+            # blended searches (RDY weighting, w = d/L) at the configured prefixes
+            for ell in cfg["ells"]:
+                pre, _ = q_maps[ell - 1]
+                rec(f"traj{ell}", lambda: fm.fmoe_search_blend(h, q_emb, pre, ell, -1.0, k, out_s, out_i))
+                tgt = ell - 1 + d
+                if tgt < L:
+                    top_i = out_i[:, 0].contiguous()
+                    top_s = out_s[:, 0].contiguous()
+                    fm.fmoe_select_experts(h, top_i, top_s, cfg["delta"], tgt, tgt + 1, m1, c1)
+            nb = cfg["insert"]
+            rec("rdy_insert", lambda: self.insert(h, new_emb[:nb].contiguous(), new_maps[:nb].contiguous()))
+            return
         if self.sess is not None:
             fm.fmoe_traj_session_reset(self.sess)        # the store changed at the last insert
         for ell in range(1, L):
@@ -192,15 +241,15 @@ class Step:
                 top_i = out_i[:, 0].contiguous()
                 top_s = out_s[:, 0].contiguous()
                 fm.fmoe_select_experts(h, top_i, top_s, cfg["delta"], tgt, tgt + 1, m1, c1)
-        rec("rdy_insert", lambda: fm.fmoe_store_insert(h, new_emb, new_maps, None, None))
+        rec("rdy_insert", lambda: self.insert(h, new_emb, new_maps))
 
 
 class HostStep(Step):
     """The same step through the C ABI with host (pinned) buffers: the library
     stages inputs H2D and outputs D2H inside the timed region."""
 
-    def __init__(self, fm, st, cfg, traj_mode="stateless"):
-        super().__init__(fm, st, cfg, traj_mode)
+    def __init__(self, fm, st, cfg, traj_mode="stateless", use_cos=True):
+        super().__init__(fm, st, cfg, traj_mode, use_cos)
         B, k, d = cfg["B"], cfg["k"], 3
         pin = lambda *shape, dtype=torch.float32: torch.empty(*shape, dtype=dtype).pin_memory()
         self.out_s, self.out_i = pin(B, k), pin(B, k, dtype=torch.int64)
@@ -213,9 +262,20 @@ class HostStep(Step):
         k, d, L = cfg["k"], 3, self.sh.L
         h = self.st._h
         out_s, out_i, top_s, top_i = self.out_s, self.out_i, self.top_s, self.top_i
-        fm.fmoe_search_semantic(h, q_emb, k, out_s, out_i)
+        self.semantic(h, q_emb, k, out_s, out_i)      # cosines stay in device memory
         top_s.copy_(out_s[:, 0]); top_i.copy_(out_i[:, 0])
         fm.fmoe_select_experts(h, top_i, top_s, cfg["delta"], 0, d, self.mask, self.cnt)
+        if cfg.get("kind") == "blend":
+            for ell in cfg["ells"]:
+                pre, _ = q_maps[ell - 1]
+                fm.fmoe_search_blend(h, q_emb, pre, ell, -1.0, k, out_s, out_i)
+                tgt = ell - 1 + d
+                if tgt < L:
+                    top_s.copy_(out_s[:, 0]); top_i.copy_(out_i[:, 0])
+                    fm.fmoe_select_experts(h, top_i, top_s, cfg["delta"], tgt, tgt + 1, self.m1, self.c1)
+            nb = cfg["insert"]
+            self.insert(h, new_emb[:nb].contiguous(), new_maps[:nb].contiguous())
+            return float(out_s[0, 0])
         if self.sess is not None:
             fm.fmoe_traj_session_reset(self.sess)
         for ell in range(1, L):
@@ -228,12 +288,19 @@ class HostStep(Step):
             if tgt < L:
                 top_s.copy_(out_s[:, 0]); top_i.copy_(out_i[:, 0])
                 fm.fmoe_select_experts(h, top_i, top_s, cfg["delta"], tgt, tgt + 1, self.m1, self.c1)
-        fm.fmoe_store_insert(h, new_emb, new_maps, None, None)
+        self.insert(h, new_emb, new_maps)
         return float(out_s[0, 0])
 
     @staticmethod
     def bytes_per_step(cfg, B, traj_mode="stateless"):
         sh, k, d, L = cfg["shape"], cfg["k"], 3, cfg["shape"].L
+        if cfg.get("kind") == "blend":
+            nb, ells = cfg["insert"], cfg["ells"]
+            h2d = B * sh.D * 4 + sum(B * (sh.D + ell * sh.E) * 4 for ell in ells) + nb * (sh.D + L * sh.E) * 4
+            n_sel = 1 + sum(1 for ell in ells if ell - 1 + d < L)
+            h2d += n_sel * B * 12
+            d2h = (1 + len(ells)) * B * k * 12 + B * d * 12 + (n_sel - 1) * B * 12
+            return h2d, d2h
         traj_in = sum(B * (1 if traj_mode == "session" else ell) * sh.E * 4 for ell in range(1, L))
         h2d = B * sh.D * 4 + traj_in + B * (sh.D + L * sh.E) * 4
         n_sel = 1 + sum(1 for ell in range(1, L) if ell - 1 + d < L)
@@ -250,8 +317,8 @@ def make_queries(cfg, N, pool, seed, dev):
     for p in range(pool):
         qe, qm, _ = S.queries(sh, seed + 101 * p, N, B, device=dev)
         pre = [(qm[:, :ell].contiguous(), qm[:, ell - 1].contiguous()) for ell in range(1, sh.L)]
-        ne, nm, _ = S.store_rows(sh, seed + 7, N + p * B, B, device=dev)   # the iteration's new contexts
-        qs.append((qe.contiguous(), pre, ne.contiguous(), nm.contiguous()))
+        # the iteration's new context = its own semantic embedding + its full gate map
+        qs.append((qe.contiguous(), pre, qe.contiguous(), qm.contiguous()))
     return qs
 
 
@@ -319,11 +386,12 @@ def run_fmoe(args, cfg, rank, world, local_rank):
         st = build_store(fm, cfg, N_local, 0, dev, args.seed)
         if cfg["B"] > 4:
             args.traj = "stateless"    # the session kernel is the B <= 4 streaming path; batches use tcgen05
-        step = Step(fm, st, cfg, args.traj)
+        step = Step(fm, st, cfg, args.traj, args.cos)
     pool = 4
     qs = make_queries(cfg, N_total, pool, args.seed, dev)
     searches, n_traj = step_counts(cfg)
-    sem_b, traj_b, rdy_b = algorithmic_bytes(cfg, N_local, args.traj if world == 1 else "stateless")
+    sem_b, traj_b, rdy_b = algorithmic_bytes(cfg, N_local, args.traj if world == 1 else "stateless",
+                                             getattr(step, "cos", None) is not None)
 
     use_graph = args.graph and world == 1
     run_stream = torch.cuda.Stream(device=dev) if use_graph else torch.cuda.current_stream(dev)
@@ -414,7 +482,7 @@ def run_fmoe(args, cfg, rank, world, local_rank):
         for qe, pre, ne, nm in qs:
             hq.append((qe.cpu().pin_memory(), [(p.cpu().pin_memory(), l.cpu().pin_memory()) for p, l in pre],
                        ne.cpu().pin_memory(), nm.cpu().pin_memory()))
-        hstep = HostStep(fm, st, cfg, args.traj)
+        hstep = HostStep(fm, st, cfg, args.traj, args.cos)
         for w in range(2):
             hstep.run(*hq[w % pool])
         torch.cuda.synchronize()
@@ -460,14 +528,24 @@ def oracle_step_sample(cfg, seed, n_sample, budget_s=15.0, max_steps=50):
     store = O.Store(n_sample, L, sh.E, sh.D, d)
     store.insert(O.quantize(emb.numpy(), dt), O.quantize(maps.numpy(), dt))
     qe, qm, _ = S.queries(sh, seed, n_sample, B)
-    ne, nm, _ = S.store_rows(sh, seed + 7, n_sample, B)
     qe, qm = O.quantize(qe.numpy(), dt), O.quantize(qm.numpy(), dt)
-    ne, nm = O.quantize(ne.numpy(), dt), O.quantize(nm.numpy(), dt)
+    ne, nm = qe, qm                      # the iteration's own context is inserted (as in the fMoE arm)
     searches, _ = step_counts(cfg)
     steps, t0 = 0, time.perf_counter()
     while True:
         s, i = store.search(qe, None, 0, 1.0, k)
         O.select_experts(store.maps, i[:, 0].tolist(), s[:, 0].tolist(), cfg["delta"], list(range(d)), sh.K)
+        if cfg.get("kind") == "blend":
+            for ell in cfg["ells"]:
+                s, i = store.search(qe, qm, ell, d / L, k)
+                if ell - 1 + d < L:
+                    O.select_experts(store.maps, i[:, 0].tolist(), s[:, 0].tolist(), cfg["delta"], [ell - 1 + d], sh.K)
+            store.insert(ne[:cfg["insert"]], nm[:cfg["insert"]])
+            steps += 1
+            el = time.perf_counter() - t0
+            if el >= budget_s or steps >= max_steps:
+                break
+            continue
         for ell in range(1, L):
             s, i = store.search(None, qm, ell, 0.0, k)
             if ell - 1 + d < L:
@@ -508,10 +586,14 @@ def main():
     local_rank = int(os.environ.get("LOCAL_RANK", 0))
     searches, n_traj = step_counts(cfg)
     sh = cfg["shape"]
+    what = (f"semantic + blend (w=d/L) at ell={','.join(map(str, cfg['ells']))} + select + RDY insert of "
+            f"{cfg['insert']} contexts" if cfg.get("kind") == "blend" else
+            f"semantic + trajectory ell=1..{sh.L - 1} + select + RDY insert of the batch")
     base_config = {"workload": f"{args.config}: {sh.name} store N={cfg['N']} maps, L={sh.L}, E={sh.E}, D={sh.D}, "
-                               f"batch {cfg['B']}, semantic + trajectory ell=1..{sh.L - 1} + select + RDY insert at "
-                               f"full capacity", "N": cfg["N"], "L": sh.L, "E": sh.E, "D": sh.D, "B": cfg["B"],
+                               f"batch {cfg['B']}, {what} at full capacity", "N": cfg["N"], "L": sh.L, "E": sh.E, "D": sh.D, "B": cfg["B"],
                    "k": cfg["k"], "store_dtype": cfg["dtype"], "searches_per_step": searches,
+                   "insert": ("RDY semantic half reused from the step's semantic search (fmoe_store_insert_cos)"
+                              if args.cos and world == 1 else "full RDY scan"),
                    "trajectory": ("incremental session: step ell reads slab ell + running dots (SURVEY §8(f) #1)"
                                   if args.traj == "session" and world == 1 and cfg["B"] <= 4 else
                                   "stateless: one search over the whole prefix per ell"),

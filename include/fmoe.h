@@ -110,6 +110,19 @@ fmoe_status fmoe_store_get_config(const fmoe_store* store, fmoe_store_config* ou
 fmoe_status fmoe_store_insert(fmoe_store* store, int64_t B, const float* emb, const float* maps,
                               int64_t* out_slot, int64_t* out_replaced, void* stream);
 
+/* As fmoe_store_insert, with the semantic half of RDY supplied by the caller:
+ * sem_cos [B][cos_stride] fp32 holds cos(emb_x, sem_y) for every context y
+ * currently in the store (columns [0, size)), e.g. the out_cos of
+ * fmoe_search_semantic_cos run on the same embeddings since the last insert.
+ * An iteration's context carries the embedding its semantic search used
+ * (P:459-461), so the RDY scan then reads only the maps instead of
+ * the embeddings again.  Results are identical to fmoe_store_insert when
+ * sem_cos holds those cosines; the caller guarantees that.  sem_cos NULL =
+ * fmoe_store_insert.  cos_stride >= size. */
+fmoe_status fmoe_store_insert_cos(fmoe_store* store, int64_t B, const float* emb, const float* maps,
+                                  const float* sem_cos, int64_t cos_stride, int64_t* out_slot,
+                                  int64_t* out_replaced, void* stream);
+
 /* Overwrite existing contexts at explicit slots (the write half of an insert;
  * used by the sharded insert, SURVEY §8(e), and to restore a snapshot).
  * emb [B][D], maps [B][L][E] fp32, slot [B] int64 GLOBAL ids.  Rows whose slot
@@ -132,6 +145,14 @@ fmoe_status fmoe_store_read(const fmoe_store* store, int64_t slot_begin, int64_t
  * 1 <= k <= FMOE_MAX_K.  A zero-norm query row gets (NaN, -1). */
 fmoe_status fmoe_search_semantic(const fmoe_store* store, int64_t B, const float* q_emb, int32_t k,
                                  float* out_score, int64_t* out_id, void* stream);
+
+/* fmoe_search_semantic that also writes every cosine: out_cos [B][cos_stride]
+ * fp32, column y = score_{x,y} of Eq. 1 for the contexts y in [0, size);
+ * cos_stride >= size (a multiple of 4 keeps the writes vectorised).  Feeds
+ * fmoe_store_insert_cos. */
+fmoe_status fmoe_search_semantic_cos(const fmoe_store* store, int64_t B, const float* q_emb, int32_t k,
+                                     float* out_score, int64_t* out_id, float* out_cos, int64_t cos_stride,
+                                     void* stream);
 
 /* Trajectory search, Eq. 2: score_{x,y} = cos(flat(q_x[0:ell]),
  * flat(map_y[0:ell])) over the ell*E entries of the observed prefix (Reading

@@ -51,6 +51,8 @@ def _load():
         "fmoe_store_insert": (I32, [P, I64, P, P, P, P, P]),
         "fmoe_store_read": (I32, [P, I64, I64, P, P, P]),
         "fmoe_store_write": (I32, [P, I64, P, P, P, P]),
+        "fmoe_store_insert_cos": (I32, [P, I64, P, P, P, I64, P, P, P]),
+        "fmoe_search_semantic_cos": (I32, [P, I64, P, I32, P, P, P, I64, P]),
         "fmoe_resolve_victims": (I32, [I64, I32, P, P, ctypes.c_int, P]),
         "fmoe_search_semantic": (I32, [P, I64, P, I32, P, P, P]),
         "fmoe_search_trajectory": (I32, [P, I64, P, I32, I32, P, P, P]),
@@ -74,7 +76,8 @@ def _load():
 
 _lib = _load()
 ABI_SYMBOLS = ("fmoe_store_create", "fmoe_store_destroy", "fmoe_store_size", "fmoe_store_get_config",
-               "fmoe_store_insert", "fmoe_store_read", "fmoe_store_write", "fmoe_resolve_victims", "fmoe_search_semantic", "fmoe_search_trajectory",
+               "fmoe_store_insert", "fmoe_store_insert_cos", "fmoe_search_semantic_cos", "fmoe_store_read",
+               "fmoe_store_write", "fmoe_resolve_victims", "fmoe_search_semantic", "fmoe_search_trajectory",
                "fmoe_search_blend", "fmoe_select_experts", "fmoe_traj_session_create", "fmoe_traj_session_step",
                "fmoe_traj_session_reset", "fmoe_traj_session_destroy", "fmoe_topk_merge", "fmoe_status_string",
                "fmoe_last_error", "fmoe_kernel_launch_count")
@@ -127,6 +130,16 @@ def fmoe_store_size(h) -> int:
 def fmoe_store_insert(h, emb, maps, out_slot=None, out_replaced=None, stream=None):
     _check(_lib.fmoe_store_insert(h, emb.shape[0], _ptr(_f32(emb)), _ptr(_f32(maps)), _ptr(out_slot),
                                   _ptr(out_replaced), _stream(stream)))
+
+
+def fmoe_store_insert_cos(h, emb, maps, sem_cos, cos_stride, out_slot=None, out_replaced=None, stream=None):
+    _check(_lib.fmoe_store_insert_cos(h, emb.shape[0], _ptr(_f32(emb)), _ptr(_f32(maps)), _ptr(sem_cos), cos_stride,
+                                      _ptr(out_slot), _ptr(out_replaced), _stream(stream)))
+
+
+def fmoe_search_semantic_cos(h, q_emb, k, out_score, out_id, out_cos, cos_stride, stream=None):
+    _check(_lib.fmoe_search_semantic_cos(h, q_emb.shape[0], _ptr(_f32(q_emb)), k, _ptr(out_score), _ptr(out_id),
+                                         _ptr(out_cos), cos_stride, _stream(stream)))
 
 
 def fmoe_store_write(h, emb, maps, slot, stream=None):

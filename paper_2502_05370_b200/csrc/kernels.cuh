@@ -58,6 +58,11 @@ struct ScanArgs {
   int check_valid;           // 1: zero-norm query -> (NaN, -1)
   unsigned long long* trace; // debug phase tracer [kTraceBlocks][8] or null
   unsigned long long* best;  // [B] zeroed keys for the k == 1 merge (reset by the last block)
+  // semantic cosines: a semantic scan may write them (out_cos), a blend/RDY scan
+  // may take them instead of re-reading the embeddings (sem_cos); [B][cos_stride]
+  float* out_cos;
+  const float* sem_cos;
+  int64_t cos_stride;
 };
 
 // debug tracer buffer (null unless fmoe_debug_trace enabled it)
@@ -102,6 +107,7 @@ struct UmmaLaunch {
   UmmaPlanIn in;
   const float* q_emb; const float* q_prefix; int64_t q_stride;   // this pass's first query
   void* scratch;               // umma_scratch_bytes(in)
+  float* out_cos; const float* sem_cos; int64_t cos_stride;   // see ScanArgs
   float* valid;                // [nq] validity flags of this pass
   uint64_t* cand; int cand_q0; int grid;
   unsigned long long* trace;

@@ -333,7 +333,13 @@ __global__ void __launch_bounds__(kScanThreads, TPI >= 1 ? 2 : 3) scan_gemv_kern
 #pragma unroll
     for (int q = 0; q < NQ; ++q) {
       float s = 0.f;
-      if (SEM) s = w * (sem[q] * rq0[q] * re);
+      if (SEM) {
+        const float c = sem[q] * rq0[q] * re;          // the semantic cosine (Eq. 1)
+        if (a.out_cos && ok && q < a.nq) a.out_cos[int64_t(a.q0 + q) * a.cos_stride + y] = c;
+        s = w * c;
+      } else if (a.sem_cos) {                          // cached cosine of this (query, row)
+        s = (ok && q < a.nq) ? w * __ldcs(a.sem_cos + int64_t(a.q0 + q) * a.cos_stride + y) : 0.f;
+      }
       if (TRAJ) s = fmaf(w1, trj[q] * rq1[q] * rm, s);
       const uint64_t key = ok ? pack_key(s, a.id_offset + uint32_t(y)) : 0ull;
       lists[q].offer(key, a.k);
@@ -352,9 +358,11 @@ using KernelFn = void (*)(const ScanArgs);
 
 // multi-tile trajectory path: trajectory-only, one 16-byte chunk per
 // row-layer; TPI*LB = 16 loads in flight per lane, TPI capped by registers.
+static bool sem_in(const ScanArgs& a) { return a.w_sem != 0.f && !a.sem_cos; }
+
 static int traj_tpi(const ScanArgs& a) {
   const int esz = a.st.bf16 ? 2 : 4;
-  if (a.w_sem != 0.f || a.st.Ep * esz != 16) return 0;
+  if (sem_in(a) || a.sem_cos || a.st.Ep * esz != 16) return 0;
   const int cap = a.nq <= 1 ? 16 : (a.nq <= 2 ? 8 : 4);
   int tpi = 1;
   while (tpi * 2 <= cap && tpi * 2 * a.ell <= 16) tpi *= 2;
@@ -364,7 +372,7 @@ static int traj_tpi(const ScanArgs& a) {
 template <class Tag, int NQ, int KPL>
 static KernelFn pick_mode(const ScanArgs& a) {
   if (a.w_sem == 1.f) return scan_gemv_kernel<Tag, NQ, KPL, true, false, 0>;
-  if (a.w_sem == 0.f) {
+  if (!sem_in(a)) {
     switch (traj_tpi(a)) {
       case 16: if constexpr (NQ == 1) return scan_gemv_kernel<Tag, NQ, KPL, false, true, 16>; break;
       case 8: if constexpr (NQ <= 2) return scan_gemv_kernel<Tag, NQ, KPL, false, true, 8>; break;
@@ -395,7 +403,7 @@ static KernelFn pick(const ScanArgs& a, int* NQ) {
 
 static size_t scan_smem(const ScanArgs& a, int NQ) {
   size_t f = 0;
-  if (a.w_sem != 0.f) f += size_t(NQ) * a.st.Dp;
+  if (sem_in(a)) f += size_t(NQ) * a.st.Dp;
   if (a.w_sem != 1.f) f += size_t(NQ) * a.ell * a.st.Ep;
   size_t bytes = f * 4;
   const size_t merge = size_t(kScanWarps) * NQ * a.k * 8;

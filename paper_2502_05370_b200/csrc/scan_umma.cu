@@ -52,6 +52,12 @@ constexpr int kStageB = UM_N * 128;          // 32 KB
 constexpr int kUmStageBytes = kStageA + kStageB;
 constexpr int kUmMaxStages = 4;
 
+__device__ __forceinline__ int nvalid_rows(int64_t yc, int64_t n_rows, bool live) {
+  if (!live) return 0;
+  const int64_t left = n_rows - yc;
+  return left >= 32 ? 32 : (left <= 0 ? 0 : int(left));
+}
+
 // ------------------------------------------------------------------ PTX wrappers
 __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, int c0, int c1, uint64_t* bar) {
   asm volatile(
@@ -134,6 +140,9 @@ struct UmmaParams {
   int cand_q0;          // query offset of this pass in cand
   int grid;
   unsigned long long* trace;
+  float* out_cos;               // semantic kernels: cosines [B][cos_stride] (optional)
+  const float* sem_cos;         // trajectory kernels: cached semantic cosines to blend (optional)
+  int64_t cos_stride;
 };
 
 // Sorted insert into a per-thread list in shared memory (entry i at
@@ -311,6 +320,7 @@ __global__ void __launch_bounds__(kUmThreads, 1)
     const float w = p.w, w1 = 1.f - p.w;
     const int k = p.k;
     const bool split = p.split_kb > 0;
+    const bool vec4 = (p.cos_stride & 3) == 0;      // 16-byte aligned cosine rows
     constexpr int HC = UM_N / 2;                  // columns per half
     uint64_t* ml = lists + size_t(half) * k * UM_M + q;   // this thread's list: entry i at ml[i*128]
     const uint32_t ml_s = smem_u32(ml);
@@ -357,13 +367,27 @@ __global__ void __launch_bounds__(kUmThreads, 1)
         const int64_t yc = int64_t(ybase) + c * 32;
         const int64_t left = p.n_rows - yc;
         const unsigned vmask = !live ? 0u : (left >= 32 ? 0xffffffffu : (left <= 0 ? 0u : ((1u << left) - 1u)));
+        float cached[32];
+        if (!SEM && p.sem_cos) {
+          const float* cp = p.sem_cos + int64_t(p.cand_q0 + q) * p.cos_stride + yc;
+#pragma unroll
+          for (int j = 0; j < 32; j += 4) {
+            if (vec4 && j + 4 <= nvalid_rows(yc, p.n_rows, live)) {
+              const float4 f = __ldcs(reinterpret_cast<const float4*>(cp + j));
+              cached[j] = f.x; cached[j + 1] = f.y; cached[j + 2] = f.z; cached[j + 3] = f.w;
+            } else {
+#pragma unroll
+              for (int u = 0; u < 4; ++u) cached[j + u] = (j + u < nvalid_rows(yc, p.n_rows, live)) ? cp[j + u] : 0.f;
+            }
+          }
+        }
         tc_wait_ld();
         // fast path: 32 scores, a float compare each against the k-th score
         float sc[32];
         unsigned m = 0;
 #pragma unroll
         for (int j = 0; j < 32; ++j) {
-          float v = 0.f;
+          float v = (!SEM && p.sem_cos) ? w * cached[j] : 0.f;
           if (SEM) {
             const float dot = (!TRAJ && split) ? __uint_as_float(vs[j]) + __uint_as_float(vt[j]) : __uint_as_float(vs[j]);
             v = w * (dot * rqs * __shfl_sync(0xffffffffu, rec, j));
@@ -373,6 +397,18 @@ __global__ void __launch_bounds__(kUmThreads, 1)
           m |= (v >= thr_s ? 1u : 0u) << j;
         }
         m &= vmask;
+        if (SEM && !TRAJ && p.out_cos && live) {
+          float* op = p.out_cos + int64_t(p.cand_q0 + q) * p.cos_stride + yc;
+          const int nv = nvalid_rows(yc, p.n_rows, live);
+#pragma unroll
+          for (int j = 0; j < 32; j += 4) {
+            if (vec4 && j + 4 <= nv) __stcs(reinterpret_cast<float4*>(op + j), make_float4(sc[j], sc[j + 1], sc[j + 2], sc[j + 3]));
+            else
+#pragma unroll
+              for (int u = 0; u < 4; ++u)
+                if (j + u < nv) op[j + u] = sc[j + u];
+          }
+        }
         // rare path: exact key order (score desc, id asc) for the candidates
         while (m) {
           const int j = __ffs(m) - 1;
@@ -515,7 +551,7 @@ int umma_grid(const UmmaPlanIn& in) {
 
 cudaError_t launch_umma(const UmmaLaunch& L, cudaStream_t s) {
   const UmmaPlanIn& in = L.in;
-  const bool sem = in.w_sem != 0.f, traj = in.w_sem != 1.f;
+  const bool sem = in.w_sem != 0.f && !L.sem_cos, traj = in.w_sem != 1.f;
   const int ell_pad = traj ? in.ell + ((in.Ep * 2 == 16) ? (in.ell & 1) : 0) : 0;
   char* scr = static_cast<char*>(L.scratch);
   __nv_bfloat16* qs = reinterpret_cast<__nv_bfloat16*>(scr);
@@ -581,6 +617,9 @@ cudaError_t launch_umma(const UmmaLaunch& L, cudaStream_t s) {
   p.cand_q0 = L.cand_q0;
   p.grid = L.grid;
   p.trace = L.trace;
+  p.out_cos = L.out_cos;
+  p.sem_cos = L.sem_cos;
+  p.cos_stride = L.cos_stride;
   const size_t smem = 1024 + size_t(p.stages) * kUmStageBytes + lists;
   using Fn = void (*)(const CUtensorMap, const CUtensorMap, const CUtensorMap, const CUtensorMap, const UmmaParams);
   const Fn fn = sem && traj ? scan_umma_kernel<true, true> : sem ? scan_umma_kernel<true, false>

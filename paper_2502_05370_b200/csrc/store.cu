@@ -216,9 +216,15 @@ size_t align_up(size_t x) { return (x + 255) & ~size_t(255); }
 
 // Batched call on the tensor cores: passes of <= 128 queries, per-CTA lists,
 // then one merge kernel over all passes.
+struct CosArgs {
+  float* out = nullptr;          // semantic scans: write the cosines
+  const float* in = nullptr;     // RDY / blend scans: blend these instead of re-reading embeddings
+  int64_t stride = 0;
+};
+
 fmoe_status run_search_umma(const fmoe_store* st, UmmaPlanIn in, int64_t B, const float* dq, const float* dp,
                             int64_t q_stride, cudaStream_t s, float* ds, int64_t* di, uint64_t* dkeys,
-                            bool check_queries) {
+                            bool check_queries, const CosArgs& cos) {
   const int grid = umma_grid(in);
   const int n_lists = 2 * grid;                       // one list per (CTA, column half)
   const size_t cand_b = align_up(size_t(B) * n_lists * in.k * 8);
@@ -244,6 +250,9 @@ fmoe_status run_search_umma(const fmoe_store* st, UmmaPlanIn in, int64_t B, cons
     L.cand_q0 = int(q0);
     L.grid = grid;
     L.trace = trace_buffer();
+    L.out_cos = cos.out ? cos.out + q0 * cos.stride : nullptr;
+    L.sem_cos = cos.in ? cos.in + q0 * cos.stride : nullptr;
+    L.cos_stride = cos.stride;
     cudaError_t e = launch_umma(L, s);
     if (e != cudaSuccess) return cuda_fail(e, "umma scan launch");
   }
@@ -256,7 +265,7 @@ fmoe_status run_search_umma(const fmoe_store* st, UmmaPlanIn in, int64_t B, cons
 // the candidate lists (returned in *extra_ptr) for the caller.
 fmoe_status run_search(const fmoe_store* st, int64_t B, const float* dq, const float* dp, int64_t q_stride, int ell,
                        float w, int k, int64_t n_rows, uint32_t id_offset, cudaStream_t s, float* ds, int64_t* di,
-                       uint64_t* dkeys, bool check_queries) {
+                       uint64_t* dkeys, bool check_queries, const CosArgs& cos = CosArgs()) {
   if (n_rows == 0) {
     cudaError_t e = launch_merge_keys(int(B), 0, k, nullptr, k, nullptr, ds, di, dkeys, s);
     return e == cudaSuccess ? FMOE_OK : cuda_fail(e, "merge launch");
@@ -267,7 +276,7 @@ fmoe_status run_search(const fmoe_store* st, int64_t B, const float* dq, const f
     in.bf16 = 1; in.nq = int(B < 128 ? B : 128); in.k = k; in.D = st->cfg.D; in.Dp = st->Dp; in.E = st->cfg.E;
     in.Ep = st->Ep; in.L = st->cfg.L; in.ell = ell; in.w_sem = w; in.n_rows = n_rows; in.cap = st->cfg.capacity;
     in.id_offset = id_offset; in.emb = st->emb; in.maps = st->maps; in.r_e = st->r_e; in.psq = st->psq;
-    if (umma_supported(in)) return run_search_umma(st, in, B, dq, dp, q_stride, s, ds, di, dkeys, check_queries);
+    if (umma_supported(in)) return run_search_umma(st, in, B, dq, dp, q_stride, s, ds, di, dkeys, check_queries, cos);
   }
   ScanArgs a{};
   a.st = st->view();
@@ -300,6 +309,9 @@ fmoe_status run_search(const fmoe_store* st, int64_t B, const float* dq, const f
   a.out_keys = dkeys;
   a.check_valid = check_queries ? 1 : 0;
   a.trace = trace_buffer();
+  a.out_cos = cos.out;
+  a.sem_cos = cos.in;
+  a.cos_stride = cos.stride;
   for (int p = 0; p < npass; ++p) {
     a.q0 = 4 * p;
     a.nq = int(B - a.q0 < 4 ? B - a.q0 : 4);
@@ -311,7 +323,8 @@ fmoe_status run_search(const fmoe_store* st, int64_t B, const float* dq, const f
 }
 
 fmoe_status search_common(const fmoe_store* st, int64_t B, const float* q_emb, const float* q_prefix, int32_t ell,
-                          float w, int32_t k, float* out_score, int64_t* out_id, void* stream) {
+                          float w, int32_t k, float* out_score, int64_t* out_id, void* stream,
+                          float* out_cos = nullptr, int64_t cos_stride = 0) {
   if (!st) return fail(FMOE_ERR_INVALID_ARG, "null store");
   if (B < 0) return fail(FMOE_ERR_INVALID_ARG, "B < 0");
   if (k < 1 || k > FMOE_MAX_K) return fail(FMOE_ERR_INVALID_ARG, "k must be in [1, 64]");
@@ -329,10 +342,13 @@ fmoe_status search_common(const fmoe_store* st, int64_t B, const float* q_emb, c
   const float* dp = traj ? S.in(q_prefix, size_t(B) * ell * E) : nullptr;
   float* ds = S.out(out_score, size_t(B) * k);
   int64_t* di = S.out(out_id, size_t(B) * k);
+  CosArgs cos;
+  cos.out = out_cos ? S.out(out_cos, size_t(B) * cos_stride) : nullptr;
+  cos.stride = cos_stride;
   fmoe_status r = S.check();
   if (r == FMOE_OK)
     r = run_search(st, B, dq, dp, int64_t(ell) * E, traj ? ell : 0, w, k, st->n, uint32_t(st->cfg.id_offset), s, ds,
-                   di, nullptr, true);
+                   di, nullptr, true, cos);
   return S.finish(r);
 }
 
@@ -427,7 +443,14 @@ fmoe_status fmoe_store_get_config(const fmoe_store* st, fmoe_store_config* out_c
 
 fmoe_status fmoe_store_insert(fmoe_store* st, int64_t B, const float* emb, const float* maps, int64_t* out_slot,
                               int64_t* out_replaced, void* stream) {
+  return fmoe_store_insert_cos(st, B, emb, maps, nullptr, 0, out_slot, out_replaced, stream);
+}
+
+fmoe_status fmoe_store_insert_cos(fmoe_store* st, int64_t B, const float* emb, const float* maps,
+                                  const float* sem_cos, int64_t cos_stride, int64_t* out_slot,
+                                  int64_t* out_replaced, void* stream) {
   if (!st) return fail(FMOE_ERR_INVALID_ARG, "null store");
+  if (sem_cos && cos_stride < st->n) return fail(FMOE_ERR_INVALID_ARG, "cos_stride < store size");
   if (B < 0 || B > (int64_t(1) << 30)) return fail(FMOE_ERR_INVALID_ARG, "B");
   if (B == 0) return FMOE_OK;
   if (!emb || !maps) return fail(FMOE_ERR_INVALID_ARG, "null emb/maps");
@@ -441,6 +464,7 @@ fmoe_status fmoe_store_insert(fmoe_store* st, int64_t B, const float* emb, const
   Staging S(s, st->device);
   const float* de = S.in(emb, size_t(B) * D);
   const float* dm = S.in(maps, size_t(B) * L * E);
+  const float* dcos = sem_cos && nrep > 0 ? S.in(sem_cos, size_t(B) * cos_stride) : nullptr;
   int64_t* dslot = S.out(out_slot, size_t(B));
   int64_t* drep = S.out(out_replaced, size_t(B));
   int64_t* slots_all = nrep > 0 ? static_cast<int64_t*>(S.scratch(size_t(B) * 8)) : nullptr;
@@ -454,8 +478,11 @@ fmoe_status fmoe_store_insert(fmoe_store* st, int64_t B, const float* emb, const
       // RDY_{x,y} = d/L sem + (L-d)/L traj over full maps, against
       // the contexts present before this call: rows [0, n0).
       const float w = float(st->cfg.d) / float(L);
+      CosArgs cos;
+      cos.in = dcos ? dcos + a * cos_stride : nullptr;     // cos(emb_x, sem_y) from the semantic search
+      cos.stride = cos_stride;
       r = run_search(st, nrep, de + a * D, dm + a * int64_t(L) * E, int64_t(L) * E, L, w, kk, n0, 0u, s, nullptr,
-                     nullptr, keys, false);
+                     nullptr, keys, false, cos);
     }
     if (r == FMOE_OK) {
       cudaError_t e = launch_resolve(int(nrep), kk, keys, off, slots_all, int(a), n0, dslot, drep, s);
@@ -659,6 +686,13 @@ fmoe_status fmoe_store_read(const fmoe_store* st, int64_t slot_begin, int64_t co
 fmoe_status fmoe_search_semantic(const fmoe_store* st, int64_t B, const float* q_emb, int32_t k, float* out_score,
                                  int64_t* out_id, void* stream) {
   return search_common(st, B, q_emb, nullptr, 0, 1.f, k, out_score, out_id, stream);
+}
+
+fmoe_status fmoe_search_semantic_cos(const fmoe_store* st, int64_t B, const float* q_emb, int32_t k, float* out_score,
+                                     int64_t* out_id, float* out_cos, int64_t cos_stride, void* stream) {
+  if (!st) return fail(FMOE_ERR_INVALID_ARG, "null store");
+  if (out_cos && cos_stride < st->n) return fail(FMOE_ERR_INVALID_ARG, "cos_stride < store size");
+  return search_common(st, B, q_emb, nullptr, 0, 1.f, k, out_score, out_id, stream, out_cos, cos_stride);
 }
 
 fmoe_status fmoe_search_trajectory(const fmoe_store* st, int64_t B, const float* q_prefix, int32_t ell, int32_t k,

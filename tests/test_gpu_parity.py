@@ -322,3 +322,38 @@ def test_trajectory_session_invalidated_by_insert(lib):
     assert i.item() in range(40)
     sess.close()
     st.close()
+
+
+# ---------------------------------------------------------------- cached semantic cosines -> RDY insert
+@pytest.mark.parametrize("B", [1, 3, 20])
+def test_semantic_cos_matrix_and_insert_cos(lib, B):
+    sh = S.Shape("mix", 8, 8, 2, 1040, n_clusters=4)        # D >= 1024: K-split tcgen05 path at B=20
+    N = 1500
+    emb, maps, _ = S.store_rows(sh, 21, 0, N + B)
+    stride = N + 4
+    for dt in ("bf16", "f32"):
+        a = lib.ExpertMapStore(sh.L, sh.E, sh.K, sh.D, 3, N, dt)
+        b = lib.ExpertMapStore(sh.L, sh.E, sh.K, sh.D, 3, N, dt)
+        a.insert(emb[:N].cuda(), maps[:N].cuda())
+        b.insert(emb[:N].cuda(), maps[:N].cuda())
+        qe, qm = emb[N:].contiguous(), maps[N:].contiguous()
+        cos = torch.full((B, stride), -7.0, device="cuda")
+        s = torch.empty(B, 4, device="cuda")
+        i = torch.empty(B, 4, dtype=torch.int64, device="cuda")
+        lib.fmoe_search_semantic_cos(a._h, qe.cuda(), 4, s, i, cos, stride)
+        ref = O.semantic_scores(O.quantize(qe.numpy(), dt), O.quantize(emb[:N].numpy(), dt))
+        got = cos[:, :N].cpu().numpy().astype(np.float64)
+        assert np.all(np.abs(got - ref) <= TOL)
+        assert torch.all(cos[:, N:] == -7.0)                   # columns >= size untouched
+        check_topk(s, i, ref, 4)
+        # the insert that reuses the cosines == the plain insert
+        sa = torch.empty(B, dtype=torch.int64, device="cuda")
+        ra = torch.empty(B, dtype=torch.int64, device="cuda")
+        lib.fmoe_store_insert_cos(a._h, qe.cuda(), qm.cuda(), cos, stride, sa, ra)
+        sb, rb = b.insert(qe.cuda(), qm.cuda())
+        assert torch.equal(sa, sb) and torch.equal(ra, rb)
+        ea, ma = a.read(0, N)
+        eb, mb = b.read(0, N)
+        assert torch.equal(ea, eb) and torch.equal(ma, mb)
+        a.close()
+        b.close()
