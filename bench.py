@@ -460,10 +460,19 @@ def run_fmoe(args, cfg, rank, world, local_rank):
     scan_ms = kind_ms.get("semantic", 0) + traj_ms + kind_ms.get("rdy_insert", 0)
     scan_bytes = sem_b + sum(traj_b.values()) + rdy_b
     peaks = load_peaks()
-    achieved = scan_bytes / (scan_ms * 1e-3) / 1e9
+    # the dominant kernel of the step: the semantic scan (one launch per step at B <= 4;
+    # prep + scan + merge at B >= 5), algorithmic bytes per launch / its mean event time
+    sem_ms = kind_ms.get("semantic", 0.0)
+    achieved = sem_b / (sem_ms * 1e-3) / 1e9 if sem_ms > 0 else 0.0
+    agg = scan_bytes / (scan_ms * 1e-3) / 1e9 if scan_ms > 0 else 0.0
     roofline = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peaks["hbm_gbs"], "unit": "GB/s",
-                "frac": round(achieved / peaks["hbm_gbs"], 4), "traffic": None,
-                "kernel": "the scan kernels of a step (all 33 searches; CUDA events around each search call, eager pass)",
+                "frac": round(achieved / peaks["hbm_gbs"], 4), "traffic": measured_traffic(args.config),
+                "kernel": "semantic scan (Eq. 1 + fused top-k), the largest share of the step; CUDA events "
+                          "around each call on the launching stream, eager timed pass",
+                "algorithmic_bytes_per_launch": sem_b,
+                "share_of_step": round(sem_ms / (ms_eager / eager_steps), 3) if ms_eager > 0 else None,
+                "step_aggregate": {"achieved": round(agg, 1), "frac": round(agg / peaks["hbm_gbs"], 4),
+                                   "bytes": scan_bytes, "what": "all scans of a step (semantic, trajectory, RDY)"},
                 "eager_ms_per_step": round(ms_eager / eager_steps, 4),
                 "peak_source": peaks["source"],
                 "breakdown": {
@@ -506,6 +515,15 @@ def run_fmoe(args, cfg, rank, world, local_rank):
 
 def sh_L(cfg):
     return cfg["shape"].L
+
+
+def measured_traffic(config):
+    """dram read+write bytes per launch of the dominant kernel from the committed
+    `ncu --set full` capture summary (profiles/traffic.json), or None."""
+    p = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(p):
+        return json.load(open(p)).get(config)
+    return None
 
 
 def load_peaks():
