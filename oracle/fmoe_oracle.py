@@ -340,3 +340,48 @@ def brute_force_min_prefetch_set(p, delta: float, K: int):
         if feasible:
             return size, feasible
     return E, [tuple(range(E))]
+
+
+# --------------------------------------------------------------------------
+# Expert-cache priorities
+# --------------------------------------------------------------------------
+def prefetch_priority(p: float, layer: int, l_now: int) -> float:
+    """PRI^prefetch_{l,j} = p_{l,j} / (l - l_now); requires l > l_now."""
+    if layer <= l_now:
+        raise ValueError("target layer must be after the current layer")
+    return float(p) / float(layer - l_now)
+
+
+def eviction_priority(p: float, freq: float, eps: float = 1e-6) -> float:
+    """PRI^evict_{l,j} = 1 / (p_{l,j} * freq_{l,j}), p floored at eps (S:377,
+    Reading R13: the paper's formula is undefined at p = 0)."""
+    return 1.0 / (max(float(p), eps) * float(freq))
+
+
+def prefetch_plan(store_maps, map_id, score, delta, layers, K, l_now):
+    """Prefetch jobs of each query: every expert of the Eq. 4-6 prefetch set of each
+    target layer t (selection as `select_experts`), with PRI^prefetch = p/(t - l_now),
+    ordered by priority descending, ties -> lower layer, then lower expert.
+    Layers are 0-based on both sides, so t - l_now is the paper's l - l_now.
+    Returns, per query, a list of (t, j, priority)."""
+    m = np.asarray(store_maps, dtype=np.float64)
+    out = []
+    for x in range(len(map_id)):
+        jobs = []
+        if map_id[x] >= 0:
+            dl = selection_threshold(score[x]) if delta < 0 else float(delta)
+            for t in layers:
+                picked, _ = select_prefetch_set(m[map_id[x], t], dl, K)
+                for j in picked:
+                    jobs.append((t, j, prefetch_priority(m[map_id[x], t, j], t, l_now)))
+        jobs.sort(key=lambda r: (-r[2], r[0], r[1]))
+        out.append(jobs)
+    return out
+
+
+def eviction_order(p, freq, eps: float = 1e-6):
+    """Cache entries (index = insertion order) sorted for eviction: PRI^evict descending,
+    ties -> the least recently inserted (lower index) first."""
+    pri = [eviction_priority(pp, ff, eps) for pp, ff in zip(p, freq)]
+    order = sorted(range(len(pri)), key=lambda i: (-pri[i], i))
+    return pri, order

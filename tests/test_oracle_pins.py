@@ -321,3 +321,51 @@ def test_paper_store_memory_closed_form(ex):
     # "< 200 MB" at 32K maps; the fp32 map payload alone gives 188.7 MB
     mb = ex["n_maps"] * ex["L"] * ex["E"] * ex["bytes_per_elem"] / 1e6
     assert abs(mb - ex["expect_mb"]) < 1e-5 and mb < 200
+
+
+# ---------------------------------------------------------------- cache priorities
+def test_prefetch_priority_golden():
+    ex = GOLD["prefetch_priority"]
+    assert abs(O.prefetch_priority(ex[0]["p"], ex[0]["layer"], ex[0]["l_now"]) - ex[0]["expect"]) < 1e-15
+    assert abs(O.prefetch_priority(ex[1]["p"], ex[1]["layer"], ex[1]["l_now"]) - ex[1]["expect"]) < 1e-15
+    pri = [O.prefetch_priority(p, 10 + dist, 10) for p, dist in ex[2]["jobs"]]
+    assert int(np.argmax(pri)) == ex[2]["expect_first"]
+    with pytest.raises(ValueError):
+        O.prefetch_priority(0.5, 2, 2)
+
+
+def test_eviction_priority_golden():
+    ex = GOLD["eviction_priority"]
+    assert abs(O.eviction_priority(ex[0]["p"], ex[0]["freq"]) - ex[0]["expect"]) < 1e-15
+    assert abs(O.eviction_priority(ex[1]["p"], ex[1]["freq"]) - ex[1]["expect"]) < 1e-6
+    p, f = zip(*ex[2]["cache"])
+    _, order = O.eviction_order(p, f)
+    assert order == ex[2]["expect_order"]
+
+
+def test_prefetch_plan_properties():
+    # every planned job is in the Eq. 4-6 set of its layer; order = priority desc,
+    # then layer asc, expert asc; priority = p / distance (recomputed with a loop)
+    m = rng.dirichlet(np.full(6, 0.4), size=(4, 9))
+    plans = O.prefetch_plan(m, [2, -1, 0], [0.7, 0.5, -0.2], -1.0, [3, 4, 5], 2, 1)
+    assert plans[1] == []
+    for x, mid, sc in ((0, 2, 0.7), (2, 0, -0.2)):
+        jobs = plans[x]
+        keys = [(-pr, t, j) for t, j, pr in jobs]
+        assert keys == sorted(keys)
+        for t in (3, 4, 5):
+            picked, _ = O.select_prefetch_set(m[mid, t], O.selection_threshold(sc), 2)
+            assert sorted(j for tt, j, _ in jobs if tt == t) == sorted(picked)
+        for t, j, pr in jobs:
+            assert pr == m[mid, t, j] / (t - 1)
+    # monotone: a farther layer never outranks the same probability nearer
+    assert O.prefetch_priority(0.4, 5, 1) < O.prefetch_priority(0.4, 3, 1)
+
+
+def test_eviction_order_is_a_stable_sort_by_priority():
+    p = rng.choice([0.0, 0.1, 0.25, 0.5], size=200)
+    f = rng.integers(1, 5, size=200)
+    pri, order = O.eviction_order(p, f)
+    assert sorted(order) == list(range(200))
+    for a, b in zip(order, order[1:]):
+        assert pri[a] > pri[b] or (pri[a] == pri[b] and a < b)
