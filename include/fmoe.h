@@ -206,6 +206,28 @@ fmoe_status fmoe_select_experts(const fmoe_store* store, int64_t B, const int64_
                                 int32_t layer_end, uint64_t* out_mask, int32_t* out_count,
                                 void* stream);
 
+/* ---- expert-cache priorities ------------ */
+
+/* Prefetch plan: for each query, every expert of the Eq. 4-6 prefetch set of
+ * each target layer t in [layer_begin, layer_end) of its matched map
+ * (selection exactly as fmoe_select_experts, same delta rule), with
+ * PRI^prefetch = p_{t,j} / (t - l_now) in float64, ordered by
+ * priority descending, ties -> lower layer, then lower expert.
+ * Outputs [B][max_jobs]: out_layer, out_expert (int32, -1 past the end),
+ * out_priority (float64); out_njobs [B] (jobs beyond max_jobs are dropped).
+ * Requires l_now < layer_begin and (layer_end - layer_begin) * E <= 2048. */
+fmoe_status fmoe_prefetch_plan(const fmoe_store* store, int64_t B, const int64_t* map_id, const float* score,
+                               float delta, int32_t l_now, int32_t layer_begin, int32_t layer_end,
+                               int32_t max_jobs, int32_t* out_layer, int32_t* out_expert, double* out_priority,
+                               int32_t* out_njobs, void* stream);
+
+/* Eviction order of n cached experts: PRI^evict = 1 / (max(p, eps)
+ * * freq) in float64 (p floored at eps, Reading R13), and out_order [n]
+ * = cache indices by priority descending, ties -> lower index (= earlier
+ * inserted).  p, freq [n] fp32; out_priority [n] float64.  1 <= n <= 8192. */
+fmoe_status fmoe_eviction_order(int64_t n, const float* p, const float* freq, float eps, double* out_priority,
+                                int32_t* out_order, int device, void* stream);
+
 /* ---- sharded merge ---------------------------------------- */
 
 /* Merge n_lists candidate lists per query into the global top-k: scores

@@ -63,6 +63,8 @@ def _load():
         "fmoe_traj_session_reset": (I32, [P]),
         "fmoe_traj_session_destroy": (None, [P]),
         "fmoe_topk_merge": (I32, [I64, I32, I32, P, P, I32, P, P, ctypes.c_int, P]),
+        "fmoe_prefetch_plan": (I32, [P, I64, P, P, F, I32, I32, I32, I32, P, P, P, P, P]),
+        "fmoe_eviction_order": (I32, [I64, P, P, F, P, P, ctypes.c_int, P]),
         "fmoe_status_string": (ctypes.c_char_p, [I32]),
         "fmoe_last_error": (ctypes.c_char_p, []),
         "fmoe_kernel_launch_count": (I64, []),
@@ -79,7 +81,8 @@ ABI_SYMBOLS = ("fmoe_store_create", "fmoe_store_destroy", "fmoe_store_size", "fm
                "fmoe_store_insert", "fmoe_store_insert_cos", "fmoe_search_semantic_cos", "fmoe_store_read",
                "fmoe_store_write", "fmoe_resolve_victims", "fmoe_search_semantic", "fmoe_search_trajectory",
                "fmoe_search_blend", "fmoe_select_experts", "fmoe_traj_session_create", "fmoe_traj_session_step",
-               "fmoe_traj_session_reset", "fmoe_traj_session_destroy", "fmoe_topk_merge", "fmoe_status_string",
+               "fmoe_traj_session_reset", "fmoe_traj_session_destroy", "fmoe_topk_merge",
+               "fmoe_prefetch_plan", "fmoe_eviction_order", "fmoe_status_string",
                "fmoe_last_error", "fmoe_kernel_launch_count")
 
 
@@ -173,6 +176,18 @@ def fmoe_search_blend(h, q_emb, q_prefix, ell, w_sem, k, out_score, out_id, stre
 def fmoe_select_experts(h, map_id, score, delta, layer_begin, layer_end, out_mask, out_count, stream=None):
     _check(_lib.fmoe_select_experts(h, map_id.shape[0], _ptr(map_id), _ptr(score), delta, layer_begin, layer_end,
                                     _ptr(out_mask), _ptr(out_count), _stream(stream)))
+
+
+def fmoe_prefetch_plan(h, map_id, score, delta, l_now, layer_begin, layer_end, max_jobs, out_layer, out_expert,
+                       out_priority, out_njobs, stream=None):
+    _check(_lib.fmoe_prefetch_plan(h, map_id.shape[0], _ptr(map_id), _ptr(score), delta, l_now, layer_begin, layer_end,
+                                   max_jobs, _ptr(out_layer), _ptr(out_expert), _ptr(out_priority), _ptr(out_njobs),
+                                   _stream(stream)))
+
+
+def fmoe_eviction_order(p, freq, eps, out_priority, out_order, device=0, stream=None):
+    _check(_lib.fmoe_eviction_order(p.shape[0], _ptr(p), _ptr(freq), eps, _ptr(out_priority), _ptr(out_order),
+                                    int(device), _stream(stream)))
 
 
 def fmoe_traj_session_create(h, B):

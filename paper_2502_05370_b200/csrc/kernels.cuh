@@ -126,6 +126,14 @@ cudaError_t launch_select(const StoreView& st, int B, const int64_t* map_id, con
                           float delta, int K, int layer_begin, int layer_end, int64_t id_offset,
                           int64_t n_rows, uint64_t* out_mask, int32_t* out_count, cudaStream_t s);
 
+// Expert-cache priorities: prefetch plan per query, eviction order.
+cudaError_t launch_prefetch_plan(const StoreView& st, int B, const int64_t* map_id, const float* score, float delta,
+                                 int K, int l_now, int lb, int le, int64_t id_offset, int64_t n_rows, int max_jobs,
+                                 int32_t* out_layer, int32_t* out_expert, double* out_pri, int32_t* out_njobs,
+                                 cudaStream_t s);
+cudaError_t launch_eviction_order(int n, const float* p, const float* freq, float eps, double* out_pri,
+                                  int32_t* out_order, cudaStream_t s);
+
 // Quantise + write rows (append or replace) and their norm tables.
 //  slot of new row x: slots ? slots[x] (skip if < 0) : first_slot + x.
 struct WriteArgs {

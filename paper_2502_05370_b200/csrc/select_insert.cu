@@ -113,6 +113,54 @@ __device__ __forceinline__ float load_p(const StoreView& st, int t, int64_t row,
     return m[(int64_t(t) * st.cap + row) * st.Ep + j];
 }
 
+// delta = Clip(1 - score, 0, 1) in float64 (score clamped to [-1, 1], NaN -> 1), or the fixed delta
+__device__ __forceinline__ double selection_delta(float delta, float s) {
+  if (delta >= 0.f) return double(delta);
+  if (s != s) return 1.0;
+  double sd = double(s);
+  sd = sd < -1.0 ? -1.0 : (sd > 1.0 ? 1.0 : sd);
+  const double v = 1.0 - sd;
+  return v < 0.0 ? 0.0 : (v > 1.0 ? 1.0 : v);
+}
+
+// Eq. 4-6 for row `loc`, layer t, by one warp: rank the E <= 64 probabilities
+// by (p desc, index asc) in registers, scatter them in rank order to the warp's
+// scratch sp/si, and accumulate in float64 in that order on lane 0 (the order
+// and precision of the oracle).  Returns (on every lane) the mask and count;
+// sp/si[0..count) then hold the picked experts in selection order.
+template <class Tag>
+__device__ __forceinline__ void warp_select(const StoreView& st, int t, int64_t loc, double dl, int K, float* sp,
+                                            int* si, uint64_t* mask_out, int* count_out) {
+  const int lane = threadIdx.x & 31;
+  const int E = st.E;
+  const float NEG = -__int_as_float(0x7f800000);
+  const float p0 = lane < E ? load_p<Tag>(st, t, loc, lane) : NEG;
+  const float p1 = lane + 32 < E ? load_p<Tag>(st, t, loc, lane + 32) : NEG;
+  int r0 = 0, r1 = 0;
+  for (int j = 0; j < E; ++j) {
+    const float a = __shfl_sync(0xffffffffu, p0, j & 31);
+    const float b = __shfl_sync(0xffffffffu, p1, j & 31);
+    const float pj = j < 32 ? a : b;
+    r0 += (pj > p0) || (pj == p0 && j < lane);
+    r1 += (pj > p1) || (pj == p1 && j < lane + 32);
+  }
+  if (lane < E) { sp[r0] = p0; si[r0] = lane; }
+  if (lane + 32 < E) { sp[r1] = p1; si[r1] = lane + 32; }
+  __syncwarp();
+  uint64_t mask = 0ull;
+  int m = E;
+  if (lane == 0) {
+    double cum = 0.0;
+    for (int r = 0; r < E; ++r) {
+      cum = cum + double(sp[r]);
+      if (cum >= dl && r + 1 >= K) { m = r + 1; break; }
+    }
+    for (int r = 0; r < m; ++r) mask |= 1ull << si[r];
+  }
+  *mask_out = shfl_u64(mask, 0);
+  *count_out = __shfl_sync(0xffffffffu, m, 0);
+}
+
 template <class Tag>
 __global__ void __launch_bounds__(kSelWarps * 32) select_kernel(StoreView st, int B, const int64_t* __restrict__ map_id,
                                                                 const float* __restrict__ score, float delta, int K,
@@ -132,44 +180,11 @@ __global__ void __launch_bounds__(kSelWarps * 32) select_kernel(StoreView st, in
     if (lane == 0) { out_mask[o] = 0ull; out_count[o] = 0; }
     return;
   }
-  double dl;
-  if (delta < 0.f) {
-    const float s = score[q];
-    if (s != s) {
-      dl = 1.0;
-    } else {
-      double sd = double(s);
-      sd = sd < -1.0 ? -1.0 : (sd > 1.0 ? 1.0 : sd);
-      const double v = 1.0 - sd;
-      dl = v < 0.0 ? 0.0 : (v > 1.0 ? 1.0 : v);
-    }
-  } else {
-    dl = double(delta);
-  }
-  const int E = st.E;
-  const float NEG = -__int_as_float(0x7f800000);
-  const float p0 = lane < E ? load_p<Tag>(st, t, loc, lane) : NEG;
-  const float p1 = lane + 32 < E ? load_p<Tag>(st, t, loc, lane + 32) : NEG;
-  int r0 = 0, r1 = 0;
-  for (int j = 0; j < E; ++j) {
-    const float a = __shfl_sync(0xffffffffu, p0, j & 31);
-    const float b = __shfl_sync(0xffffffffu, p1, j & 31);
-    const float pj = j < 32 ? a : b;
-    r0 += (pj > p0) || (pj == p0 && j < lane);
-    r1 += (pj > p1) || (pj == p1 && j < lane + 32);
-  }
-  if (lane < E) { sp[warp][r0] = p0; si[warp][r0] = lane; }
-  if (lane + 32 < E) { sp[warp][r1] = p1; si[warp][r1] = lane + 32; }
-  __syncwarp();
+  const double dl = selection_delta(delta, score ? score[q] : 0.f);
+  uint64_t mask;
+  int m;
+  warp_select<Tag>(st, t, loc, dl, K, sp[warp], si[warp], &mask, &m);
   if (lane == 0) {
-    double cum = 0.0;
-    int m = E;
-    for (int r = 0; r < E; ++r) {
-      cum = cum + double(sp[warp][r]);
-      if (cum >= dl && r + 1 >= K) { m = r + 1; break; }
-    }
-    uint64_t mask = 0ull;
-    for (int r = 0; r < m; ++r) mask |= 1ull << si[warp][r];
     out_mask[o] = mask;
     out_count[o] = m;
   }
@@ -434,3 +449,135 @@ extern "C" int fmoe_debug_trace(int enable, unsigned long long* out, int max_blo
   }
   return 0;
 }
+
+// ------------------------------------------------------------------ expert-cache priorities
+namespace fmoe {
+
+struct PlanJob {
+  double pri;
+  int tie;      // ascending secondary order (prefetch: layer*64 + expert; eviction: cache index)
+};
+
+__device__ __forceinline__ bool job_before(const PlanJob& a, const PlanJob& b) {
+  return a.pri > b.pri || (a.pri == b.pri && a.tie < b.tie);
+}
+
+// block-wide bitonic sort of n2 (a power of two) entries into "before" order
+__device__ void bitonic_sort(PlanJob* v, int n2) {
+  for (int size = 2; size <= n2; size <<= 1)
+    for (int stride = size >> 1; stride > 0; stride >>= 1) {
+      __syncthreads();
+      for (int i = threadIdx.x; i < n2 / 2; i += blockDim.x) {
+        const int lo = 2 * i - (i & (stride - 1));
+        const int hi = lo + stride;
+        const bool up = (lo & size) == 0;
+        const PlanJob a = v[lo], b = v[hi];
+        if (up ? job_before(b, a) : job_before(a, b)) {
+          v[lo] = b;
+          v[hi] = a;
+        }
+      }
+    }
+  __syncthreads();
+}
+
+constexpr int kPlanThreads = 256;
+constexpr int kPlanMax = 2048;
+
+// One CTA per query: the Eq. 4-6 sets of the target layers (warp per layer,
+// warp_select), PRI^prefetch = p / (t - l_now) in float64, one bitonic sort.
+template <class Tag>
+__global__ void __launch_bounds__(kPlanThreads) plan_kernel(StoreView st, const int64_t* __restrict__ map_id,
+                                                            const float* __restrict__ score, float delta, int K,
+                                                            int l_now, int lb, int T, int64_t id_offset,
+                                                            int64_t n_rows, int max_jobs, int32_t* out_layer,
+                                                            int32_t* out_expert, double* out_pri, int32_t* out_njobs) {
+  pdl_wait();
+  __shared__ PlanJob jobs[kPlanMax];
+  __shared__ float sp[kPlanThreads / 32][kMaxE];
+  __shared__ int si[kPlanThreads / 32][kMaxE];
+  __shared__ int nj_sh;
+  const int q = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int E = st.E, n = T * E;
+  int n2 = 2;
+  while (n2 < n) n2 <<= 1;
+  for (int i = tid; i < n2; i += kPlanThreads) jobs[i] = PlanJob{-__longlong_as_double(0x7ff0000000000000ll), (1 << 30) + i};
+  if (tid == 0) nj_sh = 0;
+  __syncthreads();
+  const int64_t id = map_id[q], loc = id - id_offset;
+  if (id >= 0 && loc >= 0 && loc < n_rows) {
+    const double dl = selection_delta(delta, score ? score[q] : 0.f);
+    for (int tt = warp; tt < T; tt += kPlanThreads / 32) {
+      const int t = lb + tt;
+      uint64_t mask;
+      int m;
+      warp_select<Tag>(st, t, loc, dl, K, sp[warp], si[warp], &mask, &m);
+      for (int r = lane; r < m; r += 32) {
+        const int j = si[warp][r];
+        jobs[tt * E + j] = PlanJob{double(sp[warp][r]) / double(t - l_now), t * 64 + j};
+      }
+      if (lane == 0) atomicAdd(&nj_sh, m);
+      __syncwarp();
+    }
+  }
+  bitonic_sort(jobs, n2);
+  const int nj = nj_sh < max_jobs ? nj_sh : max_jobs;
+  for (int i = tid; i < max_jobs; i += kPlanThreads) {
+    const bool ok = i < nj;
+    out_layer[int64_t(q) * max_jobs + i] = ok ? (jobs[i].tie >> 6) : -1;
+    out_expert[int64_t(q) * max_jobs + i] = ok ? (jobs[i].tie & 63) : -1;
+    out_pri[int64_t(q) * max_jobs + i] = ok ? jobs[i].pri : 0.0;
+  }
+  if (tid == 0) out_njobs[q] = nj;
+}
+
+cudaError_t launch_prefetch_plan(const StoreView& st, int B, const int64_t* map_id, const float* score, float delta,
+                                 int K, int l_now, int lb, int le, int64_t id_offset, int64_t n_rows, int max_jobs,
+                                 int32_t* out_layer, int32_t* out_expert, double* out_pri, int32_t* out_njobs,
+                                 cudaStream_t s) {
+  if (B <= 0) return cudaSuccess;
+  count_launch();
+  if (st.bf16)
+    return launch_pdl(plan_kernel<Bf16Tag>, dim3(B), dim3(kPlanThreads), 0, s, st, map_id, score, delta, K, l_now, lb,
+                      le - lb, id_offset, n_rows, max_jobs, out_layer, out_expert, out_pri, out_njobs);
+  return launch_pdl(plan_kernel<F32Tag>, dim3(B), dim3(kPlanThreads), 0, s, st, map_id, score, delta, K, l_now, lb,
+                    le - lb, id_offset, n_rows, max_jobs, out_layer, out_expert, out_pri, out_njobs);
+}
+
+constexpr int kEvictThreads = 1024;
+
+// One CTA: PRI^evict = 1 / (max(p, eps) * freq) in float64 and the eviction order.
+__global__ void __launch_bounds__(kEvictThreads) evict_kernel(int n, const float* __restrict__ p,
+                                                              const float* __restrict__ freq, float eps,
+                                                              double* out_pri, int32_t* out_order) {
+  pdl_wait();
+  extern __shared__ PlanJob v[];
+  int n2 = 2;
+  while (n2 < n) n2 <<= 1;
+  for (int i = threadIdx.x; i < n2; i += kEvictThreads) {
+    if (i < n) {
+      const double pp = double(p[i]) > double(eps) ? double(p[i]) : double(eps);
+      const double pri = 1.0 / (pp * double(freq[i]));
+      out_pri[i] = pri;
+      v[i] = PlanJob{pri, i};
+    } else {
+      v[i] = PlanJob{-__longlong_as_double(0x7ff0000000000000ll), (1 << 30) + i};
+    }
+  }
+  bitonic_sort(v, n2);
+  for (int i = threadIdx.x; i < n; i += kEvictThreads) out_order[i] = v[i].tie;
+}
+
+cudaError_t launch_eviction_order(int n, const float* p, const float* freq, float eps, double* out_pri,
+                                  int32_t* out_order, cudaStream_t s) {
+  if (n <= 0) return cudaSuccess;
+  int n2 = 2;
+  while (n2 < n) n2 <<= 1;
+  const size_t smem = size_t(n2) * sizeof(PlanJob);
+  cudaError_t e = cudaFuncSetAttribute(evict_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+  if (e != cudaSuccess) return e;
+  count_launch();
+  return launch_pdl(evict_kernel, dim3(1), dim3(kEvictThreads), smem, s, n, p, freq, eps, out_pri, out_order);
+}
+
+}  // namespace fmoe

@@ -734,6 +734,57 @@ fmoe_status fmoe_select_experts(const fmoe_store* st, int64_t B, const int64_t* 
   return S.finish(r);
 }
 
+fmoe_status fmoe_prefetch_plan(const fmoe_store* st, int64_t B, const int64_t* map_id, const float* score, float delta,
+                               int32_t l_now, int32_t layer_begin, int32_t layer_end, int32_t max_jobs,
+                               int32_t* out_layer, int32_t* out_expert, double* out_priority, int32_t* out_njobs,
+                               void* stream) {
+  if (!st || !map_id || !out_layer || !out_expert || !out_priority || !out_njobs)
+    return fail(FMOE_ERR_INVALID_ARG, "null argument");
+  if (B < 0 || max_jobs < 1) return fail(FMOE_ERR_INVALID_ARG, "B / max_jobs");
+  if (layer_begin < 0 || layer_begin >= layer_end || layer_end > st->cfg.L || l_now >= layer_begin)
+    return fail(FMOE_ERR_INVALID_ARG, "need l_now < layer_begin < layer_end <= L");
+  if ((layer_end - layer_begin) * st->cfg.E > 2048) return fail(FMOE_ERR_INVALID_ARG, "too many (layer, expert) jobs");
+  if (!(delta <= 1.f)) return fail(FMOE_ERR_INVALID_ARG, "delta must be <= 1 (negative = dynamic)");
+  if (delta < 0.f && !score) return fail(FMOE_ERR_INVALID_ARG, "dynamic delta needs score");
+  if (B == 0) return FMOE_OK;
+  DeviceGuard g(st->device);
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  Staging S(s, st->device);
+  const int64_t* did = S.in(map_id, size_t(B));
+  const float* dsc = delta < 0.f ? S.in(score, size_t(B)) : nullptr;
+  int32_t* dl = S.out(out_layer, size_t(B) * max_jobs);
+  int32_t* de = S.out(out_expert, size_t(B) * max_jobs);
+  double* dp = S.out(out_priority, size_t(B) * max_jobs);
+  int32_t* dn = S.out(out_njobs, size_t(B));
+  fmoe_status r = S.check();
+  if (r == FMOE_OK) {
+    cudaError_t e = launch_prefetch_plan(st->view(), int(B), did, dsc, delta, st->cfg.K, l_now, layer_begin,
+                                         layer_end, st->cfg.id_offset, st->n, max_jobs, dl, de, dp, dn, s);
+    if (e != cudaSuccess) r = cuda_fail(e, "plan launch");
+  }
+  return S.finish(r);
+}
+
+fmoe_status fmoe_eviction_order(int64_t n, const float* p, const float* freq, float eps, double* out_priority,
+                                int32_t* out_order, int device, void* stream) {
+  if (n < 1 || n > 8192) return fail(FMOE_ERR_INVALID_ARG, "1 <= n <= 8192");
+  if (!p || !freq || !out_priority || !out_order) return fail(FMOE_ERR_INVALID_ARG, "null argument");
+  if (!(eps > 0.f)) return fail(FMOE_ERR_INVALID_ARG, "eps > 0");
+  DeviceGuard g(device);
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  Staging S(s, device);
+  const float* dp = S.in(p, size_t(n));
+  const float* df = S.in(freq, size_t(n));
+  double* dpr = S.out(out_priority, size_t(n));
+  int32_t* dor = S.out(out_order, size_t(n));
+  fmoe_status r = S.check();
+  if (r == FMOE_OK) {
+    cudaError_t e = launch_eviction_order(int(n), dp, df, eps, dpr, dor, s);
+    if (e != cudaSuccess) r = cuda_fail(e, "eviction launch");
+  }
+  return S.finish(r);
+}
+
 fmoe_status fmoe_topk_merge(int64_t B, int32_t n_lists, int32_t k_in, const float* scores, const int64_t* ids,
                             int32_t k, float* out_score, int64_t* out_id, int device, void* stream) {
   if (B < 0 || n_lists < 0 || k_in < 1 || k_in > FMOE_MAX_K || k < 1 || k > FMOE_MAX_K)

@@ -357,3 +357,41 @@ def test_semantic_cos_matrix_and_insert_cos(lib, B):
         assert torch.equal(ea, eb) and torch.equal(ma, mb)
         a.close()
         b.close()
+
+
+# ---------------------------------------------------------------- cache priorities
+@pytest.mark.parametrize("delta", [-1.0, 0.9])
+def test_prefetch_plan_bit_exact(setup, delta):
+    lib, st, sh = setup["lib"], setup["st"], setup["shape"]
+    rng = np.random.default_rng(11)
+    B, l_now, lb, le, max_jobs = 9, 2, 3, min(3 + 6, sh.L), 40
+    ids = rng.integers(-1, setup["N"], B)
+    sc = rng.uniform(-1, 1, B).astype(np.float32)
+    lay = torch.empty(B, max_jobs, dtype=torch.int32, device="cuda")
+    exp = torch.empty(B, max_jobs, dtype=torch.int32, device="cuda")
+    pri = torch.empty(B, max_jobs, dtype=torch.float64, device="cuda")
+    nj = torch.empty(B, dtype=torch.int32, device="cuda")
+    lib.fmoe_prefetch_plan(st._h, torch.from_numpy(ids).cuda(), torch.from_numpy(sc).cuda(), delta, l_now, lb, le,
+                           max_jobs, lay, exp, pri, nj)
+    plans = O.prefetch_plan(setup["Qm"], ids.tolist(), sc.astype(np.float64).tolist(), float(np.float32(delta)),
+                            list(range(lb, le)), sh.K, l_now)
+    for x in range(B):
+        ref = plans[x][:max_jobs]
+        n = nj[x].item()
+        assert n == len(ref)
+        got = list(zip(lay[x, :n].tolist(), exp[x, :n].tolist(), pri[x, :n].tolist()))
+        assert got == [(t, j, p) for t, j, p in ref]
+        assert (lay[x, n:] == -1).all()
+
+
+def test_eviction_order_bit_exact(lib):
+    rng = np.random.default_rng(12)
+    for n in (1, 7, 256, 1440, 5000):
+        p = rng.choice([0.0, 0.05, 0.1, 0.25, 0.5], size=n).astype(np.float32)
+        f = rng.integers(1, 6, size=n).astype(np.float32)
+        pri = torch.empty(n, dtype=torch.float64, device="cuda")
+        order = torch.empty(n, dtype=torch.int32, device="cuda")
+        lib.fmoe_eviction_order(torch.from_numpy(p).cuda(), torch.from_numpy(f).cuda(), 1e-6, pri, order)
+        rp, ro = O.eviction_order(p.astype(np.float64), f.astype(np.float64), float(np.float32(1e-6)))
+        assert pri.cpu().tolist() == rp
+        assert order.cpu().tolist() == ro
