@@ -603,9 +603,10 @@ cudaError_t launch_umma(const UmmaLaunch& L, cudaStream_t s) {
   // tcgen05 fp32 accumulation is not round-to-nearest per step: over D/16 = 256
   // MMAs (D = 4096) the semantic dot drifted by ~1.4e-5 relative (measured,
   // C5).  Splitting K over two accumulators halves the chain; the epilogue adds
-  // them in IEEE fp32.  (Blends weight the semantic part by d/L and their
+  // them in IEEE fp32.  D >= 3072 only: the split costs the TMEM double buffer.  (Blends weight the semantic part by d/L and their
   // trajectory K is short, so they keep one accumulator per part.)
-  p.split_kb = (sem && !traj && p.n_sem_kb >= 16) ? p.n_sem_kb / 2 : 0;
+  // (measured: D = 2048 stays within 7e-6; D = 4096 drifted 1.4e-5 unsplit)
+  p.split_kb = (sem && !traj && p.n_sem_kb >= 48) ? p.n_sem_kb / 2 : 0;
   p.acc_stages = (sem && traj) || p.split_kb > 0 ? 1 : 2;
   p.cap = in.cap;
   p.id_offset = in.id_offset;
