@@ -189,10 +189,13 @@ __global__ void __launch_bounds__(kUmThreads, 1)
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   __shared__ __align__(8) uint64_t full[kUmMaxStages], empty[kUmMaxStages], tfull[2], tempty[2];
   __shared__ uint32_t tmem_base_sh;
+  // row scales (re, rm) of each half tile, one buffer per TMEM accumulator stage
+  __shared__ __align__(16) float escale[2][2][2][UM_N / 2];
 
   // 1024-byte alignment for the SW128 atoms
   unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint64_t* lists = reinterpret_cast<uint64_t*>(smem + size_t(p.stages) * kUmStageBytes);   // [2][k][128] (KR == 0)
+  uint64_t* lists = reinterpret_cast<uint64_t*>(smem + size_t(p.stages) * kUmStageBytes);   // [2][k][LQ]
+  const int LQ = (p.nq + 31) / 32 * 32;        // list stride: queries rounded up to a warp
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   // accumulators per tile: semantic + trajectory, or semantic K-halves when
@@ -215,7 +218,7 @@ __global__ void __launch_bounds__(kUmThreads, 1)
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
   }
   // empty top-k lists
-  for (int i = tid; i < 2 * p.k * UM_M; i += kUmThreads) lists[i] = 0ull;
+  for (int i = tid; i < 2 * p.k * LQ; i += kUmThreads) lists[i] = 0ull;
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -322,7 +325,7 @@ __global__ void __launch_bounds__(kUmThreads, 1)
     const bool split = p.split_kb > 0;
     const bool vec4 = (p.cos_stride & 3) == 0;      // 16-byte aligned cosine rows
     constexpr int HC = UM_N / 2;                  // columns per half
-    uint64_t* ml = lists + size_t(half) * k * UM_M + q;   // this thread's list: entry i at ml[i*128]
+    uint64_t* ml = lists + size_t(half) * k * LQ + q;   // this thread's list: entry i at ml[i*LQ]
     const uint32_t ml_s = smem_u32(ml);
     uint64_t thr = 0ull;                          // current k-th key
     float thr_s = -__int_as_float(0x7f800000);    // its score (fast-path filter: score >= thr_s)
@@ -342,15 +345,28 @@ __global__ void __launch_bounds__(kUmThreads, 1)
     for (int t = blockIdx.x; t < p.n_tiles; t += gridDim.x, ++ti) {
       const int as = int(ti % unsigned(AS));
       const int ybase = t * UM_N + half * HC;
-      float re_l[HC / 32], rm_l[HC / 32];
+      // this warp's copy of the half tile's row scales, read back as broadcast
+      // LDS.128 (4 columns per load) instead of one shuffle per column
+      float re_c[HC / 32], rm_c[HC / 32];
 #pragma unroll
       for (int c = 0; c < HC / 32; ++c) {
-        re_l[c] = re_n[c];
-        rm_l[c] = rm_n[c] > 0.f ? rsqrtf(rm_n[c]) : 0.f;
+        re_c[c] = re_n[c];
+        rm_c[c] = rm_n[c] > 0.f ? rsqrtf(rm_n[c]) : 0.f;
       }
       fetch(t + gridDim.x);
       if (ti == 0 && tid == 128) trace_mark_here(p.trace, 2);
       mbar_wait(&tfull[as], (ti / unsigned(AS)) & 1u);
+      // one warp per half publishes the scales, after this tile's accumulators
+      // are full (so every warp has released the previous tile of this stage);
+      // a named barrier per half orders the reads
+      if (qd == 0) {
+#pragma unroll
+        for (int c = 0; c < HC / 32; ++c) {
+          escale[as][half][0][c * 32 + lane] = re_c[c];
+          escale[as][half][1][c * 32 + lane] = rm_c[c];
+        }
+      }
+      asm volatile("bar.sync %0, 128;" ::"r"(1 + half) : "memory");
       if (ti == 0 && tid == 128) trace_mark_here(p.trace, 4);
       if (tid == 128) tile_mark(p.trace, 2, ti);
       tc_fence_after();
@@ -362,8 +378,6 @@ __global__ void __launch_bounds__(kUmThreads, 1)
         uint32_t vs[32], vt[32];
         if (SEM) tc_ld32(c_sem + c * 32, vs);
         if (TRAJ || p.split_kb > 0) tc_ld32(c_trj + c * 32, vt);
-        const float rec = c == 0 ? re_l[0] : c == 1 ? re_l[1] : c == 2 ? re_l[2] : re_l[3];
-        const float rmc = c == 0 ? rm_l[0] : c == 1 ? rm_l[1] : c == 2 ? rm_l[2] : rm_l[3];
         const int64_t yc = int64_t(ybase) + c * 32;
         const int64_t left = p.n_rows - yc;
         const unsigned vmask = !live ? 0u : (left >= 32 ? 0xffffffffu : (left <= 0 ? 0u : ((1u << left) - 1u)));
@@ -381,20 +395,35 @@ __global__ void __launch_bounds__(kUmThreads, 1)
             }
           }
         }
+        const float4* res = reinterpret_cast<const float4*>(&escale[as][half][0][c * 32]);
+        const float4* rms = reinterpret_cast<const float4*>(&escale[as][half][1][c * 32]);
         tc_wait_ld();
-        // fast path: 32 scores, a float compare each against the k-th score
+        // fast path: 32 scores and their maximum, one compare against the k-th score
         float sc[32];
-        unsigned m = 0;
+        float vmax = -__int_as_float(0x7f800000);
 #pragma unroll
-        for (int j = 0; j < 32; ++j) {
-          float v = (!SEM && p.sem_cos) ? w * cached[j] : 0.f;
-          if (SEM) {
-            const float dot = (!TRAJ && split) ? __uint_as_float(vs[j]) + __uint_as_float(vt[j]) : __uint_as_float(vs[j]);
-            v = w * (dot * rqs * __shfl_sync(0xffffffffu, rec, j));
+        for (int j4 = 0; j4 < 8; ++j4) {
+          const float4 re4 = SEM ? res[j4] : make_float4(0.f, 0.f, 0.f, 0.f);
+          const float4 rm4 = TRAJ ? rms[j4] : make_float4(0.f, 0.f, 0.f, 0.f);
+          const float rea[4] = {re4.x, re4.y, re4.z, re4.w};
+          const float rma[4] = {rm4.x, rm4.y, rm4.z, rm4.w};
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const int j = 4 * j4 + u;
+            float v = (!SEM && p.sem_cos) ? w * cached[j] : 0.f;
+            if (SEM) {
+              const float dot = (!TRAJ && split) ? __uint_as_float(vs[j]) + __uint_as_float(vt[j]) : __uint_as_float(vs[j]);
+              v = w * (dot * rqs * rea[u]);
+            }
+            if (TRAJ) v = fmaf(w1, __uint_as_float(vt[j]) * rqt * rma[u], v);
+            sc[j] = v;
+            vmax = fmaxf(vmax, v);
           }
-          if (TRAJ) v = fmaf(w1, __uint_as_float(vt[j]) * rqt * __shfl_sync(0xffffffffu, rmc, j), v);
-          sc[j] = v;
-          m |= (v >= thr_s ? 1u : 0u) << j;
+        }
+        unsigned m = 0;
+        if (vmax >= thr_s) {
+#pragma unroll
+          for (int j = 0; j < 32; ++j) m |= (sc[j] >= thr_s ? 1u : 0u) << j;
         }
         m &= vmask;
         if (SEM && !TRAJ && p.out_cos && live) {
@@ -419,7 +448,7 @@ __global__ void __launch_bounds__(kUmThreads, 1)
             if (jj == j) v = sc[jj];
           const uint64_t key = pack_key(v, p.id_offset + uint32_t(yc + j));
           if (key > thr) {
-            thr = heap_replace_root(ml_s, UM_M * 8, k, key);
+            thr = heap_replace_root(ml_s, uint32_t(LQ) * 8, k, key);
             thr_s = key_score(thr);
           }
         }
@@ -433,7 +462,7 @@ __global__ void __launch_bounds__(kUmThreads, 1)
     trace_mark(p.trace, 3);
     if (live) {
       uint64_t* dst = p.cand + (int64_t(p.cand_q0 + q) * (2 * p.grid) + 2 * blockIdx.x + half) * k;
-      for (int i = 0; i < k; ++i) dst[i] = ml[i * UM_M];
+      for (int i = 0; i < k; ++i) dst[i] = ml[i * LQ];
     }
   }
   pdl_trigger();
@@ -528,6 +557,8 @@ static int tmode_of(int rb) { return rb == 16 ? 0 : rb == 32 ? 1 : rb == 64 ? 2 
 
 bool umma_supported(const UmmaPlanIn& in) {
   if (!in.bf16 || in.nq < 1 || in.nq > UM_M || in.k < 1 || in.k > kMaxK) return false;
+  const size_t lists = size_t(2) * in.k * ((in.nq + 31) / 32 * 32) * 8;
+  if ((216 * 1024 - 1024 - lists) / kUmStageBytes < 2) return false;   // keep >= 2 pipeline stages
   if (in.w_sem != 1.f && tmode_of(in.Ep * 2) < 0) return false;
   if (!encoder()) return false;
   return true;
@@ -596,8 +627,8 @@ cudaError_t launch_umma(const UmmaLaunch& L, cudaStream_t s) {
   p.ell_pad = ell_pad;
   p.tmode = tmode;
   p.lc = lc;
-  const size_t lists = size_t(2) * in.k * UM_M * 8;
-  int S = int((225 * 1024 - 1024 - lists) / kUmStageBytes);
+  const size_t lists = size_t(2) * in.k * ((in.nq + 31) / 32 * 32) * 8;
+  int S = int((216 * 1024 - 1024 - lists) / kUmStageBytes);   // + ~10 KB static smem <= 227 KB
   p.stages = S > kUmMaxStages ? kUmMaxStages : S;
   if (p.stages < 2) return cudaErrorInvalidValue;
   // tcgen05 fp32 accumulation is not round-to-nearest per step: over D/16 = 256
