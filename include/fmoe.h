@@ -179,6 +179,11 @@ fmoe_status fmoe_search_blend(const fmoe_store* store, int64_t B, const float* q
  * (4 bytes per query and row, kept in the session), instead of t+1 slabs.
  * The session owns B*capacity*4 bytes of device memory.  Any insert/write to
  * the store invalidates it (the next step returns INVALID_ARG until reset).
+ * Batched sessions (bf16 store, B >= 5) instead keep the query prefixes
+ * (B*L*E*4 bytes) and run the tensor-core scan over the whole prefix each
+ * step, seeded with the previous step's top-k ids (k distinct stored rows
+ * whose scores bound the k-th best from below); results are identical to
+ * fmoe_search_trajectory on the prefix.
  * 1 <= B <= 64. */
 typedef struct fmoe_traj_session fmoe_traj_session;
 fmoe_status fmoe_traj_session_create(const fmoe_store* store, int64_t B, fmoe_traj_session** out);

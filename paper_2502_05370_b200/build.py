@@ -34,7 +34,8 @@ def nvcc() -> str:
 
 def _flags():
     return ARCH + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xptxas", "-v",
-                   "--expt-relaxed-constexpr", "-I" + os.path.join(ROOT, "include"), "-I" + CSRC]
+                   "--expt-relaxed-constexpr", "-I" + os.path.join(ROOT, "include"), "-I" + CSRC] + \
+        os.environ.get("FMOE_NVCC_EXTRA", "").split()     # e.g. -DFMOE_EPI_PROFILE (tools/trace.py)
 
 
 def sources():

@@ -102,6 +102,7 @@ struct UmmaPlanIn {
   int64_t n_rows, cap;
   uint32_t id_offset;
   const void* emb; const void* maps; const float* r_e; const float* psq;
+  int rep;                     // query replication (umma_rep), uniform over a call's passes
 };
 struct UmmaLaunch {
   UmmaPlanIn in;
@@ -109,10 +110,14 @@ struct UmmaLaunch {
   void* scratch;               // umma_scratch_bytes(in)
   float* out_cos; const float* sem_cos; int64_t cos_stride;   // see ScanArgs
   float* valid;                // [nq] validity flags of this pass
+  unsigned long long* gthr;    // [nq] scratch: shared per-query admission thresholds
+  const int64_t* seed_ids;     // optional [nq][seed_stride] ids of seed_n distinct rows (trajectory only)
+  int seed_stride, seed_n;
   uint64_t* cand; int cand_q0; int grid;
   unsigned long long* trace;
 };
 bool umma_supported(const UmmaPlanIn& in);
+int umma_rep(const UmmaPlanIn& in);
 size_t umma_scratch_bytes(const UmmaPlanIn& in);
 int umma_grid(const UmmaPlanIn& in);
 cudaError_t launch_umma(const UmmaLaunch& L, cudaStream_t s);

@@ -139,10 +139,14 @@ struct UmmaParams {
   uint64_t* cand;       // [B][grid][k]
   int cand_q0;          // query offset of this pass in cand
   int grid;
+  int rep;              // query replication R (1, 2, 4): A rows r and r + 128/R hold the same
+                        // query, so all four TMEM lane quadrants (= SM sub-partitions) carry
+                        // live queries when nq <= 64; each replica scores 1/R of the columns
   unsigned long long* trace;
   float* out_cos;               // semantic kernels: cosines [B][cos_stride] (optional)
   const float* sem_cos;         // trajectory kernels: cached semantic cosines to blend (optional)
   int64_t cos_stride;
+  unsigned long long* gthr;     // [nq] shared admission threshold per query (zeroed by prep)
 };
 
 // Sorted insert into a per-thread list in shared memory (entry i at
@@ -162,8 +166,7 @@ __device__ __forceinline__ void sts64(uint32_t a, uint64_t v) {
 // shifting -- the sorted-array insert cost O(k) smem moves and dominated the
 // k = 64 RDY scan).  The merge kernel takes the lists unsorted.  Called only
 // for keys beating the root, out of line.  Returns the new root.
-__device__ __noinline__ uint64_t heap_replace_root(uint32_t l, uint32_t stride, int k, uint64_t key) {
-  int i = 0;
+__device__ __noinline__ uint64_t heap_sift(uint32_t l, uint32_t stride, int k, int i, uint64_t key) {
   while (true) {
     const int c1 = 2 * i + 1;
     if (c1 >= k) break;
@@ -180,6 +183,42 @@ __device__ __noinline__ uint64_t heap_replace_root(uint32_t l, uint32_t stride, 
   sts64(l + uint32_t(i) * stride, key);
   return lds64(l);
 }
+__device__ __forceinline__ uint64_t heap_replace_root(uint32_t l, uint32_t stride, int k, uint64_t key) {
+  return heap_sift(l, stride, k, 0, key);
+}
+// Bottom-up heap construction over an unordered list of k keys; returns the root.
+__device__ __noinline__ uint64_t heapify(uint32_t l, uint32_t stride, int k) {
+  for (int i = k / 2 - 1; i >= 0; --i) heap_sift(l, stride, k, i, lds64(l + uint32_t(i) * stride));
+  return lds64(l);
+}
+// Admit key into a thread's list holding cnt keys: append while filling
+// (cnt < k; the k-th append builds the heap), else replace the root.  Returns
+// the list's k-th key once full, else 0.
+__device__ __noinline__ uint64_t list_admit(uint32_t l, uint32_t stride, int k, int cnt, uint64_t key) {
+  if (cnt < k) {
+    sts64(l + uint32_t(cnt) * stride, key);
+    return cnt + 1 == k ? heapify(l, stride, k) : 0ull;
+  }
+  return heap_sift(l, stride, k, 0, key);
+}
+// Relaxed 64-bit read / max of the shared per-query admission threshold
+__device__ __forceinline__ uint64_t ld_relaxed_u64(const unsigned long long* p) {
+  uint64_t v;
+  asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void red_max_u64(unsigned long long* p, uint64_t v) {
+  asm volatile("red.relaxed.gpu.global.max.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
+// Epilogue cycle accounting for tools/trace.py (build with -DFMOE_EPI_PROFILE):
+// per epilogue thread of CTA 0, clock64 cycles in [tile 0, tile 1, rest] x
+// [tfull wait, named barrier, TMEM load, fast path, rare path, other].
+#ifdef FMOE_EPI_PROFILE
+#define EPI_T(slot) do { const long long c_ = clock64(); cyc[ti < 2 ? ti : 2][slot] += c_ - c_last; c_last = c_; } while (0)
+#else
+#define EPI_T(slot) do { } while (0)
+#endif
 
 template <bool SEM, bool TRAJ>
 __global__ void __launch_bounds__(kUmThreads, 1)
@@ -194,7 +233,7 @@ __global__ void __launch_bounds__(kUmThreads, 1)
 
   // 1024-byte alignment for the SW128 atoms
   unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint64_t* lists = reinterpret_cast<uint64_t*>(smem + size_t(p.stages) * kUmStageBytes);   // [2][k][LQ]
+  uint64_t* lists = reinterpret_cast<uint64_t*>(smem + size_t(p.stages) * kUmStageBytes);   // [2R][k][LQ]
   const int LQ = (p.nq + 31) / 32 * 32;        // list stride: queries rounded up to a warp
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -218,7 +257,7 @@ __global__ void __launch_bounds__(kUmThreads, 1)
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
   }
   // empty top-k lists
-  for (int i = tid; i < 2 * p.k * LQ; i += kUmThreads) lists[i] = 0ull;
+  for (int i = tid; i < 2 * p.rep * p.k * LQ; i += kUmThreads) lists[i] = 0ull;
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -314,10 +353,16 @@ __global__ void __launch_bounds__(kUmThreads, 1)
   } else if (warp >= 4) {
     // ---------------------------------------------------------------- epilogue
     // warp 4+e: TMEM lane quadrant e%4 (a warp may only read its own
-    // quadrant), column half e/4.  Thread = (query, half): its own top-k list.
+    // quadrant), column half e/4.  With replication R the quadrants hold R
+    // copies of 4/R query quadrants; copy `sub` scores the sub-th 1/R of the
+    // half's columns.  Thread = (query, column group): its own top-k list.
     const int e = warp - 4, qd = e & 3, half = e >> 2;
-    const int q = qd * 32 + lane;                 // query of this thread
+    const int R = p.rep, QA = 4 / R;              // query quadrants per replica
+    const int sub = qd / QA;                      // replica index
+    const int NC = (UM_N / 2) / 32 / R;           // 32-column chunks per tile and warp
+    const int q = (qd % QA) * 32 + lane;          // query of this thread
     const bool live = q < p.nq;
+    const int gi = half * R + sub;                // list (column group) index
     const float rqs = (SEM && live) ? p.rq_s[q] : 0.f;
     const float rqt = (TRAJ && live) ? p.rq_t[q] : 0.f;
     const float w = p.w, w1 = 1.f - p.w;
@@ -325,18 +370,41 @@ __global__ void __launch_bounds__(kUmThreads, 1)
     const bool split = p.split_kb > 0;
     const bool vec4 = (p.cos_stride & 3) == 0;      // 16-byte aligned cosine rows
     constexpr int HC = UM_N / 2;                  // columns per half
-    uint64_t* ml = lists + size_t(half) * k * LQ + q;   // this thread's list: entry i at ml[i*LQ]
+    uint64_t* ml = lists + size_t(gi) * k * LQ + q;     // this thread's list: entry i at ml[i*LQ]
     const uint32_t ml_s = smem_u32(ml);
-    uint64_t thr = 0ull;                          // current k-th key
-    float thr_s = -__int_as_float(0x7f800000);    // its score (fast-path filter: score >= thr_s)
+    // Admission: a key enters this thread's list if it beats the list's k-th
+    // key (thr) and the query's shared threshold g: the largest k-th key any
+    // list of this query (any CTA, any column group) has reached -- k better
+    // keys already exist, so nothing below it can be in the final top-k.
+    // The list fills unordered (cnt < k, no sifting) and becomes a min-heap
+    // when full.
+    uint64_t g = 0ull, published = 0ull;
+    int cnt = 0;
+    // filter score (fast path: score >= thr_s); +inf keeps idle lanes out
+    float thr_s = live ? -__int_as_float(0x7f800000) : __int_as_float(0x7f800000);
+    unsigned long long* gq = p.gthr + (live ? q : 0);
+    if (live) {                                    // a seeded scan starts at the seed bound
+      g = ld_relaxed_u64(gq);
+      if (g) thr_s = key_score(g);
+    }
+#ifdef FMOE_EPI_PROFILE
+    const uint64_t g_init = g;
+#endif
+    // single-part scans: fold the (exactly 1) weight and the query norm
+    const float cs = SEM && !TRAJ ? rqs : w * rqs, ct = TRAJ && !SEM ? rqt : w1 * rqt;
     unsigned ti = 0;
-    // per-row scales of the next half tile, loaded one tile ahead
+#ifdef FMOE_EPI_PROFILE
+    long long cyc[3][6] = {}, c_last = clock64();
+    unsigned n_cand_rest = 0;
+#endif
+    // per-row scales of the next half tile, loaded one tile ahead by the
+    // warp that publishes them
     float re_n[HC / 32], rm_n[HC / 32];
     auto fetch = [&](int t) {
 #pragma unroll
       for (int c = 0; c < HC / 32; ++c) {
         const int64_t yl = int64_t(t) * UM_N + half * HC + c * 32 + lane;
-        const bool yok = t < p.n_tiles && yl < p.n_rows;
+        const bool yok = qd == 0 && t < p.n_tiles && yl < p.n_rows;
         re_n[c] = (SEM && yok) ? __ldg(p.r_e + yl) : 0.f;
         rm_n[c] = (TRAJ && yok) ? __ldg(p.psq + yl) : 0.f;
       }
@@ -344,7 +412,7 @@ __global__ void __launch_bounds__(kUmThreads, 1)
     fetch(blockIdx.x);
     for (int t = blockIdx.x; t < p.n_tiles; t += gridDim.x, ++ti) {
       const int as = int(ti % unsigned(AS));
-      const int ybase = t * UM_N + half * HC;
+      const int ybase = t * UM_N + half * HC + sub * NC * 32;   // first column of this warp
       // this warp's copy of the half tile's row scales, read back as broadcast
       // LDS.128 (4 columns per load) instead of one shuffle per column
       float re_c[HC / 32], rm_c[HC / 32];
@@ -355,7 +423,9 @@ __global__ void __launch_bounds__(kUmThreads, 1)
       }
       fetch(t + gridDim.x);
       if (ti == 0 && tid == 128) trace_mark_here(p.trace, 2);
+      EPI_T(5);
       mbar_wait(&tfull[as], (ti / unsigned(AS)) & 1u);
+      EPI_T(0);
       // one warp per half publishes the scales, after this tile's accumulators
       // are full (so every warp has released the previous tile of this stage);
       // a named barrier per half orders the reads
@@ -367,14 +437,17 @@ __global__ void __launch_bounds__(kUmThreads, 1)
         }
       }
       asm volatile("bar.sync %0, 128;" ::"r"(1 + half) : "memory");
+      EPI_T(1);
       if (ti == 0 && tid == 128) trace_mark_here(p.trace, 4);
       if (tid == 128) tile_mark(p.trace, 2, ti);
       tc_fence_after();
+      // the shared threshold, read now and applied after this tile's chunks
+      const uint64_t g_new = live ? ld_relaxed_u64(gq) : 0ull;
       const uint32_t lane_addr = uint32_t(qd * 32) << 16;
-      const uint32_t c_sem = tmem_base + lane_addr + uint32_t(as * NACC * UM_N + half * HC);
+      const uint32_t c_sem = tmem_base + lane_addr + uint32_t(as * NACC * UM_N + half * HC + sub * NC * 32);
       const uint32_t c_trj = c_sem + (NACC == 2 ? UM_N : 0);
 #pragma unroll 1
-      for (int c = 0; c < HC / 32; ++c) {
+      for (int c = 0; c < NC; ++c) {
         uint32_t vs[32], vt[32];
         if (SEM) tc_ld32(c_sem + c * 32, vs);
         if (TRAJ || p.split_kb > 0) tc_ld32(c_trj + c * 32, vt);
@@ -395,9 +468,10 @@ __global__ void __launch_bounds__(kUmThreads, 1)
             }
           }
         }
-        const float4* res = reinterpret_cast<const float4*>(&escale[as][half][0][c * 32]);
-        const float4* rms = reinterpret_cast<const float4*>(&escale[as][half][1][c * 32]);
+        const float4* res = reinterpret_cast<const float4*>(&escale[as][half][0][(sub * NC + c) * 32]);
+        const float4* rms = reinterpret_cast<const float4*>(&escale[as][half][1][(sub * NC + c) * 32]);
         tc_wait_ld();
+        EPI_T(2);
         // fast path: 32 scores and their maximum, one compare against the k-th score
         float sc[32];
         float vmax = -__int_as_float(0x7f800000);
@@ -413,9 +487,10 @@ __global__ void __launch_bounds__(kUmThreads, 1)
             float v = (!SEM && p.sem_cos) ? w * cached[j] : 0.f;
             if (SEM) {
               const float dot = (!TRAJ && split) ? __uint_as_float(vs[j]) + __uint_as_float(vt[j]) : __uint_as_float(vs[j]);
-              v = w * (dot * rqs * rea[u]);
+              v = TRAJ ? w * (dot * rqs * rea[u]) : dot * cs * rea[u];
             }
-            if (TRAJ) v = fmaf(w1, __uint_as_float(vt[j]) * rqt * rma[u], v);
+            if (TRAJ) v = SEM || p.sem_cos ? fmaf(w1, __uint_as_float(vt[j]) * rqt * rma[u], v)
+                                           : __uint_as_float(vt[j]) * ct * rma[u];
             sc[j] = v;
             vmax = fmaxf(vmax, v);
           }
@@ -426,6 +501,7 @@ __global__ void __launch_bounds__(kUmThreads, 1)
           for (int j = 0; j < 32; ++j) m |= (sc[j] >= thr_s ? 1u : 0u) << j;
         }
         m &= vmask;
+        EPI_T(3);
         if (SEM && !TRAJ && p.out_cos && live) {
           float* op = p.out_cos + int64_t(p.cand_q0 + q) * p.cos_stride + yc;
           const int nv = nvalid_rows(yc, p.n_rows, live);
@@ -439,19 +515,44 @@ __global__ void __launch_bounds__(kUmThreads, 1)
           }
         }
         // rare path: exact key order (score desc, id asc) for the candidates
-        while (m) {
-          const int j = __ffs(m) - 1;
-          m &= m - 1;
-          float v = sc[0];
+#ifdef FMOE_EPI_PROFILE
+        if (ti >= 2) n_cand_rest += __popc(m);
+#endif
+#ifdef FMOE_NO_RARE
+        m = 0;
+#endif
+        // (the scores go through a local copy: one indexed load per candidate
+        // instead of a 31-deep select chain)
+        if (m) {
+          const uint32_t idb = p.id_offset + uint32_t(yc);
+          float scl[32];
 #pragma unroll
-          for (int jj = 1; jj < 32; ++jj)
-            if (jj == j) v = sc[jj];
-          const uint64_t key = pack_key(v, p.id_offset + uint32_t(yc + j));
-          if (key > thr) {
-            thr = heap_replace_root(ml_s, uint32_t(LQ) * 8, k, key);
-            thr_s = key_score(thr);
-          }
+          for (int j = 0; j < 32; ++j) scl[j] = sc[j];
+          do {
+            const int j = __ffs(m) - 1;
+            m &= m - 1;
+            const uint64_t key = pack_key(scl[j], idb + uint32_t(j));
+            if (key > g) {
+              const uint64_t root = list_admit(ml_s, uint32_t(LQ) * 8, k, cnt, key);
+              cnt += cnt < k ? 1 : 0;
+              if (root > g) {                     // a full list: its k-th key bounds the query
+                g = root;
+                thr_s = key_score(g);
+              }
+            }
+          } while (m);
         }
+        EPI_T(4);
+      }
+      // publish this list's bound once per tile (atomics per insert contended
+      // at k = 64), then take the shared one read at the start of this tile
+      if (g > published) {
+        red_max_u64(gq, g);
+        published = g;
+      }
+      if (g_new > g) {
+        g = g_new;
+        thr_s = key_score(g);
       }
       tc_fence_before();
       __syncwarp();
@@ -460,9 +561,28 @@ __global__ void __launch_bounds__(kUmThreads, 1)
       if (tid == 128) tile_mark(p.trace, 3, ti);
     }
     trace_mark(p.trace, 3);
-    if (live) {
-      uint64_t* dst = p.cand + (int64_t(p.cand_q0 + q) * (2 * p.grid) + 2 * blockIdx.x + half) * k;
-      for (int i = 0; i < k; ++i) dst[i] = ml[i * LQ];
+#ifdef FMOE_EPI_PROFILE
+    if (p.trace && blockIdx.x == 0)
+      for (int a = 0; a < 3; ++a)
+        for (int b = 0; b < 6; ++b)
+          p.trace[12288 + (tid - 128) * 18 + a * 6 + b] =
+              a == 2 && b == 5 ? n_cand_rest : a == 0 && b == 5 ? g_init : a == 1 && b == 5 ? g : cyc[a][b];
+#endif
+    // fold the 2R column-group lists of each query into group 0's heap, then
+    // one list per (query, CTA) goes out
+    if (live && cnt < k) heapify(ml_s, uint32_t(LQ) * 8, k);   // empty slots are key 0
+    asm volatile("bar.sync 3, %0;" ::"r"(kUmEpiWarps * 32) : "memory");
+    const int te = tid - 128;
+    if (te < p.nq) {
+      const uint32_t l0 = smem_u32(lists + te);
+      uint64_t root = lists[te];
+      for (int g = 1; g < 2 * R; ++g)
+        for (int i = 0; i < k; ++i) {
+          const uint64_t key = lists[(size_t(g) * k + i) * LQ + te];
+          if (key > root) root = heap_replace_root(l0, uint32_t(LQ) * 8, k, key);
+        }
+      uint64_t* dst = p.cand + (int64_t(p.cand_q0 + te) * p.grid + blockIdx.x) * k;
+      for (int i = 0; i < k; ++i) dst[i] = lists[size_t(i) * LQ + te];
     }
   }
   pdl_trigger();
@@ -479,18 +599,36 @@ __global__ void __launch_bounds__(kUmThreads, 1)
 // Quantises the batch to bf16 in the UMMA operand layouts (zero padding to
 // 128 rows, to Dp columns and to ell_pad layers) and computes the inverse norms
 // of the quantised rows (float64 sums) and the validity flags.
+// Seeded trajectory scans (a session step seeded with the previous step's
+// top-k ids): k distinct stored rows whose scores are known bound the k-th
+// best key from below, so the scan may start its admission threshold there.
+struct SeedArgs {
+  const int64_t* ids = nullptr;   // [nq][stride] global ids (this pass); null = no seeds
+  int stride = 0, n = 0, k = 0;   // n seeds per query (k <= n <= 64), bound = k-th best of them
+  uint32_t id_offset = 0;
+  int64_t n_rows = 0, cap = 0;
+  const __nv_bfloat16* maps = nullptr;
+  const float* psq = nullptr;     // prefix squared norms at layer ell-1
+};
+// Margin between a seed score computed here (fp32 FMA over ell*E) and the
+// scan's score of the same row (tcgen05 fp32 accumulation, same bf16 operands):
+// both are within ~1e-6 of the exact cosine; 1e-4 keeps the bound safe.
+constexpr float kSeedMargin = 1e-4f;
+
 __global__ void __launch_bounds__(256) umma_prep_kernel(const float* __restrict__ q_emb, const float* __restrict__ q_prefix,
                                                         int64_t q_stride, int nq, int D, int Dp, int E, int Ep, int ell,
                                                         int ell_pad, __nv_bfloat16* qs, __nv_bfloat16* qt, float* rq_s,
-                                                        float* rq_t, float* valid, int sem, int traj) {
+                                                        float* rq_t, float* valid, int sem, int traj, int qper,
+                                                        unsigned long long* gthr, const SeedArgs sd) {
   pdl_wait();
   __shared__ double red[2][8];
   const int q = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const bool live = q < nq;
+  const int x = q % qper;                        // source query of A row q (replication)
+  const bool live = x < nq;
   double a = 0.0, b = 0.0;
   if (sem) {
     for (int e = tid; e < Dp; e += 256) {
-      const float v = (live && e < D) ? __bfloat162float(__float2bfloat16_rn(q_emb[int64_t(q) * D + e])) : 0.f;
+      const float v = (live && e < D) ? __bfloat162float(__float2bfloat16_rn(q_emb[int64_t(x) * D + e])) : 0.f;
       qs[int64_t(q) * Dp + e] = __float2bfloat16_rn(v);
       a += double(v) * double(v);
     }
@@ -499,7 +637,7 @@ __global__ void __launch_bounds__(256) umma_prep_kernel(const float* __restrict_
     for (int i = tid; i < ell_pad * Ep; i += 256) {
       const int l = i / Ep, j = i - l * Ep;
       const float v = (live && l < ell && j < E)
-                          ? __bfloat162float(__float2bfloat16_rn(q_prefix[int64_t(q) * q_stride + l * E + j]))
+                          ? __bfloat162float(__float2bfloat16_rn(q_prefix[int64_t(x) * q_stride + l * E + j]))
                           : 0.f;
       qt[(int64_t(l) * UM_M + q) * Ep + j] = __float2bfloat16_rn(v);
       b += double(v) * double(v);
@@ -517,7 +655,45 @@ __global__ void __launch_bounds__(256) umma_prep_kernel(const float* __restrict_
     for (int w = 0; w < 8; ++w) { sa += red[0][w]; sb += red[1][w]; }
     rq_s[q] = sa > 0.0 ? float(1.0 / sqrt(sa)) : 0.f;
     rq_t[q] = sb > 0.0 ? float(1.0 / sqrt(sb)) : 0.f;
-    if (live) valid[q] = ((!sem || sa > 0.0) && (!traj || sb > 0.0)) ? 1.f : 0.f;
+    if (live && q == x) valid[q] = ((!sem || sa > 0.0) && (!traj || sb > 0.0)) ? 1.f : 0.f;
+    if (live && q == x) gthr[q] = 0ull;
+    red[0][0] = sb > 0.0 ? 1.0 / sqrt(sb) : 0.0;
+  }
+  if (!(sd.ids && traj && !sem && live && q == x && sd.k > 0 && sd.n >= sd.k && sd.n <= 64)) return;
+  // ---- seed bound: the k-th best trajectory score of the valid seed rows
+  // (ids -1, e.g. from a short candidate union, are skipped), less a margin
+  __shared__ unsigned s_sc[64];
+  __syncthreads();
+  const float rq = float(red[0][0]);
+  for (int i = warp; i < sd.n; i += 8) {
+    const int64_t gid = sd.ids[int64_t(x) * sd.stride + i];
+    const int64_t y = gid - int64_t(sd.id_offset);
+    const bool ok = gid >= 0 && y >= 0 && y < sd.n_rows;
+    float dot = 0.f;
+    if (ok)
+      for (int t = lane; t < ell * E; t += 32) {
+        const int l = t / E, j = t - l * E;
+        const float qv = __bfloat162float(__float2bfloat16_rn(q_prefix[int64_t(x) * q_stride + t]));
+        dot = fmaf(qv, __bfloat162float(sd.maps[(int64_t(l) * sd.cap + y) * Ep + j]), dot);
+      }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) dot += __shfl_xor_sync(0xffffffffu, dot, o);
+    if (lane == 0) {
+      const float ps = ok ? sd.psq[y] : 0.f;
+      const float sc = ps > 0.f ? dot * rq * rsqrtf(ps) : 0.f;
+      s_sc[i] = (ok && sc == sc) ? orderable(sc) : 0u;    // 0: no seed (below every score)
+    }
+  }
+  __syncthreads();
+  if (tid < sd.n && s_sc[tid] != 0u) {
+    // rank of seed tid among the valid seeds (ties by index): rank k-1 is the k-th best
+    const unsigned v = s_sc[tid];
+    int rank = 0;
+    for (int i = 0; i < sd.n; ++i) rank += (s_sc[i] > v || (s_sc[i] == v && i < tid)) ? 1 : 0;
+    if (rank == sd.k - 1) {
+      const float lo = from_orderable(v) - kSeedMargin;
+      gthr[q] = uint64_t(orderable(lo)) << 32;    // below every key of score >= lo
+    }
   }
 }
 
@@ -555,10 +731,31 @@ static bool make_map(CUtensorMap* m, const void* base, uint64_t cols, uint64_t r
 
 static int tmode_of(int rb) { return rb == 16 ? 0 : rb == 32 ? 1 : rb == 64 ? 2 : rb == 128 ? 3 : -1; }
 
+// smem: 1 KB alignment + S stages of 48 KB + 2R lists of k keys per query,
+// within 216 KB (+ ~10 KB static <= 227 KB)
+static size_t lists_bytes(const UmmaPlanIn& in, int R) {
+  return size_t(2 * R) * in.k * ((in.nq + 31) / 32 * 32) * 8;
+}
+static int stages_for(const UmmaPlanIn& in, int R) {
+  const size_t l = lists_bytes(in, R);
+  if (l + 1024 > 216 * 1024) return 0;
+  const int S = int((216 * 1024 - 1024 - l) / kUmStageBytes);
+  return S > kUmMaxStages ? kUmMaxStages : S;
+}
+// Query replication: nq <= 32 uses one TMEM lane quadrant, nq <= 64 two; the
+// other quadrants' epilogue warps (the other SM sub-partitions) would idle, so
+// the query rows are repeated R = 4 / quadrants times and the replicas split
+// the columns.  Backed off while the larger lists would cost pipeline stages.
+int umma_rep(const UmmaPlanIn& in) {
+  int R = in.nq <= 32 ? 4 : (in.nq <= 64 ? 2 : 1);
+  const int s1 = stages_for(in, 1), want = s1 < 3 ? s1 : 3;
+  while (R > 1 && stages_for(in, R) < want) R /= 2;
+  return R;
+}
+
 bool umma_supported(const UmmaPlanIn& in) {
   if (!in.bf16 || in.nq < 1 || in.nq > UM_M || in.k < 1 || in.k > kMaxK) return false;
-  const size_t lists = size_t(2) * in.k * ((in.nq + 31) / 32 * 32) * 8;
-  if ((216 * 1024 - 1024 - lists) / kUmStageBytes < 2) return false;   // keep >= 2 pipeline stages
+  if (stages_for(in, 1) < 2) return false;   // keep >= 2 pipeline stages
   if (in.w_sem != 1.f && tmode_of(in.Ep * 2) < 0) return false;
   if (!encoder()) return false;
   return true;
@@ -584,16 +781,29 @@ cudaError_t launch_umma(const UmmaLaunch& L, cudaStream_t s) {
   const UmmaPlanIn& in = L.in;
   const bool sem = in.w_sem != 0.f && !L.sem_cos, traj = in.w_sem != 1.f;
   const int ell_pad = traj ? in.ell + ((in.Ep * 2 == 16) ? (in.ell & 1) : 0) : 0;
+  const int R = in.rep < 1 ? 1 : in.rep;
   char* scr = static_cast<char*>(L.scratch);
   __nv_bfloat16* qs = reinterpret_cast<__nv_bfloat16*>(scr);
   __nv_bfloat16* qt = reinterpret_cast<__nv_bfloat16*>(scr + qt_offset(in));
   float* rq_s = reinterpret_cast<float*>(scr + rq_offset(in));
   float* rq_t = rq_s + UM_M;
-  // 1. query preparation
+  // 1. query preparation (+ the seed bound)
+  SeedArgs sd;
+  if (L.seed_ids && traj && !sem) {
+    sd.ids = L.seed_ids;
+    sd.stride = L.seed_stride;
+    sd.n = L.seed_n;
+    sd.k = in.k;
+    sd.id_offset = in.id_offset;
+    sd.n_rows = in.n_rows;
+    sd.cap = in.cap;
+    sd.maps = static_cast<const __nv_bfloat16*>(in.maps);
+    sd.psq = in.psq + int64_t(in.ell - 1) * in.cap;
+  }
   count_launch();
   cudaError_t e = launch_pdl(umma_prep_kernel, dim3(UM_M), dim3(256), 0, s, L.q_emb, L.q_prefix, L.q_stride, in.nq,
                              in.D, in.Dp, in.E, in.Ep, in.ell, ell_pad, qs, qt, rq_s, rq_t, L.valid, sem ? 1 : 0,
-                             traj ? 1 : 0);
+                             traj ? 1 : 0, UM_M / R, L.gthr, sd);
   if (e != cudaSuccess) return e;
   // 2. tensor maps
   CUtensorMap tq_s{}, te_s{}, tq_t{}, tm_t{};
@@ -627,10 +837,10 @@ cudaError_t launch_umma(const UmmaLaunch& L, cudaStream_t s) {
   p.ell_pad = ell_pad;
   p.tmode = tmode;
   p.lc = lc;
-  const size_t lists = size_t(2) * in.k * ((in.nq + 31) / 32 * 32) * 8;
-  int S = int((216 * 1024 - 1024 - lists) / kUmStageBytes);   // + ~10 KB static smem <= 227 KB
-  p.stages = S > kUmMaxStages ? kUmMaxStages : S;
+  const size_t lists = lists_bytes(in, R);
+  p.stages = stages_for(in, R);
   if (p.stages < 2) return cudaErrorInvalidValue;
+  p.rep = R;
   // tcgen05 fp32 accumulation is not round-to-nearest per step: over D/16 = 256
   // MMAs (D = 4096) the semantic dot drifted by ~1.4e-5 relative (measured,
   // C5).  Splitting K over two accumulators halves the chain; the epilogue adds
@@ -652,6 +862,7 @@ cudaError_t launch_umma(const UmmaLaunch& L, cudaStream_t s) {
   p.out_cos = L.out_cos;
   p.sem_cos = L.sem_cos;
   p.cos_stride = L.cos_stride;
+  p.gthr = L.gthr;
   const size_t smem = 1024 + size_t(p.stages) * kUmStageBytes + lists;
   using Fn = void (*)(const CUtensorMap, const CUtensorMap, const CUtensorMap, const CUtensorMap, const UmmaParams);
   const Fn fn = sem && traj ? scan_umma_kernel<true, true> : sem ? scan_umma_kernel<true, false>

@@ -11,27 +11,51 @@ void count_launch(int n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
 int64_t launch_count() { return g_launches.load(); }
 
 // ------------------------------------------------------------------ K4 merge
-// One warp per query: stream the candidate keys through a WarpTopK.
+// One CTA per query: 8 warps stream a strided share of the candidate keys
+// through their own WarpTopK with 4 loads in flight per lane, then warp 0
+// merges the 8 lists.
+constexpr int kMergeWarps = 8;
+constexpr int kMergeUnroll = 4;
+
 template <int KPL>
-__global__ void __launch_bounds__(32) merge_keys_kernel(int n_lists, int k_in, const uint64_t* __restrict__ keys,
+__global__ void __launch_bounds__(kMergeWarps * 32) merge_keys_kernel(int n_lists, int k_in, const uint64_t* __restrict__ keys,
                                                         int k, const float* __restrict__ valid_q,
                                                         float* out_score, int64_t* out_id, uint64_t* out_keys) {
+  __shared__ uint64_t sk[kMergeWarps][KPL * 32];
   pdl_wait();
-  const int q = blockIdx.x, lane = threadIdx.x;
+  const int q = blockIdx.x, lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   WarpTopK<KPL> m;
   m.init();
   const int64_t total = int64_t(n_lists) * k_in;
   const uint64_t* src = keys + int64_t(q) * total;
-  for (int64_t j0 = 0; j0 < total; j0 += 32) {
-    const uint64_t key = (j0 + lane < total) ? src[j0 + lane] : 0ull;
-    m.offer(key, k);
+  constexpr int64_t kStep = int64_t(kMergeWarps) * kMergeUnroll * 32;
+  for (int64_t j0 = int64_t(warp) * kMergeUnroll * 32; j0 < total; j0 += kStep) {
+    uint64_t v[kMergeUnroll];
+#pragma unroll
+    for (int u = 0; u < kMergeUnroll; ++u) {
+      const int64_t j = j0 + u * 32 + lane;
+      v[u] = j < total ? __ldcs(src + j) : 0ull;
+    }
+#pragma unroll
+    for (int u = 0; u < kMergeUnroll; ++u) m.offer(v[u], k);
   }
+  m.store(sk[warp], k);
+  __syncthreads();
+  if (warp != 0) return;
+  WarpTopK<KPL> f;
+  f.init();
+  for (int w = 0; w < kMergeWarps; ++w)
+#pragma unroll
+    for (int s = 0; s < KPL; ++s) {
+      const int j = s * 32 + lane;
+      f.offer(j < k ? sk[w][j] : 0ull, k);
+    }
   const bool valid = valid_q ? valid_q[q] != 0.f : true;
 #pragma unroll
   for (int s = 0; s < KPL; ++s) {
     const int j = s * 32 + lane;
     if (j < k) {
-      const uint64_t key = m.v[s];
+      const uint64_t key = f.v[s];
       if (out_keys) out_keys[int64_t(q) * k + j] = valid ? key : 0ull;
       if (out_score) out_score[int64_t(q) * k + j] = valid ? key_score(key) : __int_as_float(0x7fc00000);
       if (out_id) out_id[int64_t(q) * k + j] = valid ? key_id(key) : -1;
@@ -43,9 +67,9 @@ cudaError_t launch_merge_keys(int B, int n_lists, int k_in, const uint64_t* keys
                               float* out_score, int64_t* out_id, uint64_t* out_keys, cudaStream_t s) {
   if (B <= 0) return cudaSuccess;
   if (k <= 32)
-    return count_launch(), launch_pdl(merge_keys_kernel<1>, dim3(B), dim3(32), 0, s, n_lists, k_in, keys, k, valid, out_score, out_id, out_keys);
+    return count_launch(), launch_pdl(merge_keys_kernel<1>, dim3(B), dim3(kMergeWarps * 32), 0, s, n_lists, k_in, keys, k, valid, out_score, out_id, out_keys);
   else
-    return count_launch(), launch_pdl(merge_keys_kernel<2>, dim3(B), dim3(32), 0, s, n_lists, k_in, keys, k, valid, out_score, out_id, out_keys);
+    return count_launch(), launch_pdl(merge_keys_kernel<2>, dim3(B), dim3(kMergeWarps * 32), 0, s, n_lists, k_in, keys, k, valid, out_score, out_id, out_keys);
   count_launch();
   return cudaGetLastError();
 }

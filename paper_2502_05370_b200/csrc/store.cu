@@ -214,6 +214,12 @@ fmoe_status stream_scratch(const fmoe_store* st, cudaStream_t s, size_t bytes, i
 
 size_t align_up(size_t x) { return (x + 255) & ~size_t(255); }
 
+// Batches of at least this many queries go to the tensor cores (bf16 stores).
+int umma_min_batch() {
+  static const int b = getenv("FMOE_UMMA_MIN_B") ? atoi(getenv("FMOE_UMMA_MIN_B")) : 5;
+  return b;
+}
+
 // Batched call on the tensor cores: passes of <= 128 queries, per-CTA lists,
 // then one merge kernel over all passes.
 struct CosArgs {
@@ -224,19 +230,23 @@ struct CosArgs {
 
 fmoe_status run_search_umma(const fmoe_store* st, UmmaPlanIn in, int64_t B, const float* dq, const float* dp,
                             int64_t q_stride, cudaStream_t s, float* ds, int64_t* di, uint64_t* dkeys,
-                            bool check_queries, const CosArgs& cos) {
+                            bool check_queries, const CosArgs& cos, const int64_t* seed_ids, int seed_stride,
+                            int seed_n, int k_out) {
   const int grid = umma_grid(in);
-  const int n_lists = 2 * grid;                       // one list per (CTA, column half)
+  in.rep = umma_rep(in);                              // from the first (largest) pass
+  const int n_lists = grid;                           // one list per (query, CTA)
   const size_t cand_b = align_up(size_t(B) * n_lists * in.k * 8);
   const size_t valid_b = align_up(size_t(B) * 4);
   const size_t prep_b = align_up(umma_scratch_bytes(in));
   char* buf = nullptr;
   unsigned* counters = nullptr;
   unsigned long long* best = nullptr;
-  fmoe_status cs = stream_scratch(st, s, cand_b + valid_b + prep_b, 1, 1, &buf, &counters, &best);
+  const size_t gthr_b = align_up(size_t(B) * 8);
+  fmoe_status cs = stream_scratch(st, s, cand_b + valid_b + prep_b + gthr_b, 1, 1, &buf, &counters, &best);
   if (cs != FMOE_OK) return cs;
   uint64_t* cand = reinterpret_cast<uint64_t*>(buf);
   float* valid = reinterpret_cast<float*>(buf + cand_b);
+  unsigned long long* gthr = reinterpret_cast<unsigned long long*>(buf + cand_b + valid_b + prep_b);
   for (int64_t q0 = 0; q0 < B; q0 += 128) {
     UmmaLaunch L{};
     L.in = in;
@@ -246,6 +256,10 @@ fmoe_status run_search_umma(const fmoe_store* st, UmmaPlanIn in, int64_t B, cons
     L.q_stride = q_stride;
     L.scratch = buf + cand_b + valid_b;
     L.valid = valid + q0;
+    L.gthr = gthr + q0;
+    L.seed_ids = seed_ids ? seed_ids + q0 * seed_stride : nullptr;
+    L.seed_stride = seed_stride;
+    L.seed_n = seed_n;
     L.cand = cand;
     L.cand_q0 = int(q0);
     L.grid = grid;
@@ -256,7 +270,8 @@ fmoe_status run_search_umma(const fmoe_store* st, UmmaPlanIn in, int64_t B, cons
     cudaError_t e = launch_umma(L, s);
     if (e != cudaSuccess) return cuda_fail(e, "umma scan launch");
   }
-  cudaError_t e = launch_merge_keys(int(B), n_lists, in.k, cand, in.k, check_queries ? valid : nullptr, ds, di, dkeys, s);
+  cudaError_t e = launch_merge_keys(int(B), n_lists, in.k, cand, k_out > in.k ? k_out : in.k,
+                                    check_queries ? valid : nullptr, ds, di, dkeys, s);
   return e == cudaSuccess ? FMOE_OK : cuda_fail(e, "merge launch");
 }
 
@@ -265,18 +280,26 @@ fmoe_status run_search_umma(const fmoe_store* st, UmmaPlanIn in, int64_t B, cons
 // the candidate lists (returned in *extra_ptr) for the caller.
 fmoe_status run_search(const fmoe_store* st, int64_t B, const float* dq, const float* dp, int64_t q_stride, int ell,
                        float w, int k, int64_t n_rows, uint32_t id_offset, cudaStream_t s, float* ds, int64_t* di,
-                       uint64_t* dkeys, bool check_queries, const CosArgs& cos = CosArgs()) {
+                       uint64_t* dkeys, bool check_queries, const CosArgs& cos = CosArgs(),
+                       const int64_t* seed_ids = nullptr, int seed_stride = 0, int seed_n = 0, int k_out = 0,
+                       int* out_stride = nullptr) {
+  // k_out > k (tensor-core path only): the merge writes k_out keys per query,
+  // the exact top-k first; *out_stride receives the row stride written
+  if (out_stride) *out_stride = k;
   if (n_rows == 0) {
     cudaError_t e = launch_merge_keys(int(B), 0, k, nullptr, k, nullptr, ds, di, dkeys, s);
     return e == cudaSuccess ? FMOE_OK : cuda_fail(e, "merge launch");
   }
-  static const int umma_min_b = getenv("FMOE_UMMA_MIN_B") ? atoi(getenv("FMOE_UMMA_MIN_B")) : 5;
-  if (st->bf16 && B >= umma_min_b) {
+  if (st->bf16 && B >= umma_min_batch()) {
     UmmaPlanIn in{};
     in.bf16 = 1; in.nq = int(B < 128 ? B : 128); in.k = k; in.D = st->cfg.D; in.Dp = st->Dp; in.E = st->cfg.E;
     in.Ep = st->Ep; in.L = st->cfg.L; in.ell = ell; in.w_sem = w; in.n_rows = n_rows; in.cap = st->cfg.capacity;
     in.id_offset = id_offset; in.emb = st->emb; in.maps = st->maps; in.r_e = st->r_e; in.psq = st->psq;
-    if (umma_supported(in)) return run_search_umma(st, in, B, dq, dp, q_stride, s, ds, di, dkeys, check_queries, cos);
+    if (umma_supported(in)) {
+      if (out_stride && k_out > k) *out_stride = k_out;
+      return run_search_umma(st, in, B, dq, dp, q_stride, s, ds, di, dkeys, check_queries, cos, seed_ids, seed_stride,
+                             seed_n, k_out);
+    }
   }
   ScanArgs a{};
   a.st = st->view();
@@ -542,11 +565,27 @@ fmoe_status fmoe_store_write(fmoe_store* st, int64_t B, const float* emb, const 
 
 }  // extern "C"
 
+// Two implementations behind one API:
+//  * incremental (B below the tensor-core threshold, or an f32 store): the
+//    running per-row dot products acc [B][cap] (traj_session.cu);
+//  * batched (bf16 store, B >= FMOE_UMMA_MIN_B): the session keeps the query
+//    prefixes [B][L][E] and each step runs the tcgen05 scan over the whole
+//    prefix, seeded with the previous step's top-k ids -- k distinct rows
+//    whose scores at the new prefix bound the k-th best key from below, so
+//    the scan's per-query admission threshold starts near its final value
+//    instead of at -inf (the fused top-k otherwise dominates short prefixes).
+constexpr int kSessionSeeds = 32;
+
 struct fmoe_traj_session {
   const fmoe_store* st;
   int64_t B;
-  float* acc = nullptr;      // [B][cap]
-  double* qn = nullptr;      // [2][B]
+  bool batched = false;
+  float* acc = nullptr;      // [B][cap] (incremental)
+  double* qn = nullptr;      // [2][B]   (incremental)
+  float* prefix = nullptr;   // [B][L][E] (batched)
+  int64_t* prev = nullptr;   // [B][kk] the last step's top-kk ids, kk = max(k, 32) (batched)
+  float* sctmp = nullptr;    // [B][kk] its scores
+  int prev_k = 0;
   int layer = 0;
   uint64_t gen = 0;
 };
@@ -562,9 +601,13 @@ fmoe_status fmoe_traj_session_create(const fmoe_store* st, int64_t B, fmoe_traj_
   s->st = st;
   s->B = B;
   s->gen = st->gen;
-  cudaError_t e;
-  if ((e = cudaMalloc(&s->acc, size_t(B) * st->cfg.capacity * 4)) != cudaSuccess ||
-      (e = cudaMalloc(&s->qn, size_t(2) * B * 8)) != cudaSuccess) {
+  s->batched = st->bf16 && B >= umma_min_batch();
+  cudaError_t e = cudaSuccess;
+  if (s->batched ? ((e = cudaMalloc(&s->prefix, size_t(B) * st->cfg.L * st->cfg.E * 4)) != cudaSuccess ||
+                    (e = cudaMalloc(&s->prev, size_t(B) * FMOE_MAX_K * 8)) != cudaSuccess ||
+                    (e = cudaMalloc(&s->sctmp, size_t(B) * FMOE_MAX_K * 4)) != cudaSuccess)
+                 : ((e = cudaMalloc(&s->acc, size_t(B) * st->cfg.capacity * 4)) != cudaSuccess ||
+                    (e = cudaMalloc(&s->qn, size_t(2) * B * 8)) != cudaSuccess)) {
     fmoe_traj_session_destroy(s);
     return cuda_fail(e, "session memory");
   }
@@ -578,12 +621,16 @@ void fmoe_traj_session_destroy(fmoe_traj_session* s) {
   cudaDeviceSynchronize();
   cudaFree(s->acc);
   cudaFree(s->qn);
+  cudaFree(s->prefix);
+  cudaFree(s->prev);
+  cudaFree(s->sctmp);
   delete s;
 }
 
 fmoe_status fmoe_traj_session_reset(fmoe_traj_session* s) {
   if (!s) return fail(FMOE_ERR_INVALID_ARG, "null session");
   s->layer = 0;
+  s->prev_k = 0;
   s->gen = s->st->gen;
   return FMOE_OK;
 }
@@ -607,6 +654,38 @@ fmoe_status fmoe_traj_session_step(fmoe_traj_session* ss, const float* q_layer, 
   if (r == FMOE_OK && st->n == 0) {
     cudaError_t e = launch_merge_keys(int(B), 0, k, nullptr, k, nullptr, ds, di, nullptr, s);
     if (e != cudaSuccess) r = cuda_fail(e, "merge launch");
+  } else if (r == FMOE_OK && ss->batched) {
+    const int L = st->cfg.L, E = st->cfg.E, ell = ss->layer + 1;
+    cudaError_t e = cudaMemcpy2DAsync(ss->prefix + int64_t(ss->layer) * E, size_t(L) * E * 4, dq, size_t(E) * 4,
+                                      size_t(E) * 4, size_t(B), cudaMemcpyDeviceToDevice, s);
+    if (e != cudaSuccess) r = cuda_fail(e, "session prefix copy");
+    // The session keeps kk = max(k, 32) rows per query from the merge: the
+    // exact top-k followed by the next best keys of the per-CTA lists --
+    // distinct rows with high scores, which seed the next step (their k-th
+    // best score at the next prefix is a tight lower bound on its k-th best).
+    // The caller gets the first k.  The seeds are read by the query
+    // preparation kernel before this step's merge rewrites prev (stream order).
+    int kk = k > kSessionSeeds ? k : kSessionSeeds;
+    if (r == FMOE_OK) {
+      const bool seeded = ss->prev_k >= k;
+      r = run_search(st, B, nullptr, ss->prefix, int64_t(L) * E, ell, 0.f, k, st->n, uint32_t(st->cfg.id_offset), s,
+                     ss->sctmp, ss->prev, nullptr, true, CosArgs(), seeded ? ss->prev : nullptr, ss->prev_k,
+                     ss->prev_k, kk, &kk);
+    }
+    if (r == FMOE_OK && ds) {
+      e = cudaMemcpy2DAsync(ds, size_t(k) * 4, ss->sctmp, size_t(kk) * 4, size_t(k) * 4, size_t(B),
+                            cudaMemcpyDeviceToDevice, s);
+      if (e != cudaSuccess) r = cuda_fail(e, "session score copy");
+    }
+    if (r == FMOE_OK && di) {
+      e = cudaMemcpy2DAsync(di, size_t(k) * 8, ss->prev, size_t(kk) * 8, size_t(k) * 8, size_t(B),
+                            cudaMemcpyDeviceToDevice, s);
+      if (e != cudaSuccess) r = cuda_fail(e, "session id copy");
+    }
+    if (r == FMOE_OK) {
+      ss->prev_k = kk;      // == k when the search ran without extra keys
+      ++ss->layer;
+    }
   } else if (r == FMOE_OK) {
     ScanArgs a{};
     a.st = st->view();

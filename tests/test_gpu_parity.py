@@ -307,6 +307,34 @@ def test_trajectory_session_equals_eq2_at_every_prefix(setup, B, k):
         sess.close()
 
 
+@pytest.mark.parametrize("name", ["qwen_small", "mixtral_tiny", "phi_small"])
+def test_batched_session_seeded_equals_stateless(lib, name):
+    """Batched session (bf16, B >= 5): each step is the tcgen05 scan over the
+    whole prefix seeded with the previous step's ids; the seed bound only
+    filters keys that cannot reach the top-k, so every step must equal the
+    stateless search bit for bit -- also when k grows (no seeds) or shrinks."""
+    sh = SHAPES[name]
+    N, B = 5000, 40
+    st, emb, maps = make(lib, sh, N, "bf16")
+    _, qm, _ = S.queries(sh, 1, N, B)
+    Qm = O.quantize(maps, "bf16")
+    sess = st.trajectory_session(B)
+    try:
+        ks = [8, 8, 16, 4, 1, 8]
+        for ell in range(1, sh.L + 1):
+            k = ks[(ell - 1) % len(ks)]
+            gs, gi = sess.step(qm[:, ell - 1].contiguous().cuda(), k)
+            pre = qm[:, :ell].contiguous().cuda()
+            rs, ri = st.search_trajectory(pre, ell, k)
+            assert torch.equal(gi, ri), ell
+            assert torch.equal(gs, rs), ell
+            if ell in (1, 2, 7, sh.L):
+                check_topk(gs, gi, O.trajectory_scores(O.quantize(qm[:, :ell].numpy(), "bf16"), Qm, ell), k)
+    finally:
+        sess.close()
+        st.close()
+
+
 def test_trajectory_session_invalidated_by_insert(lib):
     sh = SHAPES["mixtral_tiny"]
     emb, maps, _ = S.store_rows(sh, 3, 0, 40)

@@ -81,14 +81,25 @@ def main():
         us = timeit(lambda: fm.fmoe_search_trajectory(st._h, pre, ell, a.k, out_s, out_i))
         print(f"traj ell={ell:2d}: {us:8.2f} us  {a.n * ell * a.E * s / us / 1e3:8.1f} GB/s  host {getattr(timeit, 'host_us', 0):.1f} us/call")
     sess = fm.fmoe_traj_session_create(st._h, a.B)
-    lay = qm[:, 0].contiguous()
+    lays = [qm[:, l].contiguous() for l in range(a.L)]
 
     def sweep():
         fm.fmoe_traj_session_reset(sess)
         for ell in range(1, a.L):
-            fm.fmoe_traj_session_step(sess, lay, a.k, out_s, out_i)
+            fm.fmoe_traj_session_step(sess, lays[ell - 1], a.k, out_s, out_i)
     us = timeit(sweep, reps=5, warm=2)
     print(f"session sweep ell=1..{a.L - 1}: {us:8.2f} us ({us / (a.L - 1):.2f} us/step)")
+    # per-step times of one eager sweep (events between steps)
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(a.L)]
+    for rep in range(2):
+        fm.fmoe_traj_session_reset(sess)
+        ev[0].record()
+        for ell in range(1, a.L):
+            fm.fmoe_traj_session_step(sess, lays[ell - 1], a.k, out_s, out_i)
+            ev[ell].record()
+        torch.cuda.synchronize()
+    per = [ev[i - 1].elapsed_time(ev[i]) * 1e3 for i in range(1, a.L)]
+    print("session step us: " + " ".join(f"{ell}:{t:.0f}" for ell, t in enumerate(per, 1)))
     fm.fmoe_traj_session_destroy(sess)
     us = timeit(lambda: fm.fmoe_search_semantic(st._h, qe, a.k, out_s, out_i), reps=50)
     print(f"semantic   : {us:8.2f} us  {a.n * a.D * s / us / 1e3:8.1f} GB/s")

@@ -42,18 +42,18 @@ def main():
     out_i = torch.empty(a.B, a.k, dtype=torch.int64, device="cuda")
 
     sess = fm.fmoe_traj_session_create(st._h, a.B) if a.mode == "session" else None
-    lay = qm[:, 0].contiguous()
+    lays = [qm[:, l].contiguous() for l in range(a.L)]
 
     def call():
         if a.mode == "session":
             fm.fmoe_traj_session_reset(sess)
-            for _ in range(a.ell - 1):
-                fm.fmoe_traj_session_step(sess, lay, a.k, out_s, out_i)
+            for l in range(a.ell - 1):
+                fm.fmoe_traj_session_step(sess, lays[l], a.k, out_s, out_i)
             torch.cuda.synchronize()
             if lib.fmoe_debug_trace(-1, None, 0) == 0 and getattr(call, "arm", False):
                 lib.fmoe_debug_trace(1, None, 0)
                 ev0.record()
-            fm.fmoe_traj_session_step(sess, lay, a.k, out_s, out_i)
+            fm.fmoe_traj_session_step(sess, lays[a.ell - 1], a.k, out_s, out_i)
             return
         if a.mode == "traj":
             fm.fmoe_search_trajectory(st._h, pre, a.ell, a.k, out_s, out_i)
@@ -95,6 +95,22 @@ def main():
         print("  CTA 0 per-tile timeline (us from kernel start): tile | tma_issued | mma_committed | epi_got | epi_done")
         for i in range(min(ntile, 12)):
             print("   ", i, " ".join(f"{(roles[r, i] - t0) / 1e3:8.2f}" for r in range(4)))
+        cy = flat[12288:12288 + 256 * 18].reshape(256, 3, 6).astype(np.int64)
+        if cy.any():      # library built with -DFMOE_EPI_PROFILE
+            print("  epilogue kcycles of lane 0 per warp [tfull bar tmem_ld fast rare other] (rest: other = candidates of the warp, tiles >= 2):")
+            for w in range(8):
+                c = cy[w * 32] // 1000; c[2, 5] = cy[w * 32:(w + 1) * 32, 2, 5].sum()
+                print(f"    warp {w}: tile0 {c[0].tolist()}  tile1 {c[1].tolist()}  rest {c[2].tolist()}")
+            def ksc(u):
+                u = int(u) >> 32
+                if u == 0:
+                    return float("-inf")
+                b = (u & 0x7fffffff) if (u & 0x80000000) else (~u & 0xffffffff)
+                return float(np.array([b], dtype=np.uint32).view(np.float32)[0])
+            g0 = [ksc(v) for v in cy[0:64:8, 0, 5]]
+            g1 = [ksc(v) for v in cy[0:64:8, 1, 5]]
+            print("  initial g score (lanes 0,8,..,56):", ["%.5f" % v for v in g0])
+            print("  final   g score (lanes 0,8,..,56):", ["%.5f" % v for v in g1])
     st.close()
 
 
