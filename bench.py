@@ -84,6 +84,13 @@ def step_counts(cfg):
     return searches, n_traj
 
 
+def batched_session(cfg):
+    """A session over a batch on a bf16 store runs the tcgen05 scan over the whole
+    prefix each step (seeded with the previous step's rows), not the
+    incremental running-dot kernel; its algorithmic bytes are the stateless ones."""
+    return cfg["dtype"] == "bf16" and cfg["B"] >= 5
+
+
 def algorithmic_bytes(cfg, N, traj_mode="stateless", use_cos=False):
     """bytes a scan must stream per launch (store tiles only).
     Session step ell: slab ell-1, the prefix-norm row, and the per-query running
@@ -94,7 +101,7 @@ def algorithmic_bytes(cfg, N, traj_mode="stateless", use_cos=False):
     B = cfg["B"]
     if cfg.get("kind") == "blend":
         traj = {ell: N * (sh.D + ell * sh.E) * s for ell in cfg["ells"]}
-    elif traj_mode == "session":
+    elif traj_mode == "session" and not batched_session(cfg):
         traj = {ell: N * (sh.E * s + 4 + 4 * B * (2 if ell > 1 else 1)) for ell in range(1, sh.L)}
     else:
         traj = {ell: N * ell * sh.E * s for ell in range(1, sh.L)}
@@ -384,8 +391,6 @@ def run_fmoe(args, cfg, rank, world, local_rank):
     else:
         N_local = N_total
         st = build_store(fm, cfg, N_local, 0, dev, args.seed)
-        if cfg["B"] > 4:
-            args.traj = "stateless"    # the session kernel is the B <= 4 streaming path; batches use tcgen05
         step = Step(fm, st, cfg, args.traj, args.cos)
     pool = 4
     qs = make_queries(cfg, N_total, pool, args.seed, dev)
@@ -612,9 +617,11 @@ def main():
                    "k": cfg["k"], "store_dtype": cfg["dtype"], "searches_per_step": searches,
                    "insert": ("RDY semantic half reused from the step's semantic search (fmoe_store_insert_cos)"
                               if args.cos and world == 1 else "full RDY scan"),
-                   "trajectory": ("incremental session: step ell reads slab ell + running dots (SURVEY §8(f) #1)"
-                                  if args.traj == "session" and world == 1 and cfg["B"] <= 4 else
-                                  "stateless: one search over the whole prefix per ell"),
+                   "trajectory": ("stateless: one search over the whole prefix per ell"
+                                  if args.traj != "session" or world > 1 else
+                                  "batched session: per ell one tcgen05 scan over the whole prefix, seeded with "
+                                  "the previous step's rows (fmoe_traj_session_step)" if batched_session(cfg) else
+                                  "incremental session: step ell reads slab ell + running dots (SURVEY §8(f) #1)"),
                    "l2": "inputs larger than L2 (store >> 126 MB), no flush",
                    "launch": "CUDA graph replay of the step (1 GPU)" if (args.graph and world == 1) else "eager"}
 

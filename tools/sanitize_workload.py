@@ -28,10 +28,11 @@ def main():
             st.search_blend(qe[:B].contiguous(), qm[:B].contiguous(), sh.L, -1.0, k)
         s, i = st.search_semantic(qe[:4].contiguous(), 1)
         st.select_experts(i[:, 0].contiguous(), s[:, 0].contiguous(), -1.0, 0, sh.L)
-        sess = st.trajectory_session(2)
-        for ell in range(sh.L):
-            sess.step(qm[:2, ell].contiguous(), 4)
-        sess.close()
+        for Bs in (2, 6):                   # incremental and (bf16) batched sessions
+            sess = st.trajectory_session(Bs)
+            for ell in range(sh.L):
+                sess.step(qm[:Bs, ell].contiguous(), 4)
+            sess.close()
         st.insert(e[N:].contiguous(), m[N:].contiguous())        # replacement path
         st.read(0, 10)
         torch.cuda.synchronize()
