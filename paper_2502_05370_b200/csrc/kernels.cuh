@@ -80,8 +80,11 @@ cudaError_t launch_scan_tma(const ScanArgs& a, cudaStream_t s);
 // Merge per-list candidate keys -> per-query top-k (also fills an empty
 // result when n_lists == 0).  keys [B][n_lists][k_in]; writes (out_score,
 // out_id) and/or out_keys [B][k]; valid (nullable) [B]: 0 -> (NaN, -1).
+// gate (nullable, device): when it holds 0 the launch does nothing (see
+// launch_resolve's need_full).
 cudaError_t launch_merge_keys(int B, int n_lists, int k_in, const uint64_t* keys, int k, const float* valid,
-                              float* out_score, int64_t* out_id, uint64_t* out_keys, cudaStream_t s);
+                              float* out_score, int64_t* out_id, uint64_t* out_keys, cudaStream_t s,
+                              const int* gate = nullptr);
 
 // Incremental trajectory session (traj_session.cu): step `layer` consumes one
 // layer of each query; acc [B][cap] running dots; qn [2][B] running norms.
@@ -111,6 +114,7 @@ struct UmmaLaunch {
   float* out_cos; const float* sem_cos; int64_t cos_stride;   // see ScanArgs
   float* valid;                // [nq] validity flags of this pass
   unsigned long long* gthr;    // [nq] scratch: shared per-query admission thresholds
+  const int* gate;             // nullable device flag: 0 -> every kernel of the launch returns at once
   const int64_t* seed_ids;     // optional [nq][seed_stride] ids of seed_n distinct rows (trajectory only)
   int seed_stride, seed_n;
   uint64_t* cand; int cand_q0; int grid;
@@ -156,9 +160,14 @@ cudaError_t launch_write_rows(const WriteArgs& w, cudaStream_t s);
 // candidate not claimed by an earlier row.  keys [nrep][kk] (from merge).
 //  victims [nrep] (local slot or -1); also scatters to out_slot/out_replaced
 //  at positions x0 + j, and marks appended rows [0, x0) in out_slot/out_replaced.
+//  need_full (nullable): set to 1 when some row found every one of its kk
+//  candidates claimed while its list was full and k_full > kk -- its victim
+//  may lie beyond the kk kept keys (the call's results are then provisional),
+//  else 0.  gate (nullable): skip the launch when *gate == 0.
 cudaError_t launch_resolve(int nrep, int kk, const uint64_t* keys, uint32_t id_offset,
                            int64_t* victims, int x0, int64_t first_append_slot,
-                           int64_t* out_slot, int64_t* out_replaced, cudaStream_t s);
+                           int64_t* out_slot, int64_t* out_replaced, cudaStream_t s,
+                           int* need_full = nullptr, int k_full = 0, const int* gate = nullptr);
 // Victim resolution from merged candidate ids [B][k] (best first).
 cudaError_t launch_resolve_ids(int B, int k, const int64_t* ids, int64_t* out_victim, cudaStream_t s);
 cudaError_t launch_append_ids(int n, int64_t first_slot, uint32_t id_offset, int64_t* out_slot,

@@ -139,6 +139,7 @@ struct UmmaParams {
   uint64_t* cand;       // [B][grid][k]
   int cand_q0;          // query offset of this pass in cand
   int grid;
+  const int* gate;      // nullable device flag: 0 -> return at once
   int rep;              // query replication R (1, 2, 4): A rows r and r + 128/R hold the same
                         // query, so all four TMEM lane quadrants (= SM sub-partitions) carry
                         // live queries when nq <= 64; each replica scores 1/R of the columns
@@ -227,6 +228,13 @@ __global__ void __launch_bounds__(kUmThreads, 1)
                      const UmmaParams p) {
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   __shared__ __align__(8) uint64_t full[kUmMaxStages], empty[kUmMaxStages], tfull[2], tempty[2];
+  if (p.gate) {                                  // a conditional (fallback) scan
+    pdl_wait();
+    if (*p.gate == 0) {
+      pdl_trigger();
+      return;
+    }
+  }
   __shared__ uint32_t tmem_base_sh;
   // row scales (re, rm) of each half tile, one buffer per TMEM accumulator stage
   __shared__ __align__(16) float escale[2][2][2][UM_N / 2];
@@ -619,8 +627,10 @@ __global__ void __launch_bounds__(256) umma_prep_kernel(const float* __restrict_
                                                         int64_t q_stride, int nq, int D, int Dp, int E, int Ep, int ell,
                                                         int ell_pad, __nv_bfloat16* qs, __nv_bfloat16* qt, float* rq_s,
                                                         float* rq_t, float* valid, int sem, int traj, int qper,
-                                                        unsigned long long* gthr, const SeedArgs sd) {
+                                                        unsigned long long* gthr, const SeedArgs sd,
+                                                        const int* gate) {
   pdl_wait();
+  if (gate && *gate == 0) return;
   __shared__ double red[2][8];
   const int q = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int x = q % qper;                        // source query of A row q (replication)
@@ -803,7 +813,7 @@ cudaError_t launch_umma(const UmmaLaunch& L, cudaStream_t s) {
   count_launch();
   cudaError_t e = launch_pdl(umma_prep_kernel, dim3(UM_M), dim3(256), 0, s, L.q_emb, L.q_prefix, L.q_stride, in.nq,
                              in.D, in.Dp, in.E, in.Ep, in.ell, ell_pad, qs, qt, rq_s, rq_t, L.valid, sem ? 1 : 0,
-                             traj ? 1 : 0, UM_M / R, L.gthr, sd);
+                             traj ? 1 : 0, UM_M / R, L.gthr, sd, L.gate);
   if (e != cudaSuccess) return e;
   // 2. tensor maps
   CUtensorMap tq_s{}, te_s{}, tq_t{}, tm_t{};
@@ -863,6 +873,7 @@ cudaError_t launch_umma(const UmmaLaunch& L, cudaStream_t s) {
   p.sem_cos = L.sem_cos;
   p.cos_stride = L.cos_stride;
   p.gthr = L.gthr;
+  p.gate = L.gate;
   const size_t smem = 1024 + size_t(p.stages) * kUmStageBytes + lists;
   using Fn = void (*)(const CUtensorMap, const CUtensorMap, const CUtensorMap, const CUtensorMap, const UmmaParams);
   const Fn fn = sem && traj ? scan_umma_kernel<true, true> : sem ? scan_umma_kernel<true, false>

@@ -20,9 +20,11 @@ constexpr int kMergeUnroll = 4;
 template <int KPL>
 __global__ void __launch_bounds__(kMergeWarps * 32) merge_keys_kernel(int n_lists, int k_in, const uint64_t* __restrict__ keys,
                                                         int k, const float* __restrict__ valid_q,
-                                                        float* out_score, int64_t* out_id, uint64_t* out_keys) {
+                                                        float* out_score, int64_t* out_id, uint64_t* out_keys,
+                                                        const int* gate) {
   __shared__ uint64_t sk[kMergeWarps][KPL * 32];
   pdl_wait();
+  if (gate && *gate == 0) return;
   const int q = blockIdx.x, lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   WarpTopK<KPL> m;
   m.init();
@@ -64,12 +66,13 @@ __global__ void __launch_bounds__(kMergeWarps * 32) merge_keys_kernel(int n_list
 }
 
 cudaError_t launch_merge_keys(int B, int n_lists, int k_in, const uint64_t* keys, int k, const float* valid,
-                              float* out_score, int64_t* out_id, uint64_t* out_keys, cudaStream_t s) {
+                              float* out_score, int64_t* out_id, uint64_t* out_keys, cudaStream_t s,
+                              const int* gate) {
   if (B <= 0) return cudaSuccess;
   if (k <= 32)
-    return count_launch(), launch_pdl(merge_keys_kernel<1>, dim3(B), dim3(kMergeWarps * 32), 0, s, n_lists, k_in, keys, k, valid, out_score, out_id, out_keys);
+    return count_launch(), launch_pdl(merge_keys_kernel<1>, dim3(B), dim3(kMergeWarps * 32), 0, s, n_lists, k_in, keys, k, valid, out_score, out_id, out_keys, gate);
   else
-    return count_launch(), launch_pdl(merge_keys_kernel<2>, dim3(B), dim3(kMergeWarps * 32), 0, s, n_lists, k_in, keys, k, valid, out_score, out_id, out_keys);
+    return count_launch(), launch_pdl(merge_keys_kernel<2>, dim3(B), dim3(kMergeWarps * 32), 0, s, n_lists, k_in, keys, k, valid, out_score, out_id, out_keys, gate);
   count_launch();
   return cudaGetLastError();
 }
@@ -310,10 +313,13 @@ cudaError_t launch_write_rows(const WriteArgs& w, cudaStream_t s) {
 __global__ void __launch_bounds__(32) resolve_kernel(int nrep, int kk, const uint64_t* __restrict__ keys,
                                                      uint32_t id_offset, int64_t* slots_all, int x0,
                                                      int64_t first_append_slot, int64_t* out_slot,
-                                                     int64_t* out_replaced) {
+                                                     int64_t* out_replaced, int* need_full, int k_full,
+                                                     const int* gate) {
   pdl_wait();
+  if (gate && *gate == 0) return;
   __shared__ int64_t claimed[kMaxK];
   const int lane = threadIdx.x;
+  bool need = false;
   for (int x = lane; x < x0; x += 32) {
     slots_all[x] = first_append_slot + x;
     if (out_slot) out_slot[x] = int64_t(id_offset) + first_append_slot + x;
@@ -338,6 +344,8 @@ __global__ void __launch_bounds__(32) resolve_kernel(int nrep, int kk, const uin
         break;
       }
     }
+    // exhausted while the list was full: the victim may lie beyond the kk keys
+    if (best < 0 && k_full > kk && keys[int64_t(j) * kk + kk - 1] != 0ull) need = true;
     if (lane == 0) {
       claimed[j] = best >= 0 ? best : -2;
       slots_all[x0 + j] = best;
@@ -346,13 +354,15 @@ __global__ void __launch_bounds__(32) resolve_kernel(int nrep, int kk, const uin
     }
     __syncwarp();
   }
+  if (need_full && lane == 0) *need_full = need ? 1 : 0;
 }
 
 cudaError_t launch_resolve(int nrep, int kk, const uint64_t* keys, uint32_t id_offset, int64_t* slots_all, int x0,
-                           int64_t first_append_slot, int64_t* out_slot, int64_t* out_replaced, cudaStream_t s) {
+                           int64_t first_append_slot, int64_t* out_slot, int64_t* out_replaced, cudaStream_t s,
+                           int* need_full, int k_full, const int* gate) {
   count_launch();
   return launch_pdl(resolve_kernel, dim3(1), dim3(32), 0, s, nrep, kk, keys, id_offset, slots_all, x0,
-                    first_append_slot, out_slot, out_replaced);
+                    first_append_slot, out_slot, out_replaced, need_full, k_full, gate);
   count_launch();
   return cudaGetLastError();
 }

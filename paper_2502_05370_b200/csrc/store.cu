@@ -220,6 +220,22 @@ int umma_min_batch() {
   return b;
 }
 
+// RDY insert: candidates kept per row by the first pass (see fmoe_store_insert_cos)
+constexpr int kRdyFirst = 8;
+
+// Whether a search of B queries with list length k runs on the tensor cores
+// (fills *in when it does).
+bool umma_plan(const fmoe_store* st, int64_t B, int k, int ell, float w, int64_t n_rows, uint32_t id_offset,
+               UmmaPlanIn* in) {
+  if (!st->bf16 || B < umma_min_batch()) return false;
+  UmmaPlanIn& u = *in;
+  u = UmmaPlanIn{};
+  u.bf16 = 1; u.nq = int(B < 128 ? B : 128); u.k = k; u.D = st->cfg.D; u.Dp = st->Dp; u.E = st->cfg.E;
+  u.Ep = st->Ep; u.L = st->cfg.L; u.ell = ell; u.w_sem = w; u.n_rows = n_rows; u.cap = st->cfg.capacity;
+  u.id_offset = id_offset; u.emb = st->emb; u.maps = st->maps; u.r_e = st->r_e; u.psq = st->psq;
+  return umma_supported(u);
+}
+
 // Batched call on the tensor cores: passes of <= 128 queries, per-CTA lists,
 // then one merge kernel over all passes.
 struct CosArgs {
@@ -231,7 +247,7 @@ struct CosArgs {
 fmoe_status run_search_umma(const fmoe_store* st, UmmaPlanIn in, int64_t B, const float* dq, const float* dp,
                             int64_t q_stride, cudaStream_t s, float* ds, int64_t* di, uint64_t* dkeys,
                             bool check_queries, const CosArgs& cos, const int64_t* seed_ids, int seed_stride,
-                            int seed_n, int k_out) {
+                            int seed_n, int k_out, const int* gate) {
   const int grid = umma_grid(in);
   in.rep = umma_rep(in);                              // from the first (largest) pass
   const int n_lists = grid;                           // one list per (query, CTA)
@@ -260,6 +276,7 @@ fmoe_status run_search_umma(const fmoe_store* st, UmmaPlanIn in, int64_t B, cons
     L.seed_ids = seed_ids ? seed_ids + q0 * seed_stride : nullptr;
     L.seed_stride = seed_stride;
     L.seed_n = seed_n;
+    L.gate = gate;
     L.cand = cand;
     L.cand_q0 = int(q0);
     L.grid = grid;
@@ -271,7 +288,7 @@ fmoe_status run_search_umma(const fmoe_store* st, UmmaPlanIn in, int64_t B, cons
     if (e != cudaSuccess) return cuda_fail(e, "umma scan launch");
   }
   cudaError_t e = launch_merge_keys(int(B), n_lists, in.k, cand, k_out > in.k ? k_out : in.k,
-                                    check_queries ? valid : nullptr, ds, di, dkeys, s);
+                                    check_queries ? valid : nullptr, ds, di, dkeys, s, gate);
   return e == cudaSuccess ? FMOE_OK : cuda_fail(e, "merge launch");
 }
 
@@ -282,7 +299,7 @@ fmoe_status run_search(const fmoe_store* st, int64_t B, const float* dq, const f
                        float w, int k, int64_t n_rows, uint32_t id_offset, cudaStream_t s, float* ds, int64_t* di,
                        uint64_t* dkeys, bool check_queries, const CosArgs& cos = CosArgs(),
                        const int64_t* seed_ids = nullptr, int seed_stride = 0, int seed_n = 0, int k_out = 0,
-                       int* out_stride = nullptr) {
+                       int* out_stride = nullptr, const int* gate = nullptr) {
   // k_out > k (tensor-core path only): the merge writes k_out keys per query,
   // the exact top-k first; *out_stride receives the row stride written
   if (out_stride) *out_stride = k;
@@ -290,17 +307,13 @@ fmoe_status run_search(const fmoe_store* st, int64_t B, const float* dq, const f
     cudaError_t e = launch_merge_keys(int(B), 0, k, nullptr, k, nullptr, ds, di, dkeys, s);
     return e == cudaSuccess ? FMOE_OK : cuda_fail(e, "merge launch");
   }
-  if (st->bf16 && B >= umma_min_batch()) {
-    UmmaPlanIn in{};
-    in.bf16 = 1; in.nq = int(B < 128 ? B : 128); in.k = k; in.D = st->cfg.D; in.Dp = st->Dp; in.E = st->cfg.E;
-    in.Ep = st->Ep; in.L = st->cfg.L; in.ell = ell; in.w_sem = w; in.n_rows = n_rows; in.cap = st->cfg.capacity;
-    in.id_offset = id_offset; in.emb = st->emb; in.maps = st->maps; in.r_e = st->r_e; in.psq = st->psq;
-    if (umma_supported(in)) {
-      if (out_stride && k_out > k) *out_stride = k_out;
-      return run_search_umma(st, in, B, dq, dp, q_stride, s, ds, di, dkeys, check_queries, cos, seed_ids, seed_stride,
-                             seed_n, k_out);
-    }
+  UmmaPlanIn in{};
+  if (umma_plan(st, B, k, ell, w, n_rows, id_offset, &in)) {
+    if (out_stride && k_out > k) *out_stride = k_out;
+    return run_search_umma(st, in, B, dq, dp, q_stride, s, ds, di, dkeys, check_queries, cos, seed_ids, seed_stride,
+                           seed_n, k_out, gate);
   }
+  if (gate) return fail(FMOE_ERR_UNSUPPORTED, "gated search needs the tensor-core path");
   ScanArgs a{};
   a.st = st->view();
   a.n_rows = n_rows;
@@ -494,21 +507,39 @@ fmoe_status fmoe_store_insert_cos(fmoe_store* st, int64_t B, const float* emb, c
   fmoe_status r = S.check();
   const uint32_t off = uint32_t(st->cfg.id_offset);
   if (r == FMOE_OK && nrep > 0) {
+    // Row j (batch order) takes its best candidate not claimed by rows < j, so
+    // kk = min(nrep, n0) candidates per row always suffice.  Most batches need
+    // far fewer: a first pass keeps kRdyFirst, and only when some row finds
+    // all of them claimed does a second, gated pass (device flag, no host
+    // sync) rescan with kk and redo the resolution -- same result either way.
     const int kk = int(nrep < n0 ? nrep : n0);
+    const float w = float(st->cfg.d) / float(L);
+    const int k1 = kk < kRdyFirst ? kk : kRdyFirst;
+    UmmaPlanIn p1{}, p2{};
+    const bool two = k1 < kk && umma_plan(st, nrep, k1, L, w, n0, 0u, &p1) && umma_plan(st, nrep, kk, L, w, n0, 0u, &p2);
     uint64_t* keys = static_cast<uint64_t*>(S.scratch(size_t(nrep) * (kk > 0 ? kk : 1) * 8));
+    uint64_t* keys1 = two ? static_cast<uint64_t*>(S.scratch(size_t(nrep) * k1 * 8)) : nullptr;
+    int* need = two ? static_cast<int*>(S.scratch(sizeof(int))) : nullptr;
     r = S.check();
-    if (r == FMOE_OK && kk > 0) {
-      // RDY_{x,y} = d/L sem + (L-d)/L traj over full maps, against
-      // the contexts present before this call: rows [0, n0).
-      const float w = float(st->cfg.d) / float(L);
-      CosArgs cos;
-      cos.in = dcos ? dcos + a * cos_stride : nullptr;     // cos(emb_x, sem_y) from the semantic search
-      cos.stride = cos_stride;
-      r = run_search(st, nrep, de + a * D, dm + a * int64_t(L) * E, int64_t(L) * E, L, w, kk, n0, 0u, s, nullptr,
-                     nullptr, keys, false, cos);
+    // RDY_{x,y} = d/L sem + (L-d)/L traj over full maps, against
+    // the contexts present before this call: rows [0, n0).
+    CosArgs cos;
+    cos.in = dcos ? dcos + a * cos_stride : nullptr;     // cos(emb_x, sem_y) from the semantic search
+    cos.stride = cos_stride;
+    const float* qe = de + a * D;
+    const float* qm = dm + a * int64_t(L) * E;
+    if (r == FMOE_OK && two) {
+      r = run_search(st, nrep, qe, qm, int64_t(L) * E, L, w, k1, n0, 0u, s, nullptr, nullptr, keys1, false, cos);
+      if (r == FMOE_OK) {
+        cudaError_t e = launch_resolve(int(nrep), k1, keys1, off, slots_all, int(a), n0, dslot, drep, s, need, kk);
+        if (e != cudaSuccess) r = cuda_fail(e, "resolve launch");
+      }
     }
+    if (r == FMOE_OK && kk > 0)
+      r = run_search(st, nrep, qe, qm, int64_t(L) * E, L, w, kk, n0, 0u, s, nullptr, nullptr, keys, false, cos,
+                     nullptr, 0, 0, 0, nullptr, need);
     if (r == FMOE_OK) {
-      cudaError_t e = launch_resolve(int(nrep), kk, keys, off, slots_all, int(a), n0, dslot, drep, s);
+      cudaError_t e = launch_resolve(int(nrep), kk, keys, off, slots_all, int(a), n0, dslot, drep, s, nullptr, 0, need);
       if (e != cudaSuccess) r = cuda_fail(e, "resolve launch");
     }
   } else if (r == FMOE_OK) {

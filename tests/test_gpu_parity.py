@@ -243,6 +243,29 @@ def test_insert_duplicate_batch_distinct_victims(lib):
     st.close()
 
 
+@pytest.mark.parametrize("n_dup", [6, 30, 64])
+def test_insert_many_conflicts_two_pass(lib, n_dup):
+    """A batch of n_dup copies of one stored context plus fresh rows: the
+    copies compete for the same victims, so beyond the first-pass list length
+    (8) rows find all their candidates claimed and the gated full-length pass
+    must take over; the result equals the oracle's R8 resolution."""
+    sh = S.Shape("qw", 6, 60, 4, 200, n_clusters=8)
+    C = 1500
+    emb, maps, _ = S.store_rows(sh, 13, 0, C + 64)
+    st = lib.ExpertMapStore(sh.L, sh.E, sh.K, sh.D, 3, C, "bf16")
+    st.insert(emb[:C].cuda(), maps[:C].cuda())
+    ref = O.Store(C, sh.L, sh.E, sh.D, 3)
+    ref.insert(O.quantize(emb[:C].numpy(), "bf16"), O.quantize(maps[:C].numpy(), "bf16"))
+    be = torch.cat([emb[40:41].repeat(n_dup, 1), emb[C:C + 64 - n_dup]])
+    bm = torch.cat([maps[40:41].repeat(n_dup, 1, 1), maps[C:C + 64 - n_dup]])
+    slot, rep = st.insert(be.cuda(), bm.cuda())
+    rs, rr = ref.insert(O.quantize(be.numpy(), "bf16"), O.quantize(bm.numpy(), "bf16"))
+    assert slot.cpu().tolist() == rs
+    assert rep.cpu().tolist() == rr
+    assert len(set(rs)) == 64
+    st.close()
+
+
 def test_topk_merge_api(lib):
     rng = np.random.default_rng(3)
     G, B, kin, k = 4, 5, 8, 8
