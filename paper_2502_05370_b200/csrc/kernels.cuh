@@ -106,6 +106,7 @@ struct UmmaPlanIn {
   uint32_t id_offset;
   const void* emb; const void* maps; const float* r_e; const float* psq;
   int rep;                     // query replication (umma_rep), uniform over a call's passes
+  int cg;                      // 1: CTAs, 2: CTA pairs (M = 256); 0 = by nq.  Uniform over a call's passes
 };
 struct UmmaLaunch {
   UmmaPlanIn in;
@@ -123,7 +124,8 @@ struct UmmaLaunch {
 bool umma_supported(const UmmaPlanIn& in);
 int umma_rep(const UmmaPlanIn& in);
 size_t umma_scratch_bytes(const UmmaPlanIn& in);
-int umma_grid(const UmmaPlanIn& in);
+int umma_grid(const UmmaPlanIn& in);   // CTAs to launch (a multiple of umma_cg)
+int umma_cg(const UmmaPlanIn& in);
 cudaError_t launch_umma(const UmmaLaunch& L, cudaStream_t s);
 // Merge (score, id) lists from an all-gather: [n_lists][B][k_in].
 cudaError_t launch_merge_lists(int B, int n_lists, int k_in, const float* scores,

@@ -1,6 +1,10 @@
 // scan_umma.cu -- K3: batched scoring on the 5th-gen tensor cores (tcgen05),
 // fused with a per-query top-k epilogue.  bf16 stores, 5 <= B <= 128 queries
-// per pass.
+// per pass on single CTAs, 129..256 on CTA pairs (cta_group::2, M = 256: each
+// CTA of a pair holds 128 query rows and half of every 256-row store tile, the
+// leader issues the MMAs for both, each CTA's TMEM receives its own queries'
+// accumulators; the peer's loads are relayed to the leader's stage barrier and
+// the MMA commits multicast to both CTAs).
 //
 // What it computes (Eq. 1, Eq. 2 and the RDY blend):
 //   S_sem [x][y] = (q~_x . e~_y) * r_q(x) * r_e[y]
@@ -33,8 +37,12 @@
 // spans two layers (LBO = the layer stride inside the stage); RB = 32 (Phi):
 // SWIZZLE_32B, one MMA per layer; RB = 64: SWIZZLE_64B, 2 MMAs per layer;
 // RB = 128 (Qwen, E = 60 padded to 64): SWIZZLE_128B, 4 MMAs per layer.
+// RB = 16 operands are moved with 1-D bulk copies (a layer's rows of a tile are
+// one contiguous run of the slab): 16-byte-wide tensor boxes cost one TMA
+// request per row and held the Mixtral-shape trajectory scan at 1.6 TB/s.
 #include <cuda.h>
 
+#include <cstdlib>
 #include <map>
 #include <mutex>
 
@@ -47,10 +55,11 @@ constexpr int UM_M = 128;
 constexpr int UM_N = 256;
 constexpr int kUmEpiWarps = 8;               // 2 per SM sub-partition: two column halves
 constexpr int kUmThreads = (4 + kUmEpiWarps) * 32;
-constexpr int kStageA = UM_M * 128;          // 16 KB
-constexpr int kStageB = UM_N * 128;          // 32 KB
-constexpr int kUmStageBytes = kStageA + kStageB;
-constexpr int kUmMaxStages = 4;
+constexpr int kStageA = UM_M * 128;          // 16 KB of queries per stage (per CTA)
+// store rows per CTA and tile: all 256 (cta_group::1), or half (cta_group::2)
+__host__ __device__ constexpr int um_rows(int cg) { return UM_N / cg; }
+__host__ __device__ constexpr int um_stage_bytes(int cg) { return kStageA + um_rows(cg) * 128; }
+constexpr int kUmMaxStages = 8;
 
 __device__ __forceinline__ int nvalid_rows(int64_t yc, int64_t n_rows, bool live) {
   if (!live) return 0;
@@ -75,12 +84,81 @@ __device__ __forceinline__ void tc_commit(uint64_t* bar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
                : "memory");
 }
-__device__ __forceinline__ void tc_mma(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc, uint32_t idesc, uint32_t acc) {
+// cta_group::2: the commit arrives on the barrier at the same offset in both
+// CTAs of the pair (multicast mask 0b11)
+__device__ __forceinline__ void tc_commit_pair(uint64_t* bar) {
   asm volatile(
-      "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
-      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
-      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(acc)
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+          smem_u32(bar)),
+      "h"(uint16_t(3))
       : "memory");
+}
+template <int CG>
+__device__ __forceinline__ void tc_mma(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc, uint32_t idesc, uint32_t acc) {
+  if constexpr (CG == 1)
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
+        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(acc)
+        : "memory");
+  else
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
+        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(acc)
+        : "memory");
+}
+// thread-block cluster helpers (CTA pairs)
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+// shared::cluster address of the same variable in CTA `rank` of the cluster
+__device__ __forceinline__ uint32_t mapa_rank(const void* p, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(smem_u32(p)), "r"(rank));
+  return r;
+}
+__device__ __forceinline__ void mbar_arrive_remote(uint32_t cluster_addr) {
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
+}
+// L2 prefetches (no smem, no barrier): the store operand of a k-block issued
+// ahead of the smem ring, so its TMA load later hits L2
+__device__ __forceinline__ void tma_prefetch_l2(const CUtensorMap* map, int c0, int c1) {
+  asm volatile("cp.async.bulk.prefetch.tensor.2d.L2.global.tile [%0, {%1, %2}];" ::"l"(reinterpret_cast<uint64_t>(map)),
+               "r"(c0), "r"(c1)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_prefetch_l2(const void* src, unsigned bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
+}
+// Non-critical waiter (the epilogue warps wait most of a tile for its
+// accumulators): poll with test_wait and a real sleep in between.  The
+// try_wait suspend loop wakes on every mbarrier event of the CTA -- each TMA
+// complete_tx -- so eight warps waking every ~100 cycles competed with the
+// producer/MMA barrier traffic.
+__device__ __forceinline__ bool mbar_test(uint64_t* bar, unsigned parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tmbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n\tselp.u32 %0, 1, 0, p;\n\t}"
+      : "=r"(ok)
+      : "r"(smem_u32(bar)), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
+__device__ __forceinline__ void mbar_wait_backoff(uint64_t* bar, unsigned parity, unsigned ns) {
+  while (!mbar_test(bar, parity)) __nanosleep(ns);
+}
+// global -> shared 1-D bulk copy without a cache hint (query operands: re-read by every tile)
+__device__ __forceinline__ void bulk_g2s_plain(void* dst, const void* src, unsigned bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_u32(dst)),
+               "l"(src), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
 }
 __device__ __forceinline__ void tc_ld32(uint32_t taddr, uint32_t (&r)[32]) {
   asm volatile(
@@ -119,7 +197,7 @@ struct UmmaParams {
   int64_t n_rows;       // rows to scan
   int n_tiles;
   int k;                // list length
-  int nq;               // queries of this pass (<= 128)
+  int nq;               // queries of this pass (<= 128 * CG; CTA r of a pair owns rows r*128..)
   float w;              // blend weight
   int n_sem_kb;         // semantic k-blocks (64 elements), 0 if no semantic part
   int n_traj_kb;        // trajectory k-blocks (stages)
@@ -128,9 +206,14 @@ struct UmmaParams {
   int lc;               // layers per trajectory stage
   int stages;
   int acc_stages;       // TMEM accumulator buffers (1 or 2)
+  int epi_sleep;        // epilogue accumulator wait: ns between polls (0 = try_wait suspend loop)
+  int l2pf;             // L2 prefetch distance of the store operand, in k-blocks (0 = off)
   int split_kb;         // semantic-only: k-blocks >= split_kb accumulate into a second TMEM
                         // accumulator, summed in fp32 by the epilogue (0 = no split)
   int64_t cap;          // slab stride (rows) of the map tensor
+  int L;                // map layers (slabs)
+  const unsigned char* maps;   // map slabs (bulk-copy path, RB = 16)
+  const unsigned char* qt;     // trajectory query operand [CG][ell_pad][128][Ep] (bulk-copy path)
   uint32_t id_offset;
   const float* rq_s;    // [128] query inverse norms (0 for padding rows)
   const float* rq_t;
@@ -138,7 +221,7 @@ struct UmmaParams {
   const float* psq;     // [cap] prefix squared norms at layer ell-1 (traj)
   uint64_t* cand;       // [B][grid][k]
   int cand_q0;          // query offset of this pass in cand
-  int grid;
+  int grid;             // lists per query = CTAs / CG
   const int* gate;      // nullable device flag: 0 -> return at once
   int rep;              // query replication R (1, 2, 4): A rows r and r + 128/R hold the same
                         // query, so all four TMEM lane quadrants (= SM sub-partitions) carry
@@ -221,7 +304,7 @@ __device__ __forceinline__ void red_max_u64(unsigned long long* p, uint64_t v) {
 #define EPI_T(slot) do { } while (0)
 #endif
 
-template <bool SEM, bool TRAJ>
+template <bool SEM, bool TRAJ, int CG>
 __global__ void __launch_bounds__(kUmThreads, 1)
     scan_umma_kernel(const __grid_constant__ CUtensorMap tm_qs, const __grid_constant__ CUtensorMap tm_es,
                      const __grid_constant__ CUtensorMap tm_qt, const __grid_constant__ CUtensorMap tm_mt,
@@ -230,7 +313,7 @@ __global__ void __launch_bounds__(kUmThreads, 1)
   __shared__ __align__(8) uint64_t full[kUmMaxStages], empty[kUmMaxStages], tfull[2], tempty[2];
   if (p.gate) {                                  // a conditional (fallback) scan
     pdl_wait();
-    if (*p.gate == 0) {
+    if (*p.gate == 0) {                          // (both CTAs of a pair read the same flag)
       pdl_trigger();
       return;
     }
@@ -239,10 +322,20 @@ __global__ void __launch_bounds__(kUmThreads, 1)
   // row scales (re, rm) of each half tile, one buffer per TMEM accumulator stage
   __shared__ __align__(16) float escale[2][2][2][UM_N / 2];
 
-  // 1024-byte alignment for the SW128 atoms
+  // 1024-byte alignment for the SW128 atoms (the same offsets in both CTAs of a pair)
   unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint64_t* lists = reinterpret_cast<uint64_t*>(smem + size_t(p.stages) * kUmStageBytes);   // [2R][k][LQ]
-  const int LQ = (p.nq + 31) / 32 * 32;        // list stride: queries rounded up to a warp
+  constexpr int NB = um_rows(CG);                // store rows of a tile held by this CTA
+  constexpr int SBY = um_stage_bytes(CG);
+  uint64_t* lists = reinterpret_cast<uint64_t*>(smem + size_t(p.stages) * SBY);   // [2R][k][LQ]
+  // CTA pair (cta_group::2): rank r owns query rows r*128.. of the M = 256
+  // operand and store rows r*128.. of each 256-row tile; the leader (rank 0)
+  // issues the MMAs for both, the accumulators of its queries land in each
+  // CTA's own TMEM
+  const int rank = CG == 2 ? int(cluster_rank()) : 0;
+  const bool leader = rank == 0;
+  const int cid = int(blockIdx.x) / CG, ncl = int(gridDim.x) / CG;
+  const int nq_c = p.nq - rank * UM_M < 0 ? 0 : (p.nq - rank * UM_M > UM_M ? UM_M : p.nq - rank * UM_M);
+  const int LQ = (nq_c + 31) / 32 * 32;          // list stride: queries rounded up to a warp
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   // accumulators per tile: semantic + trajectory, or semantic K-halves when
@@ -251,8 +344,9 @@ __global__ void __launch_bounds__(kUmThreads, 1)
   const int S = p.stages, AS = p.acc_stages;
 
   if (tid == 0) {
-    for (int s = 0; s < S; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
-    for (int a = 0; a < AS; ++a) { mbar_init(&tfull[a], 1); mbar_init(&tempty[a], kUmEpiWarps); }
+    // the leader's stage barrier also waits for the peer's relay arrival
+    for (int s = 0; s < S; ++s) { mbar_init(&full[s], (CG == 2 && leader) ? 2 : 1); mbar_init(&empty[s], 1); }
+    for (int a = 0; a < AS; ++a) { mbar_init(&tfull[a], 1); mbar_init(&tempty[a], CG * kUmEpiWarps); }
     mbar_fence_init();
   }
   if (warp == 0 && lane == 0) {
@@ -260,14 +354,21 @@ __global__ void __launch_bounds__(kUmThreads, 1)
     if (TRAJ) { tma_prefetch(&tm_qt); tma_prefetch(&tm_mt); }
   }
   if (warp == 2) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(&tmem_base_sh))
-                 : "memory");
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    if constexpr (CG == 1) {
+      asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(&tmem_base_sh))
+                   : "memory");
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    } else {
+      asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(&tmem_base_sh))
+                   : "memory");
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+    }
   }
   // empty top-k lists
   for (int i = tid; i < 2 * p.rep * p.k * LQ; i += kUmThreads) lists[i] = 0ull;
   tc_fence_before();
-  __syncthreads();
+  if constexpr (CG == 2) cluster_sync_all();      // peer barriers initialised before any remote arrive
+  else __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = tmem_base_sh;
   trace_mark(p.trace, 0);
@@ -279,39 +380,99 @@ __global__ void __launch_bounds__(kUmThreads, 1)
   if (warp == 0) {
     // ---------------------------------------------------------------- TMA producer
     if (lane == 0) {
+      const uint64_t pol = policy_evict_first();
+      // store operand of k-block kb of tile t -> L2
+      auto prefetch = [&](int t, int kb) {
+        const int y0 = t * UM_N + rank * NB;
+        if (SEM && kb < p.n_sem_kb) {
+          tma_prefetch_l2(&tm_es, kb * 64, y0);
+          return;
+        }
+        const int l0 = (kb - p.n_sem_kb) * p.lc;
+        const int nl = p.ell_pad - l0 < p.lc ? p.ell_pad - l0 : p.lc;
+        if (p.tmode == 0) {
+          const int64_t left = p.cap - y0;
+          const int rows = left >= NB ? NB : (left <= 0 ? 0 : int(left));
+          if (rows > 0)
+            for (int l = 0; l < nl && l0 + l < p.L; ++l)
+              bulk_prefetch_l2(p.maps + (int64_t(l0 + l) * p.cap + y0) * 16, unsigned(rows * 16));
+        } else {
+          for (int l = 0; l < nl; ++l) tma_prefetch_l2(&tm_mt, 0, int((l0 + l) * p.cap + y0));
+        }
+      };
+      int pt = cid, pkb = 0;                     // prefetch cursor, l2pf k-blocks ahead
+      for (int i = 0; i < p.l2pf && pt < p.n_tiles; ++i)
+        if (++pkb == n_kb) { pkb = 0; pt += ncl; }
       unsigned u = 0;
-      for (int t = blockIdx.x; t < p.n_tiles; t += gridDim.x) {
-        const int y0 = t * UM_N;
+      for (int t = cid; t < p.n_tiles; t += ncl) {
+        const int y0 = t * UM_N + rank * NB;           // this CTA's store rows of the tile
         for (int kb = 0; kb < n_kb; ++kb, ++u) {
           const int s = int(u % unsigned(S));
+          if (p.l2pf > 0 && pt < p.n_tiles) {
+            prefetch(pt, pkb);
+            if (++pkb == n_kb) { pkb = 0; pt += ncl; }
+          }
           mbar_wait(&empty[s], ((u / unsigned(S)) & 1u) ^ 1u);
-          unsigned char* sa = smem + size_t(s) * kUmStageBytes;
+          unsigned char* sa = smem + size_t(s) * SBY;
           unsigned char* sb = sa + kStageA;
           if (SEM && kb < p.n_sem_kb) {
-            mbar_arrive_expect_tx(&full[s], kUmStageBytes);
-            tma_load_2d(sa, &tm_qs, kb * 64, 0, &full[s]);
+            mbar_arrive_expect_tx(&full[s], unsigned(SBY));
+            tma_load_2d(sa, &tm_qs, kb * 64, rank * UM_M, &full[s]);
             tma_load_2d(sb, &tm_es, kb * 64, y0, &full[s]);
           } else {
             const int j = kb - p.n_sem_kb;
             const int l0 = j * p.lc;
             const int nl = p.ell_pad - l0 < p.lc ? p.ell_pad - l0 : p.lc;
-            mbar_arrive_expect_tx(&full[s], unsigned(nl * (UM_M + UM_N) * RB));
-            for (int l = 0; l < nl; ++l) {
-              tma_load_2d(sa + l * UM_M * RB, &tm_qt, 0, (l0 + l) * UM_M, &full[s]);
-              tma_load_2d(sb + l * UM_N * RB, &tm_mt, 0, int((l0 + l) * p.cap + y0), &full[s]);
+            if (p.tmode == 0) {
+              // 16-byte rows: a layer's NB rows are one contiguous run of the
+              // slab and already the no-swizzle K-major core-matrix layout, so
+              // 1-D bulk copies replace 16-byte-wide tensor boxes (which cost
+              // one TMA request per row)
+              const int64_t left = p.cap - y0;
+              const int rows = left >= NB ? NB : (left <= 0 ? 0 : int(left));
+              const unsigned ba = unsigned(nl * UM_M * 16), bb = unsigned(rows * 16);
+              mbar_arrive_expect_tx(&full[s], ba + unsigned(nl) * bb);
+              bulk_g2s_plain(sa, p.qt + (size_t(rank) * p.ell_pad + l0) * UM_M * 16, ba, &full[s]);
+              if (rows > 0)
+                for (int l = 0; l < nl; ++l) {
+                  // a padding layer past the last slab re-reads a real one: finite
+                  // values against the zero query columns
+                  const int ls = l0 + l < p.L ? l0 + l : p.L - 1;
+                  bulk_g2s(sb + l * NB * 16, p.maps + (int64_t(ls) * p.cap + y0) * 16, bb, &full[s], pol);
+                }
+            } else {
+              mbar_arrive_expect_tx(&full[s], unsigned(nl * (UM_M + NB) * RB));
+              for (int l = 0; l < nl; ++l) {
+                tma_load_2d(sa + l * UM_M * RB, &tm_qt, 0, (rank * p.ell_pad + l0 + l) * UM_M, &full[s]);
+                tma_load_2d(sb + l * NB * RB, &tm_mt, 0, int((l0 + l) * p.cap + y0), &full[s]);
+              }
             }
           }
         }
-        tile_mark(p.trace, 0, unsigned((t - int(blockIdx.x)) / int(gridDim.x)));
+        tile_mark(p.trace, 0, unsigned((t - cid) / ncl));
       }
       trace_mark_here(p.trace, 5);
+    }
+  } else if (warp == 1 && CG == 2 && !leader) {
+    // ---------------------------------------------------------------- peer relay
+    // the leader's MMAs read this CTA's stage too: forward each completed
+    // stage to the leader's barrier
+    if (lane == 0) {
+      const uint32_t rfull = mapa_rank(&full[0], 0);
+      unsigned u = 0;
+      for (int t = cid; t < p.n_tiles; t += ncl)
+        for (int kb = 0; kb < n_kb; ++kb, ++u) {
+          const int s = int(u % unsigned(S));
+          mbar_wait(&full[s], (u / unsigned(S)) & 1u);
+          mbar_arrive_remote(rfull + uint32_t(s) * 8u);
+        }
     }
   } else if (warp == 1) {
     // ---------------------------------------------------------------- MMA issuer
     if (lane == 0) {
-      constexpr uint32_t idesc = umma_idesc(UM_M, UM_N);
+      constexpr uint32_t idesc = umma_idesc(UM_M * CG, UM_N);
       unsigned u = 0, ti = 0;
-      for (int t = blockIdx.x; t < p.n_tiles; t += gridDim.x, ++ti) {
+      for (int t = cid; t < p.n_tiles; t += ncl, ++ti) {
         const int as = int(ti % unsigned(AS));
         mbar_wait(&tempty[as], ((ti / unsigned(AS)) & 1u) ^ 1u);
         tc_fence_after();
@@ -321,7 +482,7 @@ __global__ void __launch_bounds__(kUmThreads, 1)
           const int s = int(u % unsigned(S));
           mbar_wait(&full[s], (u / unsigned(S)) & 1u);
           tc_fence_after();
-          const unsigned char* sa = smem + size_t(s) * kUmStageBytes;
+          const unsigned char* sa = smem + size_t(s) * SBY;
           const unsigned char* sb = sa + kStageA;
           if (SEM && kb < p.n_sem_kb) {
             const bool hi = !TRAJ && p.split_kb > 0 && kb >= p.split_kb;
@@ -329,8 +490,8 @@ __global__ void __launch_bounds__(kUmThreads, 1)
             const int kb0 = hi ? p.split_kb : 0;
 #pragma unroll
             for (int kk = 0; kk < 4; ++kk)
-              tc_mma(d, umma_desc(sa + kk * 32, 16, 1024, 2), umma_desc(sb + kk * 32, 16, 1024, 2), idesc,
-                     (kb != kb0 || kk) ? 1u : 0u);
+              tc_mma<CG>(d, umma_desc(sa + kk * 32, 16, 1024, 2), umma_desc(sb + kk * 32, 16, 1024, 2), idesc,
+                         (kb != kb0 || kk) ? 1u : 0u);
           } else {
             const int j = kb - p.n_sem_kb;
             const int l0 = j * p.lc;
@@ -339,21 +500,23 @@ __global__ void __launch_bounds__(kUmThreads, 1)
             if (p.tmode == 0) {
               // two 16-byte layers per K=16 MMA: LBO = the layer stride
               for (int l = 0; l < nl; l += 2)
-                tc_mma(d_trj, umma_desc(sa + l * UM_M * 16, UM_M * 16, 128, 0),
-                       umma_desc(sb + l * UM_N * 16, UM_N * 16, 128, 0), idesc, (first && l == 0) ? 0u : 1u);
+                tc_mma<CG>(d_trj, umma_desc(sa + l * UM_M * 16, UM_M * 16, 128, 0),
+                           umma_desc(sb + l * NB * 16, NB * 16, 128, 0), idesc, (first && l == 0) ? 0u : 1u);
             } else {
               const uint32_t layout = p.tmode == 1 ? 6u : (p.tmode == 2 ? 4u : 2u);
               const int ksteps = RB / 32;
               for (int l = 0; l < nl; ++l)
                 for (int kk = 0; kk < ksteps; ++kk)
-                  tc_mma(d_trj, umma_desc(sa + l * UM_M * RB + kk * 32, 16, 8 * RB, layout),
-                         umma_desc(sb + l * UM_N * RB + kk * 32, 16, 8 * RB, layout), idesc,
-                         (first && l == 0 && kk == 0) ? 0u : 1u);
+                  tc_mma<CG>(d_trj, umma_desc(sa + l * UM_M * RB + kk * 32, 16, 8 * RB, layout),
+                             umma_desc(sb + l * NB * RB + kk * 32, 16, 8 * RB, layout), idesc,
+                             (first && l == 0 && kk == 0) ? 0u : 1u);
             }
           }
-          tc_commit(&empty[s]);            // stage s may be refilled once these MMAs retire
+          // stage s may be refilled (in both CTAs of a pair) once these MMAs retire
+          if constexpr (CG == 2) tc_commit_pair(&empty[s]); else tc_commit(&empty[s]);
         }
-        tc_commit(&tfull[as]);             // accumulators of tile t complete
+        // accumulators of tile t complete
+        if constexpr (CG == 2) tc_commit_pair(&tfull[as]); else tc_commit(&tfull[as]);
         tile_mark(p.trace, 1, ti);
       }
       trace_mark_here(p.trace, 7);
@@ -368,11 +531,12 @@ __global__ void __launch_bounds__(kUmThreads, 1)
     const int R = p.rep, QA = 4 / R;              // query quadrants per replica
     const int sub = qd / QA;                      // replica index
     const int NC = (UM_N / 2) / 32 / R;           // 32-column chunks per tile and warp
-    const int q = (qd % QA) * 32 + lane;          // query of this thread
-    const bool live = q < p.nq;
+    const int q = (qd % QA) * 32 + lane;          // query of this thread (this CTA's TMEM lane)
+    const int qg = rank * UM_M + q;               // ... and its row in the pass
+    const bool live = q < nq_c;
     const int gi = half * R + sub;                // list (column group) index
-    const float rqs = (SEM && live) ? p.rq_s[q] : 0.f;
-    const float rqt = (TRAJ && live) ? p.rq_t[q] : 0.f;
+    const float rqs = (SEM && live) ? p.rq_s[qg] : 0.f;
+    const float rqt = (TRAJ && live) ? p.rq_t[qg] : 0.f;
     const float w = p.w, w1 = 1.f - p.w;
     const int k = p.k;
     const bool split = p.split_kb > 0;
@@ -390,7 +554,7 @@ __global__ void __launch_bounds__(kUmThreads, 1)
     int cnt = 0;
     // filter score (fast path: score >= thr_s); +inf keeps idle lanes out
     float thr_s = live ? -__int_as_float(0x7f800000) : __int_as_float(0x7f800000);
-    unsigned long long* gq = p.gthr + (live ? q : 0);
+    unsigned long long* gq = p.gthr + (live ? qg : 0);
     if (live) {                                    // a seeded scan starts at the seed bound
       g = ld_relaxed_u64(gq);
       if (g) thr_s = key_score(g);
@@ -417,8 +581,8 @@ __global__ void __launch_bounds__(kUmThreads, 1)
         rm_n[c] = (TRAJ && yok) ? __ldg(p.psq + yl) : 0.f;
       }
     };
-    fetch(blockIdx.x);
-    for (int t = blockIdx.x; t < p.n_tiles; t += gridDim.x, ++ti) {
+    fetch(cid);
+    for (int t = cid; t < p.n_tiles; t += ncl, ++ti) {
       const int as = int(ti % unsigned(AS));
       const int ybase = t * UM_N + half * HC + sub * NC * 32;   // first column of this warp
       // this warp's copy of the half tile's row scales, read back as broadcast
@@ -429,10 +593,11 @@ __global__ void __launch_bounds__(kUmThreads, 1)
         re_c[c] = re_n[c];
         rm_c[c] = rm_n[c] > 0.f ? rsqrtf(rm_n[c]) : 0.f;
       }
-      fetch(t + gridDim.x);
+      fetch(t + ncl);
       if (ti == 0 && tid == 128) trace_mark_here(p.trace, 2);
       EPI_T(5);
-      mbar_wait(&tfull[as], (ti / unsigned(AS)) & 1u);
+      if (p.epi_sleep > 0) mbar_wait_backoff(&tfull[as], (ti / unsigned(AS)) & 1u, unsigned(p.epi_sleep));
+      else mbar_wait(&tfull[as], (ti / unsigned(AS)) & 1u);
       EPI_T(0);
       // one warp per half publishes the scales, after this tile's accumulators
       // are full (so every warp has released the previous tile of this stage);
@@ -464,7 +629,7 @@ __global__ void __launch_bounds__(kUmThreads, 1)
         const unsigned vmask = !live ? 0u : (left >= 32 ? 0xffffffffu : (left <= 0 ? 0u : ((1u << left) - 1u)));
         float cached[32];
         if (!SEM && p.sem_cos) {
-          const float* cp = p.sem_cos + int64_t(p.cand_q0 + q) * p.cos_stride + yc;
+          const float* cp = p.sem_cos + int64_t(p.cand_q0 + qg) * p.cos_stride + yc;
 #pragma unroll
           for (int j = 0; j < 32; j += 4) {
             if (vec4 && j + 4 <= nvalid_rows(yc, p.n_rows, live)) {
@@ -511,7 +676,7 @@ __global__ void __launch_bounds__(kUmThreads, 1)
         m &= vmask;
         EPI_T(3);
         if (SEM && !TRAJ && p.out_cos && live) {
-          float* op = p.out_cos + int64_t(p.cand_q0 + q) * p.cos_stride + yc;
+          float* op = p.out_cos + int64_t(p.cand_q0 + qg) * p.cos_stride + yc;
           const int nv = nvalid_rows(yc, p.n_rows, live);
 #pragma unroll
           for (int j = 0; j < 32; j += 4) {
@@ -564,7 +729,10 @@ __global__ void __launch_bounds__(kUmThreads, 1)
       }
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(&tempty[as]);
+      if (lane == 0) {                            // the leader's MMA waits for both CTAs' epilogues
+        if (CG == 2 && !leader) mbar_arrive_remote(mapa_rank(&tempty[as], 0));
+        else mbar_arrive(&tempty[as]);
+      }
       if (ti == 0 && tid == 128) trace_mark_here(p.trace, 1);
       if (tid == 128) tile_mark(p.trace, 3, ti);
     }
@@ -581,7 +749,7 @@ __global__ void __launch_bounds__(kUmThreads, 1)
     if (live && cnt < k) heapify(ml_s, uint32_t(LQ) * 8, k);   // empty slots are key 0
     asm volatile("bar.sync 3, %0;" ::"r"(kUmEpiWarps * 32) : "memory");
     const int te = tid - 128;
-    if (te < p.nq) {
+    if (te < nq_c) {
       const uint32_t l0 = smem_u32(lists + te);
       uint64_t root = lists[te];
       for (int g = 1; g < 2 * R; ++g)
@@ -589,16 +757,21 @@ __global__ void __launch_bounds__(kUmThreads, 1)
           const uint64_t key = lists[(size_t(g) * k + i) * LQ + te];
           if (key > root) root = heap_replace_root(l0, uint32_t(LQ) * 8, k, key);
         }
-      uint64_t* dst = p.cand + (int64_t(p.cand_q0 + te) * p.grid + blockIdx.x) * k;
+      uint64_t* dst = p.cand + (int64_t(p.cand_q0 + rank * UM_M + te) * p.grid + cid) * k;
       for (int i = 0; i < k; ++i) dst[i] = lists[size_t(i) * LQ + te];
     }
   }
   pdl_trigger();
   tc_fence_before();
-  __syncthreads();
+  __syncwarp();
+  if constexpr (CG == 2) cluster_sync_all();      // no CTA leaves while its peer may still signal it
+  else __syncthreads();
   if (warp == 2) {
     tc_fence_after();
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem_base) : "memory");
+    if constexpr (CG == 1)
+      asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem_base) : "memory");
+    else
+      asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, 512;" ::"r"(tmem_base) : "memory");
   }
   trace_mark(p.trace, 6);
 }
@@ -649,7 +822,8 @@ __global__ void __launch_bounds__(256) umma_prep_kernel(const float* __restrict_
       const float v = (live && l < ell && j < E)
                           ? __bfloat162float(__float2bfloat16_rn(q_prefix[int64_t(x) * q_stride + l * E + j]))
                           : 0.f;
-      qt[(int64_t(l) * UM_M + q) * Ep + j] = __float2bfloat16_rn(v);
+      // [CG][ell_pad][128][Ep]: each CTA of a pair reads its own contiguous block
+      qt[((int64_t(q / UM_M) * ell_pad + l) * UM_M + q % UM_M) * Ep + j] = __float2bfloat16_rn(v);
       b += double(v) * double(v);
     }
   }
@@ -741,40 +915,47 @@ static bool make_map(CUtensorMap* m, const void* base, uint64_t cols, uint64_t r
 
 static int tmode_of(int rb) { return rb == 16 ? 0 : rb == 32 ? 1 : rb == 64 ? 2 : rb == 128 ? 3 : -1; }
 
-// smem: 1 KB alignment + S stages of 48 KB + 2R lists of k keys per query,
-// within 216 KB (+ ~10 KB static <= 227 KB)
+// CTA pairs (cta_group::2, M = 256) for passes of more than 128 queries
+static int cg_of(const UmmaPlanIn& in) { return in.cg > 0 ? in.cg : (in.nq > UM_M ? 2 : 1); }
+// smem: 1 KB alignment + S stages (48 KB; 32 KB per CTA of a pair) + 2R lists
+// of k keys per query of the CTA, within 216 KB (+ ~10 KB static <= 227 KB)
 static size_t lists_bytes(const UmmaPlanIn& in, int R) {
-  return size_t(2 * R) * in.k * ((in.nq + 31) / 32 * 32) * 8;
+  const int nq = in.nq < UM_M ? in.nq : UM_M;
+  return size_t(2 * R) * in.k * ((nq + 31) / 32 * 32) * 8;
 }
 static int stages_for(const UmmaPlanIn& in, int R) {
   const size_t l = lists_bytes(in, R);
   if (l + 1024 > 216 * 1024) return 0;
-  const int S = int((216 * 1024 - 1024 - l) / kUmStageBytes);
-  return S > kUmMaxStages ? kUmMaxStages : S;
+  const int S = int((216 * 1024 - 1024 - l) / size_t(um_stage_bytes(cg_of(in))));
+  static const int env = getenv("FMOE_UMMA_STAGES") ? atoi(getenv("FMOE_UMMA_STAGES")) : 0;
+  const int cap = env > 0 ? env : (cg_of(in) == 2 ? 6 : 4);
+  return S > cap ? cap : S;
 }
 // Query replication: nq <= 32 uses one TMEM lane quadrant, nq <= 64 two; the
 // other quadrants' epilogue warps (the other SM sub-partitions) would idle, so
 // the query rows are repeated R = 4 / quadrants times and the replicas split
 // the columns.  Backed off while the larger lists would cost pipeline stages.
 int umma_rep(const UmmaPlanIn& in) {
-  int R = in.nq <= 32 ? 4 : (in.nq <= 64 ? 2 : 1);
+  int R = in.nq <= 32 ? 4 : (in.nq <= 64 ? 2 : 1);   // (1 for CTA pairs: nq > 128)
   const int s1 = stages_for(in, 1), want = s1 < 3 ? s1 : 3;
   while (R > 1 && stages_for(in, R) < want) R /= 2;
   return R;
 }
 
 bool umma_supported(const UmmaPlanIn& in) {
-  if (!in.bf16 || in.nq < 1 || in.nq > UM_M || in.k < 1 || in.k > kMaxK) return false;
+  if (!in.bf16 || in.nq < 1 || in.nq > 2 * UM_M || in.k < 1 || in.k > kMaxK) return false;
   if (stages_for(in, 1) < 2) return false;   // keep >= 2 pipeline stages
   if (in.w_sem != 1.f && tmode_of(in.Ep * 2) < 0) return false;
   if (!encoder()) return false;
   return true;
 }
 
-// scratch layout: qs [128][Dp] bf16 | qt [ell+2][128][Ep] bf16 | rq_s, rq_t [128] f32
-static size_t qt_offset(const UmmaPlanIn& in) { return size_t(UM_M) * in.Dp * 2; }
-static size_t rq_offset(const UmmaPlanIn& in) { return qt_offset(in) + size_t(in.ell + 2) * UM_M * in.Ep * 2; }
-size_t umma_scratch_bytes(const UmmaPlanIn& in) { return rq_offset(in) + 2 * UM_M * 4 + 256; }
+// scratch layout (MQ = 256 rows, enough for either CTA mode):
+//   qs [MQ][Dp] bf16 | qt [CG][ell+2][128][Ep] bf16 | rq_s, rq_t [MQ] f32
+constexpr int kMQ = 2 * UM_M;
+static size_t qt_offset(const UmmaPlanIn& in) { return size_t(kMQ) * in.Dp * 2; }
+static size_t rq_offset(const UmmaPlanIn& in) { return qt_offset(in) + size_t(in.ell + 2) * kMQ * in.Ep * 2; }
+size_t umma_scratch_bytes(const UmmaPlanIn& in) { return rq_offset(in) + 2 * kMQ * 4 + 256; }
 
 int umma_grid(const UmmaPlanIn& in) {
   static int sms = 0;
@@ -783,20 +964,26 @@ int umma_grid(const UmmaPlanIn& in) {
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   }
+  // one CTA (or CTA pair) per SM (pair of SMs), persistent over the tiles
+  const int cg = cg_of(in);
   const int64_t tiles = (in.n_rows + UM_N - 1) / UM_N;
-  return int(tiles < sms ? (tiles < 1 ? 1 : tiles) : sms);
+  const int64_t units = sms / cg;
+  return cg * int(tiles < units ? (tiles < 1 ? 1 : tiles) : units);
 }
+int umma_cg(const UmmaPlanIn& in) { return cg_of(in); }
 
 cudaError_t launch_umma(const UmmaLaunch& L, cudaStream_t s) {
   const UmmaPlanIn& in = L.in;
   const bool sem = in.w_sem != 0.f && !L.sem_cos, traj = in.w_sem != 1.f;
   const int ell_pad = traj ? in.ell + ((in.Ep * 2 == 16) ? (in.ell & 1) : 0) : 0;
-  const int R = in.rep < 1 ? 1 : in.rep;
+  const int CG = cg_of(in);
+  const int R = CG == 2 || in.rep < 1 ? 1 : in.rep;
+  const int MQ = UM_M * CG;
   char* scr = static_cast<char*>(L.scratch);
   __nv_bfloat16* qs = reinterpret_cast<__nv_bfloat16*>(scr);
   __nv_bfloat16* qt = reinterpret_cast<__nv_bfloat16*>(scr + qt_offset(in));
   float* rq_s = reinterpret_cast<float*>(scr + rq_offset(in));
-  float* rq_t = rq_s + UM_M;
+  float* rq_t = rq_s + kMQ;
   // 1. query preparation (+ the seed bound)
   SeedArgs sd;
   if (L.seed_ids && traj && !sem) {
@@ -811,15 +998,15 @@ cudaError_t launch_umma(const UmmaLaunch& L, cudaStream_t s) {
     sd.psq = in.psq + int64_t(in.ell - 1) * in.cap;
   }
   count_launch();
-  cudaError_t e = launch_pdl(umma_prep_kernel, dim3(UM_M), dim3(256), 0, s, L.q_emb, L.q_prefix, L.q_stride, in.nq,
+  cudaError_t e = launch_pdl(umma_prep_kernel, dim3(MQ), dim3(256), 0, s, L.q_emb, L.q_prefix, L.q_stride, in.nq,
                              in.D, in.Dp, in.E, in.Ep, in.ell, ell_pad, qs, qt, rq_s, rq_t, L.valid, sem ? 1 : 0,
-                             traj ? 1 : 0, UM_M / R, L.gthr, sd, L.gate);
+                             traj ? 1 : 0, MQ / R, L.gthr, sd, L.gate);
   if (e != cudaSuccess) return e;
   // 2. tensor maps
   CUtensorMap tq_s{}, te_s{}, tq_t{}, tm_t{};
   if (sem) {
-    if (!make_map(&tq_s, qs, in.Dp, UM_M, 64, UM_M, CU_TENSOR_MAP_SWIZZLE_128B) ||
-        !make_map(&te_s, in.emb, in.Dp, in.cap, 64, UM_N, CU_TENSOR_MAP_SWIZZLE_128B))
+    if (!make_map(&tq_s, qs, in.Dp, MQ, 64, UM_M, CU_TENSOR_MAP_SWIZZLE_128B) ||
+        !make_map(&te_s, in.emb, in.Dp, in.cap, 64, um_rows(CG), CU_TENSOR_MAP_SWIZZLE_128B))
       return cudaErrorInvalidValue;
   }
   int tmode = 0, lc = 0, n_traj_kb = 0;
@@ -830,8 +1017,8 @@ cudaError_t launch_umma(const UmmaLaunch& L, cudaStream_t s) {
                                   : tmode == 1 ? CU_TENSOR_MAP_SWIZZLE_32B
                                   : tmode == 2 ? CU_TENSOR_MAP_SWIZZLE_64B
                                                : CU_TENSOR_MAP_SWIZZLE_128B;
-    if (!make_map(&tq_t, qt, in.Ep, uint64_t(ell_pad) * UM_M, in.Ep, UM_M, sw) ||
-        !make_map(&tm_t, in.maps, in.Ep, uint64_t(in.L) * in.cap, in.Ep, UM_N, sw))
+    if (!make_map(&tq_t, qt, in.Ep, uint64_t(CG) * ell_pad * UM_M, in.Ep, UM_M, sw) ||
+        !make_map(&tm_t, in.maps, in.Ep, uint64_t(in.L) * in.cap, in.Ep, um_rows(CG), sw))
       return cudaErrorInvalidValue;
     lc = kStageA / (UM_M * rb);
     n_traj_kb = (ell_pad + lc - 1) / lc;
@@ -859,7 +1046,16 @@ cudaError_t launch_umma(const UmmaLaunch& L, cudaStream_t s) {
   // (measured: D = 2048 stays within 7e-6; D = 4096 drifted 1.4e-5 unsplit)
   p.split_kb = (sem && !traj && p.n_sem_kb >= 48) ? p.n_sem_kb / 2 : 0;
   p.acc_stages = (sem && traj) || p.split_kb > 0 ? 1 : 2;
+  {
+    static const int pf_env = getenv("FMOE_L2PF") ? atoi(getenv("FMOE_L2PF")) : -1;
+    p.l2pf = pf_env >= 0 ? pf_env : 0;   // measured: no gain at either CTA mode (kept as a knob)
+    static const int es_env = getenv("FMOE_EPI_SLEEP") ? atoi(getenv("FMOE_EPI_SLEEP")) : -1;
+    p.epi_sleep = es_env >= 0 ? es_env : 0;   // measured neutral (64..1000 ns); kept as a knob
+  }
   p.cap = in.cap;
+  p.L = in.L;
+  p.maps = static_cast<const unsigned char*>(in.maps);
+  p.qt = reinterpret_cast<const unsigned char*>(qt);
   p.id_offset = in.id_offset;
   p.rq_s = rq_s;
   p.rq_t = rq_t;
@@ -867,17 +1063,21 @@ cudaError_t launch_umma(const UmmaLaunch& L, cudaStream_t s) {
   p.psq = traj ? in.psq + int64_t(in.ell - 1) * in.cap : in.psq;
   p.cand = L.cand;
   p.cand_q0 = L.cand_q0;
-  p.grid = L.grid;
+  p.grid = L.grid / CG;
   p.trace = L.trace;
   p.out_cos = L.out_cos;
   p.sem_cos = L.sem_cos;
   p.cos_stride = L.cos_stride;
   p.gthr = L.gthr;
   p.gate = L.gate;
-  const size_t smem = 1024 + size_t(p.stages) * kUmStageBytes + lists;
+  const size_t smem = 1024 + size_t(p.stages) * um_stage_bytes(CG) + lists;
   using Fn = void (*)(const CUtensorMap, const CUtensorMap, const CUtensorMap, const CUtensorMap, const UmmaParams);
-  const Fn fn = sem && traj ? scan_umma_kernel<true, true> : sem ? scan_umma_kernel<true, false>
-                                                               : scan_umma_kernel<false, true>;
+  const Fn fn = CG == 2 ? (sem && traj ? scan_umma_kernel<true, true, 2>
+                           : sem       ? scan_umma_kernel<true, false, 2>
+                                       : scan_umma_kernel<false, true, 2>)
+                        : (sem && traj ? scan_umma_kernel<true, true, 1>
+                           : sem       ? scan_umma_kernel<true, false, 1>
+                                       : scan_umma_kernel<false, true, 1>);
   {
     static std::mutex mu;
     static std::map<const void*, size_t> set;
@@ -891,7 +1091,23 @@ cudaError_t launch_umma(const UmmaLaunch& L, cudaStream_t s) {
     }
   }
   count_launch();
-  return launch_pdl(fn, dim3(L.grid), dim3(kUmThreads), smem, s, tq_s, te_s, tq_t, tm_t, p);
+  if (CG == 1) return launch_pdl(fn, dim3(L.grid), dim3(kUmThreads), smem, s, tq_s, te_s, tq_t, tm_t, p);
+  // CTA pairs: clusters of 2 (one TPC), with programmatic dependent launch
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(L.grid);
+  cfg.blockDim = dim3(kUmThreads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[2];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  at[1].id = cudaLaunchAttributeClusterDimension;
+  at[1].val.clusterDim.x = 2;
+  at[1].val.clusterDim.y = 1;
+  at[1].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 2;
+  return cudaLaunchKernelEx(&cfg, fn, tq_s, te_s, tq_t, tm_t, p);
 }
 
 }  // namespace fmoe

@@ -230,14 +230,15 @@ bool umma_plan(const fmoe_store* st, int64_t B, int k, int ell, float w, int64_t
   if (!st->bf16 || B < umma_min_batch()) return false;
   UmmaPlanIn& u = *in;
   u = UmmaPlanIn{};
-  u.bf16 = 1; u.nq = int(B < 128 ? B : 128); u.k = k; u.D = st->cfg.D; u.Dp = st->Dp; u.E = st->cfg.E;
+  u.bf16 = 1; u.nq = int(B < 256 ? B : 256); u.k = k; u.D = st->cfg.D; u.Dp = st->Dp; u.E = st->cfg.E;
   u.Ep = st->Ep; u.L = st->cfg.L; u.ell = ell; u.w_sem = w; u.n_rows = n_rows; u.cap = st->cfg.capacity;
   u.id_offset = id_offset; u.emb = st->emb; u.maps = st->maps; u.r_e = st->r_e; u.psq = st->psq;
   return umma_supported(u);
 }
 
-// Batched call on the tensor cores: passes of <= 128 queries, per-CTA lists,
-// then one merge kernel over all passes.
+// Batched call on the tensor cores: passes of <= 128 queries (CTAs) or <= 256
+// (CTA pairs, cta_group::2), per-CTA(-pair) lists, then one merge kernel over
+// all passes.
 struct CosArgs {
   float* out = nullptr;          // semantic scans: write the cosines
   const float* in = nullptr;     // RDY / blend scans: blend these instead of re-reading embeddings
@@ -248,9 +249,11 @@ fmoe_status run_search_umma(const fmoe_store* st, UmmaPlanIn in, int64_t B, cons
                             int64_t q_stride, cudaStream_t s, float* ds, int64_t* di, uint64_t* dkeys,
                             bool check_queries, const CosArgs& cos, const int64_t* seed_ids, int seed_stride,
                             int seed_n, int k_out, const int* gate) {
+  in.cg = umma_cg(in);                                // from the first (largest) pass
   const int grid = umma_grid(in);
-  in.rep = umma_rep(in);                              // from the first (largest) pass
-  const int n_lists = grid;                           // one list per (query, CTA)
+  in.rep = umma_rep(in);
+  const int pass = in.cg * 128;
+  const int n_lists = grid / in.cg;                   // one list per (query, CTA or CTA pair)
   const size_t cand_b = align_up(size_t(B) * n_lists * in.k * 8);
   const size_t valid_b = align_up(size_t(B) * 4);
   const size_t prep_b = align_up(umma_scratch_bytes(in));
@@ -263,10 +266,10 @@ fmoe_status run_search_umma(const fmoe_store* st, UmmaPlanIn in, int64_t B, cons
   uint64_t* cand = reinterpret_cast<uint64_t*>(buf);
   float* valid = reinterpret_cast<float*>(buf + cand_b);
   unsigned long long* gthr = reinterpret_cast<unsigned long long*>(buf + cand_b + valid_b + prep_b);
-  for (int64_t q0 = 0; q0 < B; q0 += 128) {
+  for (int64_t q0 = 0; q0 < B; q0 += pass) {
     UmmaLaunch L{};
     L.in = in;
-    L.in.nq = int(B - q0 < 128 ? B - q0 : 128);
+    L.in.nq = int(B - q0 < pass ? B - q0 : pass);
     L.q_emb = dq ? dq + q0 * in.D : nullptr;
     L.q_prefix = dp ? dp + q0 * q_stride : nullptr;
     L.q_stride = q_stride;

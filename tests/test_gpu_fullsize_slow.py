@@ -48,6 +48,13 @@ def test_c5_sixteen_million_batch_256(lib):
         w = float(np.float32(3 / sh.L))
         check_returned_scores(sh, s[:32], i[:32], qe[:32], pre[:32], ell, w)
         check_block_not_better(sh, N, s[:32, 0], qe[:32], pre[:32], ell, w, block=500)
+        # queries 128..255 live in the second CTA of each pair (cta_group::2)
+        check_returned_scores(sh, s[224:], i[224:], qe[224:], pre[224:], ell, w)
+        check_block_not_better(sh, N, s[224:, 0], qe[224:], pre[224:], ell, w, block=500)
+        # trajectory only (16-byte map rows: bulk-copy operands)
+        s, i = st.search_trajectory(pre, ell, 8)
+        check_returned_scores(sh, s[:16], i[:16], qe[:16], pre[:16], ell, 0.0)
+        check_returned_scores(sh, s[240:], i[240:], qe[240:], pre[240:], ell, 0.0)
         assert np.all(i[:, 0].cpu().numpy()[pl >= 0] == pl[pl >= 0])
     finally:
         st.close()

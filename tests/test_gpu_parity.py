@@ -284,7 +284,8 @@ def test_topk_merge_api(lib):
 
 
 # ---------------------------------------------------------------- batched (tcgen05 path, B >= 5, bf16)
-@pytest.mark.parametrize("B,k", [(16, 1), (64, 8), (130, 64)])
+# 130, 256: one pass on CTA pairs (cta_group::2, M = 256); 300: a 256-query pass + a ragged 44-query pass
+@pytest.mark.parametrize("B,k", [(16, 1), (64, 8), (130, 64), (256, 8), (300, 3)])
 @pytest.mark.parametrize("mode", ["sem", "traj3", "trajL", "blend"])
 def test_batched_tcgen05(setup, B, k, mode):
     if setup["dtype"] != "bf16":
