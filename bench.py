@@ -173,7 +173,9 @@ class Step:
     def __init__(self, fm, st, cfg, traj_mode="stateless", use_cos=True):
         self.fm, self.st, self.cfg = fm, st, cfg
         self.sh = cfg["shape"]
-        self.sess = fm.fmoe_traj_session_create(st._h, cfg["B"]) if traj_mode == "session" else None
+        # (blend workloads search at fixed prefixes: no trajectory sweep, no session)
+        self.sess = (fm.fmoe_traj_session_create(st._h, cfg["B"])
+                     if traj_mode == "session" and cfg.get("kind") != "blend" else None)
         # semantic cosines kept on the device for the RDY insert (fmoe_store_insert_cos):
         # the iteration's new context carries the embedding its semantic search used
         n = len(st)

@@ -206,6 +206,7 @@ struct UmmaParams {
   int lc;               // layers per trajectory stage
   int stages;
   int acc_stages;       // TMEM accumulator buffers (1 or 2)
+  int fake_loads;       // debug knob (FMOE_FAKE_LOADS=1): skip the loads, results are garbage
   int epi_sleep;        // epilogue accumulator wait: ns between polls (0 = try_wait suspend loop)
   int l2pf;             // L2 prefetch distance of the store operand, in k-blocks (0 = off)
   int split_kb;         // semantic-only: k-blocks >= split_kb accumulate into a second TMEM
@@ -415,6 +416,10 @@ __global__ void __launch_bounds__(kUmThreads, 1)
           mbar_wait(&empty[s], ((u / unsigned(S)) & 1u) ^ 1u);
           unsigned char* sa = smem + size_t(s) * SBY;
           unsigned char* sb = sa + kStageA;
+          if (p.fake_loads) {                    // debug: MMAs on stale smem (feed excluded)
+            mbar_arrive(&full[s]);
+            continue;
+          }
           if (SEM && kb < p.n_sem_kb) {
             mbar_arrive_expect_tx(&full[s], unsigned(SBY));
             tma_load_2d(sa, &tm_qs, kb * 64, rank * UM_M, &full[s]);
@@ -1050,7 +1055,9 @@ cudaError_t launch_umma(const UmmaLaunch& L, cudaStream_t s) {
     static const int pf_env = getenv("FMOE_L2PF") ? atoi(getenv("FMOE_L2PF")) : -1;
     p.l2pf = pf_env >= 0 ? pf_env : 0;   // measured: no gain at either CTA mode (kept as a knob)
     static const int es_env = getenv("FMOE_EPI_SLEEP") ? atoi(getenv("FMOE_EPI_SLEEP")) : -1;
-    p.epi_sleep = es_env >= 0 ? es_env : 0;   // measured neutral (64..1000 ns); kept as a knob
+    p.epi_sleep = es_env >= 0 ? es_env : 0;
+    static const int fk_env = getenv("FMOE_FAKE_LOADS") ? atoi(getenv("FMOE_FAKE_LOADS")) : 0;
+    p.fake_loads = fk_env;   // measured neutral (64..1000 ns); kept as a knob
   }
   p.cap = in.cap;
   p.L = in.L;
