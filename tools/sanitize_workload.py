@@ -21,8 +21,9 @@ def main():
         e, m, _ = S.store_rows(sh, 3, 0, N + 20, device="cuda")
         st = fm.ExpertMapStore(sh.L, sh.E, sh.K, sh.D, 3, N, dt)
         st.insert(e[:N].contiguous(), m[:N].contiguous())
-        qe, qm, _ = S.queries(sh, 3, N, 20, device="cuda")
-        for B, k in ((1, 1), (3, 8), (6, 40), (20, 8)):
+        qe, qm, _ = S.queries(sh, 3, N, 260, device="cuda")
+        # (150, 8), (260, 3): CTA-pair passes (cta_group::2), the second one ragged
+        for B, k in ((1, 1), (3, 8), (6, 40), (20, 8), (150, 8), (260, 3)):
             st.search_semantic(qe[:B].contiguous(), k)
             st.search_trajectory(qm[:B].contiguous(), 3, k)
             st.search_blend(qe[:B].contiguous(), qm[:B].contiguous(), sh.L, -1.0, k)
