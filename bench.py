@@ -241,11 +241,16 @@ class Step:
             fm.fmoe_traj_session_reset(self.sess)        # the store changed at the last insert
         for ell in range(1, L):
             pre, lay = q_maps[ell - 1]
+            tgt = ell - 1 + d
+            if self.sess is not None and tgt < L:
+                # session step + selection of target layer ell+d in one call
+                rec(f"traj{ell}", lambda: fm.fmoe_traj_session_step_select(self.sess, lay, k, out_s, out_i,
+                                                                          cfg["delta"], tgt, tgt + 1, m1, c1))
+                continue
             if self.sess is not None:
                 rec(f"traj{ell}", lambda: fm.fmoe_traj_session_step(self.sess, lay, k, out_s, out_i))
             else:
                 rec(f"traj{ell}", lambda: fm.fmoe_search_trajectory(h, pre, ell, k, out_s, out_i))
-            tgt = ell - 1 + d
             if tgt < L:
                 top_i = out_i[:, 0].contiguous()
                 top_s = out_s[:, 0].contiguous()
@@ -289,11 +294,15 @@ class HostStep(Step):
             fm.fmoe_traj_session_reset(self.sess)
         for ell in range(1, L):
             pre, lay = q_maps[ell - 1]
+            tgt = ell - 1 + d
+            if self.sess is not None and tgt < L:
+                fm.fmoe_traj_session_step_select(self.sess, lay, k, out_s, out_i, cfg["delta"], tgt, tgt + 1,
+                                                 self.m1, self.c1)
+                continue
             if self.sess is not None:
                 fm.fmoe_traj_session_step(self.sess, lay, k, out_s, out_i)
             else:
                 fm.fmoe_search_trajectory(h, pre, ell, k, out_s, out_i)
-            tgt = ell - 1 + d
             if tgt < L:
                 top_s.copy_(out_s[:, 0]); top_i.copy_(out_i[:, 0])
                 fm.fmoe_select_experts(h, top_i, top_s, cfg["delta"], tgt, tgt + 1, self.m1, self.c1)
@@ -313,7 +322,8 @@ class HostStep(Step):
         traj_in = sum(B * (1 if traj_mode == "session" else ell) * sh.E * 4 for ell in range(1, L))
         h2d = B * sh.D * 4 + traj_in + B * (sh.D + L * sh.E) * 4
         n_sel = 1 + sum(1 for ell in range(1, L) if ell - 1 + d < L)
-        h2d += n_sel * B * (8 + 4)                                  # map ids + scores into select
+        # map ids + scores into select (a session step selects on the device: no copy)
+        h2d += (1 if traj_mode == "session" else n_sel) * B * (8 + 4)
         d2h = (L) * B * k * (4 + 8)                                 # search outputs
         d2h += B * d * (8 + 4) + (n_sel - 1) * B * (8 + 4)          # masks + counts
         return h2d, d2h

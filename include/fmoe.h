@@ -190,6 +190,18 @@ fmoe_status fmoe_traj_session_create(const fmoe_store* store, int64_t B, fmoe_tr
 /* q_layer [B][E] fp32: layer t of every query.  Outputs as fmoe_search_trajectory. */
 fmoe_status fmoe_traj_session_step(fmoe_traj_session* session, const float* q_layer, int32_t k,
                                    float* out_score, int64_t* out_id, void* stream);
+/* A step followed by the selection of fmoe_select_experts on each
+ * query's top-1 of this step (id out_id[x][0], score out_score[x][0]) for the
+ * layers [layer_begin, layer_end): out_mask/out_count [B][layer_end -
+ * layer_begin] exactly as fmoe_select_experts would write them.  Incremental
+ * sessions run the selection in the step kernel's last block (no extra
+ * launch, no dependent round trip); batched sessions launch the select kernel
+ * after the scan.  All four outputs are required; delta, layer range and the
+ * error cases as fmoe_select_experts; otherwise as fmoe_traj_session_step. */
+fmoe_status fmoe_traj_session_step_select(fmoe_traj_session* session, const float* q_layer, int32_t k,
+                                          float* out_score, int64_t* out_id, float delta, int32_t layer_begin,
+                                          int32_t layer_end, uint64_t* out_mask, int32_t* out_count,
+                                          void* stream);
 /* Start a new prefix (next step consumes layer 0); re-validates against the store. */
 fmoe_status fmoe_traj_session_reset(fmoe_traj_session* session);
 void fmoe_traj_session_destroy(fmoe_traj_session* session);

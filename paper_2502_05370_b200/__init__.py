@@ -60,6 +60,7 @@ def _load():
         "fmoe_select_experts": (I32, [P, I64, P, P, F, I32, I32, P, P, P]),
         "fmoe_traj_session_create": (I32, [P, I64, ctypes.POINTER(P)]),
         "fmoe_traj_session_step": (I32, [P, P, I32, P, P, P]),
+        "fmoe_traj_session_step_select": (I32, [P, P, I32, P, P, F, I32, I32, P, P, P]),
         "fmoe_traj_session_reset": (I32, [P]),
         "fmoe_traj_session_destroy": (None, [P]),
         "fmoe_topk_merge": (I32, [I64, I32, I32, P, P, I32, P, P, ctypes.c_int, P]),
@@ -81,6 +82,7 @@ ABI_SYMBOLS = ("fmoe_store_create", "fmoe_store_destroy", "fmoe_store_size", "fm
                "fmoe_store_insert", "fmoe_store_insert_cos", "fmoe_search_semantic_cos", "fmoe_store_read",
                "fmoe_store_write", "fmoe_resolve_victims", "fmoe_search_semantic", "fmoe_search_trajectory",
                "fmoe_search_blend", "fmoe_select_experts", "fmoe_traj_session_create", "fmoe_traj_session_step",
+               "fmoe_traj_session_step_select",
                "fmoe_traj_session_reset", "fmoe_traj_session_destroy", "fmoe_topk_merge",
                "fmoe_prefetch_plan", "fmoe_eviction_order", "fmoe_status_string",
                "fmoe_last_error", "fmoe_kernel_launch_count")
@@ -200,6 +202,13 @@ def fmoe_traj_session_step(s, q_layer, k, out_score, out_id, stream=None):
     _check(_lib.fmoe_traj_session_step(s, _ptr(_f32(q_layer)), k, _ptr(out_score), _ptr(out_id), _stream(stream)))
 
 
+def fmoe_traj_session_step_select(s, q_layer, k, out_score, out_id, delta, layer_begin, layer_end, out_mask,
+                                  out_count, stream=None):
+    _check(_lib.fmoe_traj_session_step_select(s, _ptr(_f32(q_layer)), k, _ptr(out_score), _ptr(out_id), delta,
+                                              layer_begin, layer_end, _ptr(out_mask), _ptr(out_count),
+                                              _stream(stream)))
+
+
 def fmoe_traj_session_reset(s):
     _check(_lib.fmoe_traj_session_reset(s))
 
@@ -298,6 +307,18 @@ class TrajectorySession:
         i = torch.empty(self.B, k, dtype=torch.int64, device=self.store.device)
         fmoe_traj_session_step(self._s, q_layer.contiguous(), k, s, i, stream)
         return s, i
+
+    def step_select(self, q_layer, k, delta, layer_begin, layer_end, stream=None):
+        """step() followed by select_experts() on each query's top-1, in one call."""
+        dev = self.store.device
+        s = torch.empty(self.B, k, dtype=torch.float32, device=dev)
+        i = torch.empty(self.B, k, dtype=torch.int64, device=dev)
+        T = layer_end - layer_begin
+        mask = torch.empty(self.B, T, dtype=torch.int64, device=dev)   # uint64 bit pattern
+        cnt = torch.empty(self.B, T, dtype=torch.int32, device=dev)
+        fmoe_traj_session_step_select(self._s, q_layer.contiguous(), k, s, i, delta, layer_begin, layer_end, mask,
+                                      cnt, stream)
+        return s, i, mask, cnt
 
     def reset(self):
         fmoe_traj_session_reset(self._s)

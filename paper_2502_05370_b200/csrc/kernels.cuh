@@ -94,6 +94,12 @@ struct SessionArgs {
   float* acc;             // [B][cap]
   const double* qn_prev;  // [B]
   double* qn_next;        // [B]
+  // optional fused Eq. 4-6 selection on each query's top-1 (sel_T = 0: none),
+  // run by the step's last block: layers [sel_lb, sel_lb + sel_T)
+  float sel_delta;        // < 0: dynamic Clip(1 - score, 0, 1)
+  int sel_K, sel_lb, sel_T;
+  uint64_t* sel_mask;     // [B][sel_T]
+  int32_t* sel_count;     // [B][sel_T]
 };
 cudaError_t launch_traj_session(const ScanArgs& a, const SessionArgs& s, cudaStream_t stream);
 int traj_session_grid(const ScanArgs& a);
@@ -135,7 +141,8 @@ cudaError_t launch_merge_lists(int B, int n_lists, int k_in, const float* scores
 // Eq. 4-6 selection, one warp per (query, layer).
 cudaError_t launch_select(const StoreView& st, int B, const int64_t* map_id, const float* score,
                           float delta, int K, int layer_begin, int layer_end, int64_t id_offset,
-                          int64_t n_rows, uint64_t* out_mask, int32_t* out_count, cudaStream_t s);
+                          int64_t n_rows, uint64_t* out_mask, int32_t* out_count, cudaStream_t s,
+                          int stride = 1);   // map_id[q * stride], score[q * stride]
 
 // Expert-cache priorities: prefetch plan per query, eviction order.
 cudaError_t launch_prefetch_plan(const StoreView& st, int B, const int64_t* map_id, const float* score, float delta,

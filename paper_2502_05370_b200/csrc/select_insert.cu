@@ -3,6 +3,7 @@
 #include <atomic>
 #include "common.cuh"
 #include "kernels.cuh"
+#include "select.cuh"
 
 namespace fmoe {
 
@@ -122,77 +123,13 @@ cudaError_t launch_merge_lists(int B, int n_lists, int k_in, const float* scores
   return cudaGetLastError();
 }
 
-// ------------------------------------------------------------------ K5 select (Eq. 4-6)
-// One warp per (query, target layer).  The E <= 64 probabilities of the
-// matched row are ranked by (p desc, index asc) in registers (each lane owns
-// entries lane and lane+32), scattered into shared memory in rank order, and
-// one lane accumulates them in float64 in that order -- the exact order and
-// precision of the oracle, so sets are bit-identical given the same score.
-constexpr int kSelWarps = 8;
-
-template <class Tag>
-__device__ __forceinline__ float load_p(const StoreView& st, int t, int64_t row, int j) {
-  using T = typename StoreT<Tag>::T;
-  const T* m = static_cast<const T*>(st.maps);
-  if constexpr (sizeof(T) == 2)
-    return __bfloat162float(m[(int64_t(t) * st.cap + row) * st.Ep + j]);
-  else
-    return m[(int64_t(t) * st.cap + row) * st.Ep + j];
-}
-
-// delta = Clip(1 - score, 0, 1) in float64 (score clamped to [-1, 1], NaN -> 1), or the fixed delta
-__device__ __forceinline__ double selection_delta(float delta, float s) {
-  if (delta >= 0.f) return double(delta);
-  if (s != s) return 1.0;
-  double sd = double(s);
-  sd = sd < -1.0 ? -1.0 : (sd > 1.0 ? 1.0 : sd);
-  const double v = 1.0 - sd;
-  return v < 0.0 ? 0.0 : (v > 1.0 ? 1.0 : v);
-}
-
-// Eq. 4-6 for row `loc`, layer t, by one warp: rank the E <= 64 probabilities
-// by (p desc, index asc) in registers, scatter them in rank order to the warp's
-// scratch sp/si, and accumulate in float64 in that order on lane 0 (the order
-// and precision of the oracle).  Returns (on every lane) the mask and count;
-// sp/si[0..count) then hold the picked experts in selection order.
-template <class Tag>
-__device__ __forceinline__ void warp_select(const StoreView& st, int t, int64_t loc, double dl, int K, float* sp,
-                                            int* si, uint64_t* mask_out, int* count_out) {
-  const int lane = threadIdx.x & 31;
-  const int E = st.E;
-  const float NEG = -__int_as_float(0x7f800000);
-  const float p0 = lane < E ? load_p<Tag>(st, t, loc, lane) : NEG;
-  const float p1 = lane + 32 < E ? load_p<Tag>(st, t, loc, lane + 32) : NEG;
-  int r0 = 0, r1 = 0;
-  for (int j = 0; j < E; ++j) {
-    const float a = __shfl_sync(0xffffffffu, p0, j & 31);
-    const float b = __shfl_sync(0xffffffffu, p1, j & 31);
-    const float pj = j < 32 ? a : b;
-    r0 += (pj > p0) || (pj == p0 && j < lane);
-    r1 += (pj > p1) || (pj == p1 && j < lane + 32);
-  }
-  if (lane < E) { sp[r0] = p0; si[r0] = lane; }
-  if (lane + 32 < E) { sp[r1] = p1; si[r1] = lane + 32; }
-  __syncwarp();
-  uint64_t mask = 0ull;
-  int m = E;
-  if (lane == 0) {
-    double cum = 0.0;
-    for (int r = 0; r < E; ++r) {
-      cum = cum + double(sp[r]);
-      if (cum >= dl && r + 1 >= K) { m = r + 1; break; }
-    }
-    for (int r = 0; r < m; ++r) mask |= 1ull << si[r];
-  }
-  *mask_out = shfl_u64(mask, 0);
-  *count_out = __shfl_sync(0xffffffffu, m, 0);
-}
-
+// ------------------------------------------------------------------ K5 select (Eq. 4-6): kernel
+// (the per-warp selection, warp_select, is in select.cuh)
 template <class Tag>
 __global__ void __launch_bounds__(kSelWarps * 32) select_kernel(StoreView st, int B, const int64_t* __restrict__ map_id,
                                                                 const float* __restrict__ score, float delta, int K,
                                                                 int lb, int T, int64_t id_offset, int64_t n_rows,
-                                                                uint64_t* out_mask, int32_t* out_count) {
+                                                                uint64_t* out_mask, int32_t* out_count, int stride) {
   pdl_wait();
   __shared__ float sp[kSelWarps][kMaxE];
   __shared__ int si[kSelWarps][kMaxE];
@@ -200,14 +137,14 @@ __global__ void __launch_bounds__(kSelWarps * 32) select_kernel(StoreView st, in
   const int64_t gw = int64_t(blockIdx.x) * kSelWarps + warp;
   if (gw >= int64_t(B) * T) return;
   const int q = int(gw / T), tt = int(gw % T), t = lb + tt;
-  const int64_t id = map_id[q];
+  const int64_t id = map_id[int64_t(q) * stride];
   const int64_t loc = id - id_offset;
   const int64_t o = int64_t(q) * T + tt;
   if (id < 0 || loc < 0 || loc >= n_rows) {
     if (lane == 0) { out_mask[o] = 0ull; out_count[o] = 0; }
     return;
   }
-  const double dl = selection_delta(delta, score ? score[q] : 0.f);
+  const double dl = selection_delta(delta, score ? score[int64_t(q) * stride] : 0.f);
   uint64_t mask;
   int m;
   warp_select<Tag>(st, t, loc, dl, K, sp[warp], si[warp], &mask, &m);
@@ -219,17 +156,17 @@ __global__ void __launch_bounds__(kSelWarps * 32) select_kernel(StoreView st, in
 
 cudaError_t launch_select(const StoreView& st, int B, const int64_t* map_id, const float* score, float delta, int K,
                           int layer_begin, int layer_end, int64_t id_offset, int64_t n_rows, uint64_t* out_mask,
-                          int32_t* out_count, cudaStream_t s) {
+                          int32_t* out_count, cudaStream_t s, int stride) {
   const int T = layer_end - layer_begin;
   const int64_t warps = int64_t(B) * T;
   if (warps <= 0) return cudaSuccess;
   const int grid = int((warps + kSelWarps - 1) / kSelWarps);
   if (st.bf16)
     return count_launch(), launch_pdl(select_kernel<Bf16Tag>, dim3(grid), dim3(kSelWarps * 32), 0, s, st, B, map_id, score,
-                                      delta, K, layer_begin, T, id_offset, n_rows, out_mask, out_count);
+                                      delta, K, layer_begin, T, id_offset, n_rows, out_mask, out_count, stride);
   else
     return count_launch(), launch_pdl(select_kernel<F32Tag>, dim3(grid), dim3(kSelWarps * 32), 0, s, st, B, map_id, score,
-                                      delta, K, layer_begin, T, id_offset, n_rows, out_mask, out_count);
+                                      delta, K, layer_begin, T, id_offset, n_rows, out_mask, out_count, stride);
   count_launch();
   return cudaGetLastError();
 }

@@ -669,8 +669,19 @@ fmoe_status fmoe_traj_session_reset(fmoe_traj_session* s) {
   return FMOE_OK;
 }
 
-fmoe_status fmoe_traj_session_step(fmoe_traj_session* ss, const float* q_layer, int32_t k, float* out_score,
-                                   int64_t* out_id, void* stream) {
+}  // extern "C"
+
+namespace {
+// Optional selection fused into a session step (fmoe_traj_session_step_select).
+struct StepSelect {
+  float delta = -1.f;
+  int lb = 0, le = 0;                 // layers [lb, le); le == lb: none
+  uint64_t* mask = nullptr;
+  int32_t* count = nullptr;
+};
+
+fmoe_status session_step(fmoe_traj_session* ss, const float* q_layer, int32_t k, float* out_score, int64_t* out_id,
+                         const StepSelect& sel, void* stream) {
   if (!ss || !q_layer) return fail(FMOE_ERR_INVALID_ARG, "null argument");
   const fmoe_store* st = ss->st;
   if (ss->gen != st->gen) return fail(FMOE_ERR_INVALID_ARG, "store changed since the session was reset");
@@ -681,13 +692,24 @@ fmoe_status fmoe_traj_session_step(fmoe_traj_session* ss, const float* q_layer, 
   DeviceGuard g(st->device);
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   Staging S(s, st->device);
+  const int T = sel.le - sel.lb;
   const float* dq = S.in(q_layer, size_t(B) * st->cfg.E);
   float* ds = S.out(out_score, size_t(B) * k);
   int64_t* di = S.out(out_id, size_t(B) * k);
+  uint64_t* dm = T > 0 ? S.out(sel.mask, size_t(B) * T) : nullptr;
+  int32_t* dc = T > 0 ? S.out(sel.count, size_t(B) * T) : nullptr;
   fmoe_status r = S.check();
+  // selection by the select kernel on (ids, scores) with row stride `stride`
+  auto select_after = [&](const int64_t* ids, const float* sc, int stride) {
+    if (r != FMOE_OK || T <= 0) return;
+    cudaError_t e = launch_select(st->view(), int(B), ids, sc, sel.delta, st->cfg.K, sel.lb, sel.le,
+                                  st->cfg.id_offset, st->n, dm, dc, s, stride);
+    if (e != cudaSuccess) r = cuda_fail(e, "select launch");
+  };
   if (r == FMOE_OK && st->n == 0) {
     cudaError_t e = launch_merge_keys(int(B), 0, k, nullptr, k, nullptr, ds, di, nullptr, s);
     if (e != cudaSuccess) r = cuda_fail(e, "merge launch");
+    select_after(di, ds, k);
   } else if (r == FMOE_OK && ss->batched) {
     const int L = st->cfg.L, E = st->cfg.E, ell = ss->layer + 1;
     cudaError_t e = cudaMemcpy2DAsync(ss->prefix + int64_t(ss->layer) * E, size_t(L) * E * 4, dq, size_t(E) * 4,
@@ -716,6 +738,7 @@ fmoe_status fmoe_traj_session_step(fmoe_traj_session* ss, const float* q_layer, 
                             cudaMemcpyDeviceToDevice, s);
       if (e != cudaSuccess) r = cuda_fail(e, "session id copy");
     }
+    select_after(ss->prev, ss->sctmp, kk);
     if (r == FMOE_OK) {
       ss->prev_k = kk;      // == k when the search ran without extra keys
       ++ss->layer;
@@ -747,6 +770,13 @@ fmoe_status fmoe_traj_session_step(fmoe_traj_session* ss, const float* q_layer, 
       sa.acc = ss->acc;
       sa.qn_prev = ss->qn + (ss->layer & 1) * B;
       sa.qn_next = ss->qn + ((ss->layer + 1) & 1) * B;
+      // the selection runs in each pass's last block, on that pass's queries
+      sa.sel_delta = sel.delta;
+      sa.sel_K = st->cfg.K;
+      sa.sel_lb = sel.lb;
+      sa.sel_T = T > 0 ? T : 0;
+      sa.sel_mask = dm;
+      sa.sel_count = dc;
       for (int p = 0; p < npass && r == FMOE_OK; ++p) {
         a.q0 = 4 * p;
         a.nq = int(B - a.q0 < 4 ? B - a.q0 : 4);
@@ -758,6 +788,32 @@ fmoe_status fmoe_traj_session_step(fmoe_traj_session* ss, const float* q_layer, 
     }
   }
   return S.finish(r);
+}
+}  // namespace
+
+extern "C" {
+
+fmoe_status fmoe_traj_session_step(fmoe_traj_session* ss, const float* q_layer, int32_t k, float* out_score,
+                                   int64_t* out_id, void* stream) {
+  return session_step(ss, q_layer, k, out_score, out_id, StepSelect(), stream);
+}
+
+fmoe_status fmoe_traj_session_step_select(fmoe_traj_session* ss, const float* q_layer, int32_t k, float* out_score,
+                                          int64_t* out_id, float delta, int32_t layer_begin, int32_t layer_end,
+                                          uint64_t* out_mask, int32_t* out_count, void* stream) {
+  if (!ss) return fail(FMOE_ERR_INVALID_ARG, "null session");
+  const int L = ss->st->cfg.L;
+  if (layer_begin < 0 || layer_end > L || layer_begin >= layer_end)
+    return fail(FMOE_ERR_INVALID_ARG, "0 <= layer_begin < layer_end <= L");
+  if (!(delta <= 1.f)) return fail(FMOE_ERR_INVALID_ARG, "delta must be <= 1 (negative: dynamic)");
+  if (!out_score || !out_id || !out_mask || !out_count) return fail(FMOE_ERR_INVALID_ARG, "null output");
+  StepSelect sel;
+  sel.delta = delta;
+  sel.lb = layer_begin;
+  sel.le = layer_end;
+  sel.mask = out_mask;
+  sel.count = out_count;
+  return session_step(ss, q_layer, k, out_score, out_id, sel, stream);
 }
 
 fmoe_status fmoe_resolve_victims(int64_t B, int32_t k, const int64_t* ids, int64_t* out_victim, int device,

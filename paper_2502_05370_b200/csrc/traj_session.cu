@@ -18,6 +18,7 @@
 #include "common.cuh"
 #include "kernels.cuh"
 #include "merge.cuh"
+#include "select.cuh"
 
 namespace fmoe {
 
@@ -151,6 +152,31 @@ __global__ void __launch_bounds__(kSessThreads, NQ == 1 ? 4 : 2) traj_session_ke
   trace_mark(a.trace, 3);
   pdl_trigger();
   finish_topk<NQ, KPL, kSessWarps>(lists, sk, a, s_valid, &s_last);
+  if (s.sel_T <= 0) return;
+  // ---- fused selection (Eq. 4-6) on the final top-1 of each query,
+  // by the block that wrote it (its writes are visible after the barrier): one
+  // warp per (query, target layer), the same warp_select as the select kernel
+  __syncthreads();
+  if (!s_last) return;
+  __shared__ float sel_p[kSessWarps][kMaxE];
+  __shared__ int sel_i[kSessWarps][kMaxE];
+  for (int w = warp; w < a.nq * s.sel_T; w += kSessWarps) {
+    const int q = w / s.sel_T, tt = w - q * s.sel_T;
+    const int64_t ob = int64_t(a.q0 + q);
+    const int64_t id = a.out_id[ob * a.k];
+    const int64_t loc = id - int64_t(a.id_offset);
+    const int64_t o = ob * s.sel_T + tt;
+    if (id < 0 || loc < 0 || loc >= a.n_rows) {
+      if (lane == 0) { s.sel_mask[o] = 0ull; s.sel_count[o] = 0; }
+      continue;
+    }
+    const double dl = selection_delta(s.sel_delta, a.out_score[ob * a.k]);
+    uint64_t mask;
+    int m;
+    warp_select<Tag>(st, s.sel_lb + tt, loc, dl, s.sel_K, sel_p[warp], sel_i[warp], &mask, &m);
+    if (lane == 0) { s.sel_mask[o] = mask; s.sel_count[o] = m; }
+    __syncwarp();
+  }
 }
 
 cudaError_t launch_traj_session(const ScanArgs& a, const SessionArgs& s, cudaStream_t stream) {

@@ -331,6 +331,36 @@ def test_trajectory_session_equals_eq2_at_every_prefix(setup, B, k):
         sess.close()
 
 
+@pytest.mark.parametrize("B,k,delta", [(1, 1, -1.0), (3, 8, -1.0), (4, 2, 0.9), (6, 8, -1.0), (9, 1, 0.5)])
+def test_session_step_select_fused(setup, B, k, delta):
+    """fmoe_traj_session_step_select = step + fmoe_select_experts on the top-1,
+    bit for bit (incremental sessions select in the step's last block; B >= 5 on
+    bf16 is a batched session with the select kernel after the scan; B = 9 on the
+    incremental path is three 4-query passes, each selecting its own queries),
+    and the selection equals the oracle's on the returned (id, score)."""
+    st, dt, sh = setup["st"], setup["dtype"], setup["shape"]
+    qm = S.queries(sh, 1, setup["N"], B)[1]
+    a, b = st.trajectory_session(B), st.trajectory_session(B)
+    d = 3
+    try:
+        for ell in range(1, sh.L + 1):
+            lay = qm[:, ell - 1].contiguous().cuda()
+            lb, le = (ell - 1 + d, ell + d) if ell - 1 + d < sh.L else (0, sh.L)
+            fs, fi, fmask, fcnt = a.step_select(lay, k, delta, lb, le)
+            gs, gi = b.step(lay, k)
+            gmask, gcnt = st.select_experts(gi[:, 0].contiguous(), gs[:, 0].contiguous(), delta, lb, le)
+            assert torch.equal(fi, gi) and torch.equal(fs, gs)
+            assert torch.equal(fmask, gmask) and torch.equal(fcnt, gcnt)
+            if ell in (1, 4, sh.L):
+                om, oc = O.select_experts(setup["Qm"], fi[:, 0].cpu().tolist(), fs[:, 0].cpu().double().tolist(),
+                                          float(np.float32(delta)), list(range(lb, le)), sh.K)
+                assert np.array_equal(fmask.cpu().numpy().view(np.uint64), np.array(om, dtype=np.uint64))
+                assert np.array_equal(fcnt.cpu().numpy(), np.array(oc))
+    finally:
+        a.close()
+        b.close()
+
+
 @pytest.mark.parametrize("name", ["qwen_small", "mixtral_tiny", "phi_small"])
 def test_batched_session_seeded_equals_stateless(lib, name):
     """Batched session (bf16, B >= 5): each step is the tcgen05 scan over the
