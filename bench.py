@@ -260,7 +260,11 @@ class Step:
 
 class HostStep(Step):
     """The same step through the C ABI with host (pinned) buffers: the library
-    stages inputs H2D and outputs D2H inside the timed region."""
+    stages inputs H2D and outputs D2H inside the timed region.  Calls run with
+    fmoe_set_host_sync(0): copies are stream-ordered and the step synchronises
+    once, before it reads its result on the host (and, for k > 1, before the
+    host picks each search's top-1 for the selection).  A top-1 with k = 1 is
+    the search's own host output, handed to the next call as its input."""
 
     def __init__(self, fm, st, cfg, traj_mode="stateless", use_cos=True):
         super().__init__(fm, st, cfg, traj_mode, use_cos)
@@ -271,13 +275,28 @@ class HostStep(Step):
         self.mask, self.cnt = pin(B, d, dtype=torch.int64), pin(B, d, dtype=torch.int32)
         self.m1, self.c1 = pin(B, 1, dtype=torch.int64), pin(B, 1, dtype=torch.int32)
 
+    def top1(self, out_s, out_i):
+        """Host buffers holding each query's top-1 (score, id) of the last search."""
+        if out_s.shape[1] == 1:
+            return out_s.view(-1), out_i.view(-1)      # the search's own output, stream-ordered
+        torch.cuda.current_stream().synchronize()
+        self.top_s.copy_(out_s[:, 0]); self.top_i.copy_(out_i[:, 0])
+        return self.top_s, self.top_i
+
     def run(self, q_emb, q_maps, new_emb, new_maps, ev=None):
+        prev = self.fm.fmoe_set_host_sync(0)
+        try:
+            return self._run(q_emb, q_maps, new_emb, new_maps)
+        finally:
+            self.fm.fmoe_set_host_sync(prev)
+
+    def _run(self, q_emb, q_maps, new_emb, new_maps):
         fm, cfg = self.fm, self.cfg
         k, d, L = cfg["k"], 3, self.sh.L
         h = self.st._h
-        out_s, out_i, top_s, top_i = self.out_s, self.out_i, self.top_s, self.top_i
+        out_s, out_i = self.out_s, self.out_i
         self.semantic(h, q_emb, k, out_s, out_i)      # cosines stay in device memory
-        top_s.copy_(out_s[:, 0]); top_i.copy_(out_i[:, 0])
+        top_s, top_i = self.top1(out_s, out_i)
         fm.fmoe_select_experts(h, top_i, top_s, cfg["delta"], 0, d, self.mask, self.cnt)
         if cfg.get("kind") == "blend":
             for ell in cfg["ells"]:
@@ -285,10 +304,11 @@ class HostStep(Step):
                 fm.fmoe_search_blend(h, q_emb, pre, ell, -1.0, k, out_s, out_i)
                 tgt = ell - 1 + d
                 if tgt < L:
-                    top_s.copy_(out_s[:, 0]); top_i.copy_(out_i[:, 0])
+                    top_s, top_i = self.top1(out_s, out_i)
                     fm.fmoe_select_experts(h, top_i, top_s, cfg["delta"], tgt, tgt + 1, self.m1, self.c1)
             nb = cfg["insert"]
             self.insert(h, new_emb[:nb].contiguous(), new_maps[:nb].contiguous())
+            torch.cuda.current_stream().synchronize()   # the step's result, read on the host
             return float(out_s[0, 0])
         if self.sess is not None:
             fm.fmoe_traj_session_reset(self.sess)
@@ -304,9 +324,10 @@ class HostStep(Step):
             else:
                 fm.fmoe_search_trajectory(h, pre, ell, k, out_s, out_i)
             if tgt < L:
-                top_s.copy_(out_s[:, 0]); top_i.copy_(out_i[:, 0])
+                top_s, top_i = self.top1(out_s, out_i)
                 fm.fmoe_select_experts(h, top_i, top_s, cfg["delta"], tgt, tgt + 1, self.m1, self.c1)
         self.insert(h, new_emb, new_maps)
+        torch.cuda.current_stream().synchronize()       # the step's result, read on the host
         return float(out_s[0, 0])
 
     @staticmethod
@@ -521,7 +542,9 @@ def run_fmoe(args, cfg, rank, world, local_rank):
         h2d, d2h = HostStep.bytes_per_step(cfg, cfg["B"], args.traj)
         e2e = {"value": round(searches / (e_ms * 1e-3), 2), "unit": "searches/s", "ms_per_step": round(e_ms, 4),
                "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
-               "note": "host pinned buffers through the C ABI; library stages + synchronises per call"}
+               "note": "host pinned buffers through the C ABI (library stages H2D/D2H on the stream); "
+                       "fmoe_set_host_sync(0): one stream sync per step before the host reads the result "
+                       "(plus one per top-1 hand-off when k > 1)"}
     for obj in (step, locals().get("hstep")):
         if obj is not None and getattr(obj, "sess", None) is not None:
             fm.fmoe_traj_session_destroy(obj.sess)

@@ -264,6 +264,19 @@ fmoe_status fmoe_topk_merge(int64_t B, int32_t n_lists, int32_t k_in, const floa
 fmoe_status fmoe_resolve_victims(int64_t B, int32_t k, const int64_t* ids, int64_t* out_victim,
                                  int device, void* stream);
 
+/* ---- host-buffer completion ---------------------------------------------- */
+/* Calls may take host arrays (staged through device buffers on the call's
+ * stream).  enable != 0 (the default): a call with a host OUTPUT synchronises
+ * its stream before returning, so the output is ready on return.  enable == 0:
+ * the H2D/D2H copies are only enqueued (stream order), the call returns at
+ * once, and the caller synchronises the stream before reading host outputs
+ * and keeps host inputs unchanged until then (pinned memory makes the copies
+ * truly asynchronous; with pageable memory the copies themselves block).  A
+ * host output of one call may be passed as a host input of a later call on
+ * the same stream: the copies are stream-ordered.  Process-wide; returns the
+ * previous setting. */
+int32_t fmoe_set_host_sync(int32_t enable);
+
 /* ---- diagnostics --------------------------------------------------------- */
 const char* fmoe_status_string(fmoe_status s);
 /* Message of the last error on the calling thread ("" if none). */

@@ -69,6 +69,7 @@ def _load():
         "fmoe_status_string": (ctypes.c_char_p, [I32]),
         "fmoe_last_error": (ctypes.c_char_p, []),
         "fmoe_kernel_launch_count": (I64, []),
+        "fmoe_set_host_sync": (I32, [I32]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)
@@ -85,7 +86,7 @@ ABI_SYMBOLS = ("fmoe_store_create", "fmoe_store_destroy", "fmoe_store_size", "fm
                "fmoe_traj_session_step_select",
                "fmoe_traj_session_reset", "fmoe_traj_session_destroy", "fmoe_topk_merge",
                "fmoe_prefetch_plan", "fmoe_eviction_order", "fmoe_status_string",
-               "fmoe_last_error", "fmoe_kernel_launch_count")
+               "fmoe_last_error", "fmoe_kernel_launch_count", "fmoe_set_host_sync")
 
 
 def _check(st: int):
@@ -207,6 +208,12 @@ def fmoe_traj_session_step_select(s, q_layer, k, out_score, out_id, delta, layer
     _check(_lib.fmoe_traj_session_step_select(s, _ptr(_f32(q_layer)), k, _ptr(out_score), _ptr(out_id), delta,
                                               layer_begin, layer_end, _ptr(out_mask), _ptr(out_count),
                                               _stream(stream)))
+
+
+def fmoe_set_host_sync(enable):
+    """Process-wide: whether calls with host outputs synchronise (see include/fmoe.h).
+    Returns the previous setting."""
+    return int(_lib.fmoe_set_host_sync(1 if enable else 0))
 
 
 def fmoe_traj_session_reset(s):

@@ -92,6 +92,7 @@ struct SessionArgs {
   const float* q_layer;   // [B][E] fp32, this step's layer
   int layer;              // 0-based layer consumed by this step
   float* acc;             // [B][cap]
+  int64_t rpw;            // rows per warp (a contiguous range; set by launch_traj_session)
   const double* qn_prev;  // [B]
   double* qn_next;        // [B]
   // optional fused Eq. 4-6 selection on each query's top-1 (sel_T = 0: none),

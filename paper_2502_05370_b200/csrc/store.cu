@@ -1,5 +1,7 @@
 // store.cu -- the C ABI of include/fmoe.h: store object, argument checks,
 // host/device staging, and dispatch of the sm_100a kernels.
+#include <atomic>
+#include <map>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -89,10 +91,29 @@ int ptr_kind(const void* p, int dev) {
   return 0;
 }
 
+// fmoe_set_host_sync: whether a call with host outputs synchronises its stream
+std::atomic<int> g_host_sync{1};
+
+// Staging arena of a (device, stream) for the calling thread: host arguments
+// of a call are carved from one device buffer instead of one cudaMallocAsync /
+// cudaFreeAsync pair each.  A later call on the same stream may reuse the
+// bytes at once: its copies and kernels are ordered after the earlier call's.
+// Grows (stream-ordered free + malloc) when a call needed more.
+struct Arena {
+  char* base = nullptr;
+  size_t cap = 0, want = 0;
+};
+Arena& staging_arena(int dev, cudaStream_t s) {
+  thread_local std::map<std::pair<int, cudaStream_t>, Arena> arenas;
+  return arenas[{dev, s}];
+}
+
 // Stream-ordered staging of host arguments through device buffers.
 struct Staging {
   cudaStream_t s;
   int dev;
+  Arena* arena = nullptr;
+  size_t used = 0;
   std::vector<void*> allocs;
   struct Back { void* host; void* dev; size_t bytes; };
   std::vector<Back> backs;
@@ -106,6 +127,14 @@ struct Staging {
     if (err != cudaSuccess) return nullptr;
     void* p = nullptr;
     if (bytes == 0) bytes = 16;
+    bytes = (bytes + 255) & ~size_t(255);
+    if (!arena) arena = &staging_arena(dev, s);
+    if (used + bytes <= arena->cap) {
+      p = arena->base + used;
+      used += bytes;
+      return p;
+    }
+    if (used + bytes > arena->want) arena->want = used + bytes;   // grow for the next call
     cudaError_t e = cudaMallocAsync(&p, bytes, s);
     if (e != cudaSuccess) { err = e; what = "cudaMallocAsync"; return nullptr; }
     allocs.push_back(p);
@@ -149,7 +178,15 @@ struct Staging {
       }
     }
     for (void* p : allocs) cudaFreeAsync(p, s);
-    if (!backs.empty()) {
+    if (arena && arena->want > arena->cap) {
+      if (arena->base) cudaFreeAsync(arena->base, s);
+      arena->base = nullptr;
+      arena->cap = 0;
+      const size_t nb = arena->want < (size_t(1) << 20) ? (size_t(1) << 20) : arena->want;
+      if (cudaMallocAsync(reinterpret_cast<void**>(&arena->base), nb, s) == cudaSuccess) arena->cap = nb;
+      else cudaGetLastError();
+    }
+    if (!backs.empty() && g_host_sync.load(std::memory_order_relaxed)) {
       cudaError_t e = cudaStreamSynchronize(s);
       if (e != cudaSuccess && st == FMOE_OK) st = cuda_fail(e, "stream sync");
     }
@@ -410,6 +447,8 @@ const char* fmoe_status_string(fmoe_status s) {
 const char* fmoe_last_error(void) { return g_err.c_str(); }
 
 int64_t fmoe_kernel_launch_count(void) { return fmoe::launch_count(); }
+
+int32_t fmoe_set_host_sync(int32_t enable) { return g_host_sync.exchange(enable != 0 ? 1 : 0); }
 
 fmoe_status fmoe_store_create(const fmoe_store_config* cfg, int device, fmoe_store** out) {
   if (!out) return fail(FMOE_ERR_INVALID_ARG, "null out");

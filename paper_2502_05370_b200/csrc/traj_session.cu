@@ -15,6 +15,8 @@
 // Mapping: GT lanes per row (GT = 16-byte chunks per slab row, power of two),
 // 32/GT rows per pass, PASSES passes per warp iteration so a lane keeps 8
 // slab loads in flight; fused top-k via merge.cuh.
+#include <cstdlib>
+
 #include "common.cuh"
 #include "kernels.cuh"
 #include "merge.cuh"
@@ -103,21 +105,23 @@ __global__ void __launch_bounds__(kSessThreads, NQ == 1 ? 4 : 2) traj_session_ke
   const char* slab = static_cast<const char*>(st.maps) + int64_t(layer) * cap * Ep * SB;
   const float* psq = st.psq + int64_t(layer) * cap;
   const int64_t rows_per_iter = int64_t(rpp) * kPasses;
-  const int64_t nw = int64_t(gridDim.x) * kSessWarps;
   const int64_t wg = int64_t(blockIdx.x) * kSessWarps + warp;
+  // this warp's rows: one contiguous range, equal for every warp of the grid
+  const int64_t r0 = wg * s.rpw;
+  const int64_t r1 = r0 + s.rpw < n ? r0 + s.rpw : n;
 
-  for (int64_t base = wg * rows_per_iter; base < n; base += nw * rows_per_iter) {
+  for (int64_t base = r0; base < r1; base += rows_per_iter) {
     uint4 buf[kPasses];
 #pragma unroll
     for (int p = 0; p < kPasses; ++p) {
       const int64_t row = base + p * rpp + g;
-      buf[p] = (row < n && cl < CPY) ? ld_stream(slab + row * Ep * SB + cl * 16) : make_uint4(0u, 0u, 0u, 0u);
+      buf[p] = (row < r1 && cl < CPY) ? ld_stream(slab + row * Ep * SB + cl * 16) : make_uint4(0u, 0u, 0u, 0u);
     }
     float accv[kPasses][NQ], ps[kPasses];
 #pragma unroll
     for (int p = 0; p < kPasses; ++p) {
       const int64_t row = base + p * rpp + g;
-      const bool ok = lead && row < n;
+      const bool ok = lead && row < r1;
       ps[p] = ok ? __ldcs(psq + row) : 0.f;
 #pragma unroll
       for (int q = 0; q < NQ; ++q)
@@ -138,7 +142,7 @@ __global__ void __launch_bounds__(kSessThreads, NQ == 1 ? 4 : 2) traj_session_ke
         for (int o = GT >> 1; o > 0; o >>= 1) d[q] += __shfl_xor_sync(0xffffffffu, d[q], o);
       }
       const int64_t row = base + p * rpp + g;
-      const bool ok = lead && row < n;
+      const bool ok = lead && row < r1;
       const float rm = ps[p] > 0.f ? rsqrtf(ps[p]) : 0.f;
 #pragma unroll
       for (int q = 0; q < NQ; ++q) {
@@ -193,8 +197,16 @@ cudaError_t launch_traj_session(const ScanArgs& a, const SessionArgs& s, cudaStr
                                                               : traj_session_kernel<TAG, 4, 2>;
   if (a.st.bf16) { FMOE_SESS_PICK(Bf16Tag) } else { FMOE_SESS_PICK(F32Tag) }
 #undef FMOE_SESS_PICK
+  // equal contiguous row ranges per warp, in whole 32/GT-row passes
+  const int esz = a.st.bf16 ? 2 : 4;
+  int cpy = a.st.Ep * esz / 16, gt = 1;
+  while (gt < cpy) gt <<= 1;
+  const int64_t rpp = 32 / gt, nw = int64_t(a.grid) * kSessWarps;
+  SessionArgs s2 = s;
+  s2.rpw = ((a.n_rows + nw - 1) / nw + rpp - 1) / rpp * rpp;
+  if (s2.rpw < rpp) s2.rpw = rpp;
   count_launch();
-  return launch_pdl(fn, dim3(a.grid), dim3(kSessThreads), 0, stream, a, s);
+  return launch_pdl(fn, dim3(a.grid), dim3(kSessThreads), 0, stream, a, s2);
 }
 
 int traj_session_grid(const ScanArgs& a) {
@@ -209,8 +221,11 @@ int traj_session_grid(const ScanArgs& a) {
   while (gt < cpy) gt <<= 1;
   const int64_t rows_per_iter = int64_t(32 / gt) * kPasses;
   const int64_t want = (a.n_rows + rows_per_iter * kSessWarps - 1) / (rows_per_iter * kSessWarps);
-  // one wave, and (N = 1M, B = 1) about one iteration per warp: 4 CTAs/SM
+  // one full wave (every SM the same number of CTAs, rows spread evenly by
+  // launch_traj_session), and (N = 1M, B = 1) at most one iteration per warp
   const int64_t full = int64_t(a.nq <= 1 ? 4 : 2) * sms;
+  if (getenv("FMOE_SESS_BALANCE") == nullptr || atoi(getenv("FMOE_SESS_BALANCE")) != 0)
+    if (want > full / 2) return int(full);
   const int64_t gsz = want < full ? want : full;
   return int(gsz < 1 ? 1 : gsz);
 }

@@ -166,6 +166,48 @@ def test_host_pointer_path(setup):
     assert torch.equal(s_h, s_d.cpu()) and torch.equal(i_h, i_d.cpu())
 
 
+def test_host_buffers_without_per_call_sync(setup):
+    """fmoe_set_host_sync(0): host-buffer calls only enqueue their copies; a host
+    output handed to the next call as its input is stream-ordered; after one
+    stream sync every output equals the device path."""
+    lib, st, sh = setup["lib"], setup["st"], setup["shape"]
+    B = 3
+    q = setup["q_emb"][:B].contiguous().pin_memory()
+    qm = setup["q_maps"][:B].contiguous()
+    s_h = torch.empty(B, 1).pin_memory()
+    i_h = torch.empty(B, 1, dtype=torch.int64).pin_memory()
+    m_h = torch.empty(B, 3, dtype=torch.int64).pin_memory()
+    c_h = torch.empty(B, 3, dtype=torch.int32).pin_memory()
+    t_s = torch.empty(B, 2).pin_memory()
+    t_i = torch.empty(B, 2, dtype=torch.int64).pin_memory()
+    lay = [qm[:, l].contiguous().pin_memory() for l in range(4)]
+    sm_h = torch.empty(B, 1, dtype=torch.int64).pin_memory()
+    sc_h = torch.empty(B, 1, dtype=torch.int32).pin_memory()
+    sess = lib.fmoe_traj_session_create(st._h, B)
+    prev = lib.fmoe_set_host_sync(0)
+    try:
+        lib.fmoe_search_semantic(st._h, q, 1, s_h, i_h)
+        lib.fmoe_select_experts(st._h, i_h.view(-1), s_h.view(-1), -1.0, 0, 3, m_h, c_h)
+        for l in range(4):
+            lib.fmoe_traj_session_step_select(sess, lay[l], 2, t_s, t_i, -1.0, l + 3, l + 4, sm_h, sc_h)
+        torch.cuda.current_stream().synchronize()
+    finally:
+        assert lib.fmoe_set_host_sync(prev) == 0
+        lib.fmoe_traj_session_destroy(sess)
+    gs, gi = st.search_semantic(q.cuda(), 1)
+    gm, gc = st.select_experts(gi[:, 0].contiguous(), gs[:, 0].contiguous(), -1.0, 0, 3)
+    assert torch.equal(s_h, gs.cpu()) and torch.equal(i_h, gi.cpu())
+    assert torch.equal(m_h, gm.cpu()) and torch.equal(c_h, gc.cpu())
+    ref = st.trajectory_session(B)
+    try:
+        for l in range(4):
+            rs, ri, rm, rc = ref.step_select(lay[l].cuda(), 2, -1.0, l + 3, l + 4)
+        assert torch.equal(t_s, rs.cpu()) and torch.equal(t_i, ri.cpu())
+        assert torch.equal(sm_h, rm.cpu()) and torch.equal(sc_h, rc.cpu())
+    finally:
+        ref.close()
+
+
 # ---------------------------------------------------------------- edge cases
 def test_edge_cases(lib):
     sh = SHAPES["mixtral_tiny"]

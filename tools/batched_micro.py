@@ -26,6 +26,7 @@ def main():
     p.add_argument("--B", type=int, default=256)
     p.add_argument("--k", type=int, default=8)
     p.add_argument("--ell", type=int, default=31)
+    p.add_argument("--ells", default="", help="comma list: trajectory sweep over these prefixes")
     p.add_argument("--reps", type=int, default=5)
     p.add_argument("--once", action="store_true")
     p.add_argument("--only", default="")
@@ -46,6 +47,22 @@ def main():
         "trajectory": (lambda: fm.fmoe_search_trajectory(st._h, pre, a.ell, a.k, out_s, out_i), a.ell * a.E),
         "blend": (lambda: fm.fmoe_search_blend(st._h, qe, pre, a.ell, -1.0, a.k, out_s, out_i), a.D + a.ell * a.E),
     }
+    if a.ells:
+        for ell in [int(x) for x in a.ells.split(",")]:
+            pre_l = qm[:, :ell].contiguous()
+            fn = lambda: fm.fmoe_search_trajectory(st._h, pre_l, ell, a.k, out_s, out_i)
+            fn()
+            torch.cuda.synchronize()
+            ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            ev0.record()
+            for _ in range(a.reps):
+                fn()
+            ev1.record()
+            torch.cuda.synchronize()
+            us = ev0.elapsed_time(ev1) * 1e3 / a.reps
+            print(f"traj ell={ell:2d} B={a.B}: {us:8.1f} us  {a.n * ell * a.E * 2 / us / 1e3:7.1f} GB/s", flush=True)
+        st.close()
+        return
     for name, (fn, kdim) in calls.items():
         if a.only and name not in a.only.split(","):
             continue
