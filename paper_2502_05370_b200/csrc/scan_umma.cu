@@ -56,9 +56,12 @@ constexpr int UM_N = 256;
 constexpr int kUmEpiWarps = 8;               // 2 per SM sub-partition: two column halves
 constexpr int kUmThreads = (4 + kUmEpiWarps) * 32;
 constexpr int kStageA = UM_M * 128;          // 16 KB of queries per stage (per CTA)
-// store rows per CTA and tile: all 256 (cta_group::1), or half (cta_group::2)
-__host__ __device__ constexpr int um_rows(int cg) { return UM_N / cg; }
-__host__ __device__ constexpr int um_stage_bytes(int cg) { return kStageA + um_rows(cg) * 128; }
+// Tile height TN: 256 store rows, or 128 when a tile needs two accumulators
+// (blend, or the K-split semantic scan) so that two tiles' accumulators still
+// fit TMEM's 512 columns double-buffered (2 x 2 x 128).  Store rows per CTA
+// and tile: all TN (cta_group::1), or half (cta_group::2).
+__host__ __device__ constexpr int um_rows(int cg, int tn = UM_N) { return tn / cg; }
+__host__ __device__ constexpr int um_stage_bytes(int cg, int tn = UM_N) { return kStageA + um_rows(cg, tn) * 128; }
 constexpr int kUmMaxStages = 8;
 
 __device__ __forceinline__ int nvalid_rows(int64_t yc, int64_t n_rows, bool live) {
@@ -305,7 +308,7 @@ __device__ __forceinline__ void red_max_u64(unsigned long long* p, uint64_t v) {
 #define EPI_T(slot) do { } while (0)
 #endif
 
-template <bool SEM, bool TRAJ, int CG>
+template <bool SEM, bool TRAJ, int CG, int TN>
 __global__ void __launch_bounds__(kUmThreads, 1)
     scan_umma_kernel(const __grid_constant__ CUtensorMap tm_qs, const __grid_constant__ CUtensorMap tm_es,
                      const __grid_constant__ CUtensorMap tm_qt, const __grid_constant__ CUtensorMap tm_mt,
@@ -321,12 +324,12 @@ __global__ void __launch_bounds__(kUmThreads, 1)
   }
   __shared__ uint32_t tmem_base_sh;
   // row scales (re, rm) of each half tile, one buffer per TMEM accumulator stage
-  __shared__ __align__(16) float escale[2][2][2][UM_N / 2];
+  __shared__ __align__(16) float escale[2][2][2][TN / 2];
 
   // 1024-byte alignment for the SW128 atoms (the same offsets in both CTAs of a pair)
   unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  constexpr int NB = um_rows(CG);                // store rows of a tile held by this CTA
-  constexpr int SBY = um_stage_bytes(CG);
+  constexpr int NB = um_rows(CG, TN);            // store rows of a tile held by this CTA
+  constexpr int SBY = um_stage_bytes(CG, TN);
   uint64_t* lists = reinterpret_cast<uint64_t*>(smem + size_t(p.stages) * SBY);   // [2R][k][LQ]
   // CTA pair (cta_group::2): rank r owns query rows r*128.. of the M = 256
   // operand and store rows r*128.. of each 256-row tile; the leader (rank 0)
@@ -384,7 +387,7 @@ __global__ void __launch_bounds__(kUmThreads, 1)
       const uint64_t pol = policy_evict_first();
       // store operand of k-block kb of tile t -> L2
       auto prefetch = [&](int t, int kb) {
-        const int y0 = t * UM_N + rank * NB;
+        const int y0 = t * TN + rank * NB;
         if (SEM && kb < p.n_sem_kb) {
           tma_prefetch_l2(&tm_es, kb * 64, y0);
           return;
@@ -406,7 +409,7 @@ __global__ void __launch_bounds__(kUmThreads, 1)
         if (++pkb == n_kb) { pkb = 0; pt += ncl; }
       unsigned u = 0;
       for (int t = cid; t < p.n_tiles; t += ncl) {
-        const int y0 = t * UM_N + rank * NB;           // this CTA's store rows of the tile
+        const int y0 = t * TN + rank * NB;             // this CTA's store rows of the tile
         for (int kb = 0; kb < n_kb; ++kb, ++u) {
           const int s = int(u % unsigned(S));
           if (p.l2pf > 0 && pt < p.n_tiles) {
@@ -475,14 +478,14 @@ __global__ void __launch_bounds__(kUmThreads, 1)
   } else if (warp == 1) {
     // ---------------------------------------------------------------- MMA issuer
     if (lane == 0) {
-      constexpr uint32_t idesc = umma_idesc(UM_M * CG, UM_N);
+      constexpr uint32_t idesc = umma_idesc(UM_M * CG, TN);
       unsigned u = 0, ti = 0;
       for (int t = cid; t < p.n_tiles; t += ncl, ++ti) {
         const int as = int(ti % unsigned(AS));
         mbar_wait(&tempty[as], ((ti / unsigned(AS)) & 1u) ^ 1u);
         tc_fence_after();
-        const uint32_t d_sem = tmem_base + uint32_t(as * NACC * UM_N);
-        const uint32_t d_trj = d_sem + (NACC == 2 ? UM_N : 0);
+        const uint32_t d_sem = tmem_base + uint32_t(as * NACC * TN);
+        const uint32_t d_trj = d_sem + (NACC == 2 ? TN : 0);
         for (int kb = 0; kb < n_kb; ++kb, ++u) {
           const int s = int(u % unsigned(S));
           mbar_wait(&full[s], (u / unsigned(S)) & 1u);
@@ -535,7 +538,7 @@ __global__ void __launch_bounds__(kUmThreads, 1)
     const int e = warp - 4, qd = e & 3, half = e >> 2;
     const int R = p.rep, QA = 4 / R;              // query quadrants per replica
     const int sub = qd / QA;                      // replica index
-    const int NC = (UM_N / 2) / 32 / R;           // 32-column chunks per tile and warp
+    const int NC = (TN / 2) / 32 / R;             // 32-column chunks per tile and warp
     const int q = (qd % QA) * 32 + lane;          // query of this thread (this CTA's TMEM lane)
     const int qg = rank * UM_M + q;               // ... and its row in the pass
     const bool live = q < nq_c;
@@ -546,7 +549,7 @@ __global__ void __launch_bounds__(kUmThreads, 1)
     const int k = p.k;
     const bool split = p.split_kb > 0;
     const bool vec4 = (p.cos_stride & 3) == 0;      // 16-byte aligned cosine rows
-    constexpr int HC = UM_N / 2;                  // columns per half
+    constexpr int HC = TN / 2;                    // columns per half
     uint64_t* ml = lists + size_t(gi) * k * LQ + q;     // this thread's list: entry i at ml[i*LQ]
     const uint32_t ml_s = smem_u32(ml);
     // Admission: a key enters this thread's list if it beats the list's k-th
@@ -580,7 +583,7 @@ __global__ void __launch_bounds__(kUmThreads, 1)
     auto fetch = [&](int t) {
 #pragma unroll
       for (int c = 0; c < HC / 32; ++c) {
-        const int64_t yl = int64_t(t) * UM_N + half * HC + c * 32 + lane;
+        const int64_t yl = int64_t(t) * TN + half * HC + c * 32 + lane;
         const bool yok = qd == 0 && t < p.n_tiles && yl < p.n_rows;
         re_n[c] = (SEM && yok) ? __ldg(p.r_e + yl) : 0.f;
         rm_n[c] = (TRAJ && yok) ? __ldg(p.psq + yl) : 0.f;
@@ -589,7 +592,7 @@ __global__ void __launch_bounds__(kUmThreads, 1)
     fetch(cid);
     for (int t = cid; t < p.n_tiles; t += ncl, ++ti) {
       const int as = int(ti % unsigned(AS));
-      const int ybase = t * UM_N + half * HC + sub * NC * 32;   // first column of this warp
+      const int ybase = t * TN + half * HC + sub * NC * 32;     // first column of this warp
       // this warp's copy of the half tile's row scales, read back as broadcast
       // LDS.128 (4 columns per load) instead of one shuffle per column
       float re_c[HC / 32], rm_c[HC / 32];
@@ -622,8 +625,8 @@ __global__ void __launch_bounds__(kUmThreads, 1)
       // the shared threshold, read now and applied after this tile's chunks
       const uint64_t g_new = live ? ld_relaxed_u64(gq) : 0ull;
       const uint32_t lane_addr = uint32_t(qd * 32) << 16;
-      const uint32_t c_sem = tmem_base + lane_addr + uint32_t(as * NACC * UM_N + half * HC + sub * NC * 32);
-      const uint32_t c_trj = c_sem + (NACC == 2 ? UM_N : 0);
+      const uint32_t c_sem = tmem_base + lane_addr + uint32_t(as * NACC * TN + half * HC + sub * NC * 32);
+      const uint32_t c_trj = c_sem + (NACC == 2 ? TN : 0);
 #pragma unroll 1
       for (int c = 0; c < NC; ++c) {
         uint32_t vs[32], vt[32];
@@ -928,12 +931,14 @@ static size_t lists_bytes(const UmmaPlanIn& in, int R) {
   const int nq = in.nq < UM_M ? in.nq : UM_M;
   return size_t(2 * R) * in.k * ((nq + 31) / 32 * 32) * 8;
 }
-static int stages_for(const UmmaPlanIn& in, int R) {
+// (planning uses TN = 256, the larger stage: a launch at TN = 128 fits as many)
+static int stages_for(const UmmaPlanIn& in, int R, int tn = UM_N) {
   const size_t l = lists_bytes(in, R);
   if (l + 1024 > 216 * 1024) return 0;
-  const int S = int((216 * 1024 - 1024 - l) / size_t(um_stage_bytes(cg_of(in))));
+  const int cg = cg_of(in);
+  const int S = int((216 * 1024 - 1024 - l) / size_t(um_stage_bytes(cg, tn)));
   static const int env = getenv("FMOE_UMMA_STAGES") ? atoi(getenv("FMOE_UMMA_STAGES")) : 0;
-  const int cap = env > 0 ? env : (cg_of(in) == 2 ? 6 : 4);
+  const int cap = env > 0 ? env : (tn == UM_N ? (cg == 2 ? 6 : 4) : kUmMaxStages);
   return S > cap ? cap : S;
 }
 // Query replication: nq <= 32 uses one TMEM lane quadrant, nq <= 64 two; the
@@ -982,7 +987,25 @@ cudaError_t launch_umma(const UmmaLaunch& L, cudaStream_t s) {
   const bool sem = in.w_sem != 0.f && !L.sem_cos, traj = in.w_sem != 1.f;
   const int ell_pad = traj ? in.ell + ((in.Ep * 2 == 16) ? (in.ell & 1) : 0) : 0;
   const int CG = cg_of(in);
-  const int R = CG == 2 || in.rep < 1 ? 1 : in.rep;
+  // tcgen05 fp32 accumulation is not round-to-nearest per step: over D/16 = 256
+  // MMAs (D = 4096) the semantic dot drifted by ~1.4e-5 relative (measured,
+  // C5).  Splitting K over two accumulators halves the chain; the epilogue adds
+  // them in IEEE fp32 (D >= 3072; measured: D = 2048 stays within 7e-6).
+  // Blends weight the semantic part by d/L and their trajectory K is short,
+  // so they keep one accumulator per part.
+  const int n_sem_kb = sem ? (in.Dp + 63) / 64 : 0;
+  const int split_kb = (sem && !traj && n_sem_kb >= 48) ? n_sem_kb / 2 : 0;
+  // Two accumulators per tile (blend or split) single-buffer the 256-row tile's
+  // TMEM.  128-row tiles keep the double buffer (2 x 2 x 128 columns) but
+  // measured slower: the epilogue, not the serialisation, paces these scans.
+  // With the loads removed, a split D = 3072 scan ran 0.72 PFLOP/s at 256 rows
+  // and 0.68 at 128 rows; B = 256 on CTA pairs went 5.5 -> 13.1 ms.  Kept as an
+  // experiment knob (FMOE_UMMA_TN=128).
+  const bool nacc2 = (sem && traj) || split_kb > 0;
+  static const int tn_env = getenv("FMOE_UMMA_TN") ? atoi(getenv("FMOE_UMMA_TN")) : 0;
+  const int TN = tn_env == 128 ? 128 : UM_N;
+  int R = CG == 2 || in.rep < 1 ? 1 : in.rep;
+  if (TN == 128 && R > 2) R = 2;                  // >= one 32-column chunk per replica
   const int MQ = UM_M * CG;
   char* scr = static_cast<char*>(L.scratch);
   __nv_bfloat16* qs = reinterpret_cast<__nv_bfloat16*>(scr);
@@ -1011,7 +1034,7 @@ cudaError_t launch_umma(const UmmaLaunch& L, cudaStream_t s) {
   CUtensorMap tq_s{}, te_s{}, tq_t{}, tm_t{};
   if (sem) {
     if (!make_map(&tq_s, qs, in.Dp, MQ, 64, UM_M, CU_TENSOR_MAP_SWIZZLE_128B) ||
-        !make_map(&te_s, in.emb, in.Dp, in.cap, 64, um_rows(CG), CU_TENSOR_MAP_SWIZZLE_128B))
+        !make_map(&te_s, in.emb, in.Dp, in.cap, 64, um_rows(CG, TN), CU_TENSOR_MAP_SWIZZLE_128B))
       return cudaErrorInvalidValue;
   }
   int tmode = 0, lc = 0, n_traj_kb = 0;
@@ -1023,34 +1046,28 @@ cudaError_t launch_umma(const UmmaLaunch& L, cudaStream_t s) {
                                   : tmode == 2 ? CU_TENSOR_MAP_SWIZZLE_64B
                                                : CU_TENSOR_MAP_SWIZZLE_128B;
     if (!make_map(&tq_t, qt, in.Ep, uint64_t(CG) * ell_pad * UM_M, in.Ep, UM_M, sw) ||
-        !make_map(&tm_t, in.maps, in.Ep, uint64_t(in.L) * in.cap, in.Ep, um_rows(CG), sw))
+        !make_map(&tm_t, in.maps, in.Ep, uint64_t(in.L) * in.cap, in.Ep, um_rows(CG, TN), sw))
       return cudaErrorInvalidValue;
     lc = kStageA / (UM_M * rb);
     n_traj_kb = (ell_pad + lc - 1) / lc;
   }
   UmmaParams p{};
   p.n_rows = in.n_rows;
-  p.n_tiles = int((in.n_rows + UM_N - 1) / UM_N);
+  p.n_tiles = int((in.n_rows + TN - 1) / TN);
   p.k = in.k;
   p.nq = in.nq;
   p.w = in.w_sem;
-  p.n_sem_kb = sem ? (in.Dp + 63) / 64 : 0;
+  p.n_sem_kb = n_sem_kb;
   p.n_traj_kb = n_traj_kb;
   p.ell_pad = ell_pad;
   p.tmode = tmode;
   p.lc = lc;
   const size_t lists = lists_bytes(in, R);
-  p.stages = stages_for(in, R);
+  p.stages = stages_for(in, R, TN);
   if (p.stages < 2) return cudaErrorInvalidValue;
   p.rep = R;
-  // tcgen05 fp32 accumulation is not round-to-nearest per step: over D/16 = 256
-  // MMAs (D = 4096) the semantic dot drifted by ~1.4e-5 relative (measured,
-  // C5).  Splitting K over two accumulators halves the chain; the epilogue adds
-  // them in IEEE fp32.  D >= 3072 only: the split costs the TMEM double buffer.  (Blends weight the semantic part by d/L and their
-  // trajectory K is short, so they keep one accumulator per part.)
-  // (measured: D = 2048 stays within 7e-6; D = 4096 drifted 1.4e-5 unsplit)
-  p.split_kb = (sem && !traj && p.n_sem_kb >= 48) ? p.n_sem_kb / 2 : 0;
-  p.acc_stages = (sem && traj) || p.split_kb > 0 ? 1 : 2;
+  p.split_kb = split_kb;
+  p.acc_stages = nacc2 && TN == UM_N ? 1 : 2;
   {
     static const int pf_env = getenv("FMOE_L2PF") ? atoi(getenv("FMOE_L2PF")) : -1;
     p.l2pf = pf_env >= 0 ? pf_env : 0;   // measured: no gain at either CTA mode (kept as a knob)
@@ -1077,14 +1094,15 @@ cudaError_t launch_umma(const UmmaLaunch& L, cudaStream_t s) {
   p.cos_stride = L.cos_stride;
   p.gthr = L.gthr;
   p.gate = L.gate;
-  const size_t smem = 1024 + size_t(p.stages) * um_stage_bytes(CG) + lists;
+  const size_t smem = 1024 + size_t(p.stages) * um_stage_bytes(CG, TN) + lists;
   using Fn = void (*)(const CUtensorMap, const CUtensorMap, const CUtensorMap, const CUtensorMap, const UmmaParams);
-  const Fn fn = CG == 2 ? (sem && traj ? scan_umma_kernel<true, true, 2>
-                           : sem       ? scan_umma_kernel<true, false, 2>
-                                       : scan_umma_kernel<false, true, 2>)
-                        : (sem && traj ? scan_umma_kernel<true, true, 1>
-                           : sem       ? scan_umma_kernel<true, false, 1>
-                                       : scan_umma_kernel<false, true, 1>);
+#define FMOE_UMMA_PICK(CGV, TNV)                                                      \
+  (sem && traj ? scan_umma_kernel<true, true, CGV, TNV>                               \
+   : sem       ? scan_umma_kernel<true, false, CGV, TNV>                              \
+               : scan_umma_kernel<false, true, CGV, TNV>)
+  const Fn fn = CG == 2 ? (TN == 128 ? FMOE_UMMA_PICK(2, 128) : FMOE_UMMA_PICK(2, 256))
+                        : (TN == 128 ? FMOE_UMMA_PICK(1, 128) : FMOE_UMMA_PICK(1, 256));
+#undef FMOE_UMMA_PICK
   {
     static std::mutex mu;
     static std::map<const void*, size_t> set;
