@@ -10,7 +10,7 @@ numpy.  A library primitive (a dot product via ``@``, a stable sort) serves as a
 step; there is no blocking, fusion or reordering beyond what the definition
 states.  Citations are ``P:n`` = ``/root/reference/PAPER.md`` line ``n`` (and
 ``S:n`` for SPEC.md); every ambiguous passage is resolved by a reading listed in
-DESIGN.md "Readings" (R1..R12) and named next to the code that takes it.
+DESIGN.md "Readings" (R1..R14) and named next to the code that takes it.
 
 Inputs are whatever values the caller gives: to compare with a store that holds
 bf16 tiles, pass the bf16-rounded values (``quantize``) -- the "O-store" view of
@@ -385,3 +385,80 @@ def eviction_order(p, freq, eps: float = 1e-6):
     pri = [eviction_priority(pp, ff, eps) for pp, ff in zip(p, freq)]
     order = sorted(range(len(pri)), key=lambda i: (-pri[i], i))
     return pri, order
+
+
+# --------------------------------------------------------------------------
+# Expert hit rate and the map-search ablation variants
+# --------------------------------------------------------------------------
+def activated_experts(gate, K: int):
+    """The experts the router activates at one layer: the K highest gate
+    probabilities (top-K routing, K from Table 1), ties -> lower
+    expert index (Reading R14).  Returns (sorted expert list, bitmask)."""
+    g = np.asarray(gate, dtype=np.float64)
+    order = sorted(range(g.shape[0]), key=lambda j: (-g[j], j))
+    act = sorted(order[:K])
+    mask = 0
+    for j in act:
+        mask |= 1 << j
+    return act, mask
+
+
+def expert_hits(gate, masks, K: int):
+    """Expert hits of prefetch guidance (an activated expert that was
+    prefetched is a hit): for query x and layer t, hits = |A_{x,t} ∩ P_{x,t}|
+    with A = activated_experts(gate[x][t], K) and P the prefetch set (bitmask
+    masks[x][t]).  The hit rate is sum(hits) / (B*T*K): every layer activates
+    exactly K experts (Constraint 2, "total number of activated experts").
+    Returns (hits[B][T], active_masks[B][T])."""
+    g = np.asarray(gate, dtype=np.float64)
+    B, T = g.shape[0], g.shape[1]
+    hits, act = [], []
+    for x in range(B):
+        hr, ar = [], []
+        for t in range(T):
+            _, a = activated_experts(g[x, t], K)
+            hr.append(bin(a & int(masks[x][t])).count("1"))
+            ar.append(a)
+        hits.append(hr)
+        act.append(ar)
+    return hits, act
+
+
+ABLATION_VARIANTS = ("map_t", "map_ts", "map_tsd")
+
+
+def ablation_prefetch_masks(store_emb, store_maps, q_emb, q_maps, variant: str, d: int, K: int):
+    """Prefetch guidance of one inference iteration under the ablation variants
+    of P:777-790, for every layer t of every query:
+      * layers t < d (no trajectory observed yet): the semantic match (Eq. 1)
+        selects layers 0..d-1 -- "map_ts", "map_tsd"; "map_t"
+        (trajectory only) has no guidance there (empty set, Reading R14);
+      * layers t >= d: the trajectory match over the observed prefix of
+        ell = t - d + 1 layers (Eq. 2, target ell + d, Reading R1) selects layer t;
+      * selection: "map_tsd" uses the similarity-aware delta = Clip(1 - s, 0, 1)
+        of the match; "map_t"/"map_ts" take the fixed top-K of the
+        matched map (delta = 0, i.e. without the delta feature).
+    Returns masks[B][L] (python ints) and the matched ids[B][L]."""
+    q_emb = np.asarray(q_emb)
+    q_maps = np.asarray(q_maps)
+    B, L = q_maps.shape[0], q_maps.shape[1]
+    if variant not in ABLATION_VARIANTS:
+        raise ValueError(variant)
+    delta = -1.0 if variant == "map_tsd" else 0.0
+    masks = [[0] * L for _ in range(B)]
+    ids = [[-1] * L for _ in range(B)]
+    if variant != "map_t":
+        ss, si = topk(semantic_scores(q_emb, store_emb), 1)
+        m, _ = select_experts(store_maps, list(si[:, 0]), list(ss[:, 0]), delta, range(min(d, L)), K)
+        for x in range(B):
+            for t in range(min(d, L)):
+                masks[x][t] = m[x][t]
+                ids[x][t] = int(si[x, 0])
+    for t in range(d, L):
+        ell = t - d + 1
+        ts, ti = topk(trajectory_scores(q_maps, store_maps, ell), 1)
+        m, _ = select_experts(store_maps, list(ti[:, 0]), list(ts[:, 0]), delta, [t], K)
+        for x in range(B):
+            masks[x][t] = m[x][0]
+            ids[x][t] = int(ti[x, 0])
+    return masks, ids

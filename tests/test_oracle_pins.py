@@ -369,3 +369,80 @@ def test_eviction_order_is_a_stable_sort_by_priority():
     assert sorted(order) == list(range(200))
     for a, b in zip(order, order[1:]):
         assert pri[a] > pri[b] or (pri[a] == pri[b] and a < b)
+
+
+# ---------------------------------------------------------------- expert hits + ablation variants
+def test_activated_experts_hand_examples_and_ties():
+    # top-2 of a hand-made gate row; ties -> lower index (Reading R14)
+    assert O.activated_experts([0.1, 0.5, 0.4], 2) == ([1, 2], 0b110)
+    assert O.activated_experts([0.25, 0.25, 0.25, 0.25], 2) == ([0, 1], 0b11)
+    assert O.activated_experts([0.0, 0.3, 0.3, 0.4], 3) == ([1, 2, 3], 0b1110)
+    # K = E -> every expert
+    assert O.activated_experts([0.2, 0.8], 2)[1] == 0b11
+
+
+def test_activated_experts_is_the_max_mass_k_subset():
+    # brute force: the activated set is a K-subset of maximal mass, and the
+    # lexicographically smallest such subset (the tie rule)
+    r = np.random.default_rng(7)
+    for _ in range(300):
+        E = int(r.integers(2, 9))
+        K = int(r.integers(1, E + 1))
+        g = r.integers(0, 4, E).astype(np.float64) / 4.0   # many exact ties
+        act, _ = O.activated_experts(g, K)
+        best = max(sum(g[list(c)]) for c in itertools.combinations(range(E), K))
+        cands = [list(c) for c in itertools.combinations(range(E), K) if sum(g[list(c)]) == best]
+        # among max-mass subsets the rule picks the one whose sorted-by-(p desc, idx) order is smallest
+        assert sum(g[act]) == best and act in cands
+        assert all(g[j] >= g[i] for j in act for i in set(range(E)) - set(act))
+
+
+def test_expert_hits_hand_example_and_bounds():
+    gate = np.array([[[0.1, 0.5, 0.4], [0.6, 0.3, 0.1]]])
+    hits, act = O.expert_hits(gate, [[0b010, 0b111]], 2)
+    assert act == [[0b110, 0b011]] and hits == [[1, 2]]
+    hits, _ = O.expert_hits(gate, [[0, 0]], 2)
+    assert hits == [[0, 0]]
+
+
+def _ablation_store(n=200, L=8, E=8, D=16, seed=3, scale=2.0):
+    r = np.random.default_rng(seed)
+    emb = r.standard_normal((n, D))
+    logits = r.standard_normal((n, L, E)) * scale
+    maps = np.exp(logits) / np.exp(logits).sum(-1, keepdims=True)
+    return emb, maps
+
+
+@pytest.mark.parametrize("K", [1, 2, 3])
+def test_ablation_perfect_information(K):
+    # queries are exact copies of stored contexts: the match is the query itself
+    # with score 1 (delta = 0), so the selected top-K of the matched map IS the
+    # activated set: hit rate 1 for map_ts / map_tsd, and (L - d) / L for
+    # map_t (no guidance for the first d layers).  A wrong target layer, prefix
+    # length or selection order drops below 1.
+    emb, maps = _ablation_store()
+    L, d = maps.shape[1], 3
+    qi = [5, 17, 123, 199]
+    for var, expect in (("map_ts", 1.0), ("map_tsd", 1.0), ("map_t", (L - d) / L)):
+        masks, ids = O.ablation_prefetch_masks(emb, maps, emb[qi], maps[qi], var, d, K)
+        hits, _ = O.expert_hits(maps[qi], masks, K)
+        assert np.sum(hits) / (len(qi) * L * K) == pytest.approx(expect, abs=1e-15), var
+        for x, q in enumerate(qi):
+            assert all(ids[x][t] == q for t in range(d if var != "map_t" else 0, L)) or var == "map_t"
+
+
+def test_ablation_delta_dominates_fixed_topk():
+    # with the same matches, the delta set contains the fixed top-K set
+    # (count >= K in the same order, Eq. 4-6), so map_tsd hits >= map_ts hits everywhere
+    emb, maps = _ablation_store(seed=11, scale=0.3)     # flat gates: top-K mass < delta often
+    r = np.random.default_rng(12)
+    q_emb = emb[:6] + 0.8 * r.standard_normal(emb[:6].shape)
+    _, q_maps = _ablation_store(n=6, seed=13, scale=0.3)                     # fresh gates: matches well below 1
+    m_ts, id_ts = O.ablation_prefetch_masks(emb, maps, q_emb, q_maps, "map_ts", 3, 2)
+    m_tsd, id_tsd = O.ablation_prefetch_masks(emb, maps, q_emb, q_maps, "map_tsd", 3, 2)
+    assert id_ts == id_tsd
+    h_ts, _ = O.expert_hits(q_maps, m_ts, 2)
+    h_tsd, _ = O.expert_hits(q_maps, m_tsd, 2)
+    assert all(a <= b for ra, rb in zip(h_ts, h_tsd) for a, b in zip(ra, rb))
+    assert all((a & b) == a for ra, rb in zip(m_ts, m_tsd) for a, b in zip(ra, rb))
+    assert sum(bin(v).count("1") for r_ in m_tsd for v in r_) > sum(bin(v).count("1") for r_ in m_ts for v in r_)
