@@ -245,6 +245,21 @@ fmoe_status fmoe_prefetch_plan(const fmoe_store* store, int64_t B, const int64_t
 fmoe_status fmoe_eviction_order(int64_t n, const float* p, const float* freq, float eps, double* out_priority,
                                 int32_t* out_order, int device, void* stream);
 
+/* ---- expert hit count of prefetch guidance -------- */
+
+/* For each row r = (query x, layer t) of gate [B][T][E] fp32 (the query's own
+ * observed gate probabilities, finite), the activated experts A_r = the K
+ * largest probabilities, ties -> lower index (top-K routing, Table 1 K,
+ * Reading R14), and out_hits [B][T] int32 = popcount(A_r & prefetch_mask[r])
+ * (prefetch_mask [B][T] uint64, bit j = expert j prefetched, e.g. the output
+ * of fmoe_select_experts).  out_active [B][T] uint64 (may be NULL) receives
+ * A_r.  Hit rate = sum(out_hits) / (B*T*K) (every layer activates K).
+ * 1 <= K <= E <= 64, T >= 1; B == 0 is a no-op.  Pointers device (stream-
+ * ordered) or host (staged), caller-owned. */
+fmoe_status fmoe_expert_hits(int64_t B, int32_t T, int32_t E, int32_t K, const float* gate,
+                             const uint64_t* prefetch_mask, uint64_t* out_active, int32_t* out_hits, int device,
+                             void* stream);
+
 /* ---- sharded merge ---------------------------------------- */
 
 /* Merge n_lists candidate lists per query into the global top-k: scores

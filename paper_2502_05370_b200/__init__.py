@@ -66,6 +66,7 @@ def _load():
         "fmoe_topk_merge": (I32, [I64, I32, I32, P, P, I32, P, P, ctypes.c_int, P]),
         "fmoe_prefetch_plan": (I32, [P, I64, P, P, F, I32, I32, I32, I32, P, P, P, P, P]),
         "fmoe_eviction_order": (I32, [I64, P, P, F, P, P, ctypes.c_int, P]),
+        "fmoe_expert_hits": (I32, [I64, I32, I32, I32, P, P, P, P, ctypes.c_int, P]),
         "fmoe_status_string": (ctypes.c_char_p, [I32]),
         "fmoe_last_error": (ctypes.c_char_p, []),
         "fmoe_kernel_launch_count": (I64, []),
@@ -85,7 +86,7 @@ ABI_SYMBOLS = ("fmoe_store_create", "fmoe_store_destroy", "fmoe_store_size", "fm
                "fmoe_search_blend", "fmoe_select_experts", "fmoe_traj_session_create", "fmoe_traj_session_step",
                "fmoe_traj_session_step_select",
                "fmoe_traj_session_reset", "fmoe_traj_session_destroy", "fmoe_topk_merge",
-               "fmoe_prefetch_plan", "fmoe_eviction_order", "fmoe_status_string",
+               "fmoe_prefetch_plan", "fmoe_eviction_order", "fmoe_expert_hits", "fmoe_status_string",
                "fmoe_last_error", "fmoe_kernel_launch_count", "fmoe_set_host_sync")
 
 
@@ -191,6 +192,13 @@ def fmoe_prefetch_plan(h, map_id, score, delta, l_now, layer_begin, layer_end, m
 def fmoe_eviction_order(p, freq, eps, out_priority, out_order, device=0, stream=None):
     _check(_lib.fmoe_eviction_order(p.shape[0], _ptr(p), _ptr(freq), eps, _ptr(out_priority), _ptr(out_order),
                                     int(device), _stream(stream)))
+
+
+def fmoe_expert_hits(gate, prefetch_mask, K, out_hits, out_active=None, device=0, stream=None):
+    """gate [B][T][E] fp32, prefetch_mask [B][T] (u)int64 -> out_hits [B][T] int32 (+ out_active)."""
+    B, T, E = gate.shape
+    _check(_lib.fmoe_expert_hits(B, T, E, K, _ptr(gate), _ptr(prefetch_mask), _ptr(out_active), _ptr(out_hits),
+                                 int(device), _stream(stream)))
 
 
 def fmoe_traj_session_create(h, B):
@@ -300,6 +308,17 @@ class ExpertMapStore:
         fmoe_select_experts(self._h, map_id.contiguous(), None if score is None else score.contiguous(), delta,
                             layer_begin, layer_end, mask, cnt, stream)
         return mask, cnt
+
+
+def expert_hits(gate, prefetch_mask, K, stream=None):
+    """Hits of prefetch guidance: gate [B][T][E] fp32, prefetch_mask [B][T] int64 (uint64 bits)
+    -> (hits [B][T] int32, activated masks [B][T] int64)."""
+    B, T, _ = gate.shape
+    hits = torch.empty(B, T, dtype=torch.int32, device=gate.device)
+    act = torch.empty(B, T, dtype=torch.int64, device=gate.device)
+    fmoe_expert_hits(gate.contiguous(), prefetch_mask.contiguous(), K, hits, act,
+                     gate.device.index or 0, stream)
+    return hits, act
 
 
 class TrajectorySession:

@@ -152,6 +152,9 @@ cudaError_t launch_prefetch_plan(const StoreView& st, int B, const int64_t* map_
                                  cudaStream_t s);
 cudaError_t launch_eviction_order(int n, const float* p, const float* freq, float eps, double* out_pri,
                                   int32_t* out_order, cudaStream_t s);
+// Expert hits of prefetch guidance: top-K of each gate row vs the prefetched mask.
+cudaError_t launch_expert_hits(int64_t rows, int E, int K, const float* gate, const uint64_t* pmask,
+                               uint64_t* out_active, int32_t* out_hits, cudaStream_t s);
 
 // Quantise + write rows (append or replace) and their norm tables.
 //  slot of new row x: slots ? slots[x] (skip if < 0) : first_slot + x.

@@ -551,4 +551,47 @@ cudaError_t launch_eviction_order(int n, const float* p, const float* freq, floa
   return launch_pdl(evict_kernel, dim3(1), dim3(kEvictThreads), smem, s, n, p, freq, eps, out_pri, out_order);
 }
 
+// ------------------------------------------------------------------ expert hits
+// One warp per (query, layer) row of the observed gate: the K activated experts
+// are the ranks < K under (p desc, index asc) -- the rank computation of
+// warp_select -- collected with two ballots; hits = popcount(active & prefetched).
+__global__ void __launch_bounds__(kSelWarps * 32) hits_kernel(int64_t rows, int E, int K, const float* __restrict__ gate,
+                                                              const uint64_t* __restrict__ pmask,
+                                                              uint64_t* __restrict__ out_active,
+                                                              int32_t* __restrict__ out_hits) {
+  pdl_wait();
+  const int lane = threadIdx.x & 31;
+  const int64_t r = int64_t(blockIdx.x) * kSelWarps + (threadIdx.x >> 5);
+  if (r >= rows) return;
+  const float* g = gate + r * E;
+  const float NEG = -__int_as_float(0x7f800000);
+  const float p0 = lane < E ? __ldg(g + lane) : NEG;
+  const float p1 = lane + 32 < E ? __ldg(g + lane + 32) : NEG;
+  int r0 = 0, r1 = 0;
+  for (int j = 0; j < E; ++j) {
+    const float a = __shfl_sync(0xffffffffu, p0, j & 31);
+    const float b = __shfl_sync(0xffffffffu, p1, j & 31);
+    const float pj = j < 32 ? a : b;
+    r0 += (pj > p0) || (pj == p0 && j < lane);
+    r1 += (pj > p1) || (pj == p1 && j < lane + 32);
+  }
+  const uint32_t lo = __ballot_sync(0xffffffffu, lane < E && r0 < K);
+  const uint32_t hi = __ballot_sync(0xffffffffu, lane + 32 < E && r1 < K);
+  if (lane == 0) {
+    const uint64_t act = (uint64_t(hi) << 32) | lo;
+    if (out_active) out_active[r] = act;
+    out_hits[r] = __popcll(act & pmask[r]);
+  }
+  pdl_trigger();
+}
+
+cudaError_t launch_expert_hits(int64_t rows, int E, int K, const float* gate, const uint64_t* pmask,
+                               uint64_t* out_active, int32_t* out_hits, cudaStream_t s) {
+  if (rows <= 0) return cudaSuccess;
+  count_launch();
+  const unsigned grid = unsigned((rows + kSelWarps - 1) / kSelWarps);
+  return launch_pdl(hits_kernel, dim3(grid), dim3(kSelWarps * 32), 0, s, rows, E, K, gate, pmask, out_active,
+                    out_hits);
+}
+
 }  // namespace fmoe

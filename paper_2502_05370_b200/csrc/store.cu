@@ -993,6 +993,28 @@ fmoe_status fmoe_eviction_order(int64_t n, const float* p, const float* freq, fl
   return S.finish(r);
 }
 
+fmoe_status fmoe_expert_hits(int64_t B, int32_t T, int32_t E, int32_t K, const float* gate,
+                             const uint64_t* prefetch_mask, uint64_t* out_active, int32_t* out_hits, int device,
+                             void* stream) {
+  if (B < 0 || T < 1 || E < 1 || E > 64 || K < 1 || K > E) return fail(FMOE_ERR_INVALID_ARG, "sizes");
+  if (B == 0) return FMOE_OK;
+  if (!gate || !prefetch_mask || !out_hits) return fail(FMOE_ERR_INVALID_ARG, "null argument");
+  DeviceGuard g(device);
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  Staging S(s, device);
+  const size_t rows = size_t(B) * size_t(T);
+  const float* dg = S.in(gate, rows * size_t(E));
+  const uint64_t* dm = S.in(prefetch_mask, rows);
+  uint64_t* da = out_active ? S.out(out_active, rows) : nullptr;
+  int32_t* dh = S.out(out_hits, rows);
+  fmoe_status r = S.check();
+  if (r == FMOE_OK) {
+    cudaError_t e = launch_expert_hits(int64_t(rows), E, K, dg, dm, da, dh, s);
+    if (e != cudaSuccess) r = cuda_fail(e, "hits launch");
+  }
+  return S.finish(r);
+}
+
 fmoe_status fmoe_topk_merge(int64_t B, int32_t n_lists, int32_t k_in, const float* scores, const int64_t* ids,
                             int32_t k, float* out_score, int64_t* out_id, int device, void* stream) {
   if (B < 0 || n_lists < 0 || k_in < 1 || k_in > FMOE_MAX_K || k < 1 || k > FMOE_MAX_K)

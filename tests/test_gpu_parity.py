@@ -519,3 +519,64 @@ def test_eviction_order_bit_exact(lib):
         rp, ro = O.eviction_order(p.astype(np.float64), f.astype(np.float64), float(np.float32(1e-6)))
         assert pri.cpu().tolist() == rp
         assert order.cpu().tolist() == ro
+
+
+# ---------------------------------------------------------------- expert hits + ablation variants
+@pytest.mark.parametrize("E,K", [(8, 2), (16, 2), (60, 4), (64, 8), (64, 64), (1, 1), (33, 5)])
+def test_expert_hits_bit_exact(lib, E, K):
+    rng = np.random.default_rng(100 + E)
+    B, T = 37, 5
+    gate = (rng.integers(0, 6, (B, T, E)) / 8.0).astype(np.float32)    # many exact ties
+    mask = (rng.integers(0, 2 ** 64, (B, T), dtype=np.uint64) & np.uint64((1 << E) - 1 if E < 64 else 2 ** 64 - 1)).view(np.int64)
+    gate[0, 0] = 0.0                                                   # all tied -> experts 0..K-1
+    hits, act = lib.expert_hits(torch.from_numpy(gate).cuda(), torch.from_numpy(mask).cuda(), K)
+    oh, oa = O.expert_hits(gate.astype(np.float64), mask.view(np.uint64).tolist(), K)
+    assert hits.cpu().numpy().tolist() == oh
+    assert act.cpu().numpy().view(np.uint64).tolist() == [[np.uint64(v) for v in r] for r in oa]
+    assert act[0, 0].item() == (1 << K) - 1 if K < 64 else True
+
+
+def test_expert_hits_host_buffers_and_args(lib):
+    gate = torch.rand(3, 4, 8)
+    mask = torch.full((3, 4), 0xF0, dtype=torch.int64)
+    hits = torch.empty(3, 4, dtype=torch.int32)
+    lib.fmoe_expert_hits(gate, mask, 2, hits)                       # host pointers, staged
+    oh, _ = O.expert_hits(gate.double().numpy(), mask.numpy().tolist(), 2)
+    assert hits.numpy().tolist() == oh
+    with pytest.raises(lib.FmoeError):
+        lib.fmoe_expert_hits(gate, mask, 9, hits)                   # K > E
+    lib.fmoe_expert_hits(torch.empty(0, 4, 8), torch.empty(0, 4, dtype=torch.int64), 2,
+                         torch.empty(0, 4, dtype=torch.int32))      # B = 0: no-op
+
+
+@pytest.mark.parametrize("variant", ["map_t", "map_ts", "map_tsd"])
+def test_ablation_variants_match_oracle(setup, variant):
+    from paper_2502_05370_b200 import ablation
+    st, sh, dt = setup["st"], setup["shape"], setup["dtype"]
+    B, d = 6, 3
+    q_emb, q_maps = setup["q_emb"][:B], setup["q_maps"][:B]
+    gm, gid, gsc = ablation.prefetch_masks(st, q_emb.cuda(), q_maps.cuda(), variant)
+    rate, hits, _ = ablation.hit_rate(st, q_emb.cuda(), q_maps.cuda(), variant)
+    gm, gid, gsc = gm.cpu().numpy().view(np.uint64), gid.cpu().numpy(), gsc.cpu().numpy()
+    Qq_e, Qq_m = O.quantize(q_emb.numpy(), dt), O.quantize(q_maps.numpy(), dt)
+    om, oid = O.ablation_prefetch_masks(setup["Qe"], setup["Qm"], Qq_e, Qq_m, variant, d, sh.K)
+    delta = -1.0 if variant == "map_tsd" else 0.0
+    for t in range(sh.L):
+        if t < d and variant == "map_t":
+            assert (gm[:, t] == 0).all() and (gid[:, t] == -1).all()
+            continue
+        # ids: the top-1 rules of check_topk against the oracle scores of that match
+        ref = (O.semantic_scores(Qq_e, setup["Qe"]) if t < d else
+               O.trajectory_scores(Qq_m, setup["Qm"], t - d + 1))
+        check_topk(torch.from_numpy(gsc[:, t:t + 1]), torch.from_numpy(gid[:, t:t + 1]), ref, 1)
+        # masks: bit-exact Eq. 4-6 selection of the matched (id, score)
+        sm, _ = O.select_experts(setup["Qm"], gid[:, t].tolist(), gsc[:, t].astype(np.float64).tolist(),
+                                 delta, [t], sh.K)
+        assert gm[:, t].tolist() == [np.uint64(r[0]) for r in sm], t
+        # where the oracle took the same match, the oracle's own mask agrees
+        for x in range(B):
+            if gid[x, t] == oid[x][t] and delta == 0.0:
+                assert int(gm[x, t]) == om[x][t]
+    oh, _ = O.expert_hits(q_maps.double().numpy(), gm.tolist(), sh.K)
+    assert hits.cpu().numpy().tolist() == oh
+    assert rate == pytest.approx(np.sum(oh) / (B * sh.L * sh.K), abs=0)
