@@ -60,8 +60,10 @@ def parse():
     p.add_argument("--warmup", type=int, default=3)
     p.add_argument("--config", default="C2", choices=sorted(WORKLOADS))
     p.add_argument("--impl", default="fmoe", choices=["fmoe", "reference"])
-    p.add_argument("--traj", default="session", choices=["session", "stateless"],
-                   help="trajectory sweep: incremental session (SURVEY §8(f) #1) or one stateless search per prefix")
+    p.add_argument("--traj", default="sweep", choices=["sweep", "session", "stateless"],
+                   help="trajectory steps: one session-sweep call (B = 1, k = 1: every step in one launch, running "
+                        "dots in registers; other batches fall back to 'session'), one incremental session step "
+                        "per layer (SURVEY §8(f) #1), or one stateless search per prefix")
     p.add_argument("--no-graph", dest="graph", action="store_false",
                    help="time eager launches instead of a CUDA-graph replay of the step")
     p.add_argument("--no-cos", dest="cos", action="store_false",
@@ -91,6 +93,13 @@ def batched_session(cfg):
     return cfg["dtype"] == "bf16" and cfg["B"] >= 5
 
 
+def use_sweep(cfg):
+    """fmoe_traj_session_sweep's fused kernel: one request (B = 1), top-1, 16-byte slab rows."""
+    s = 2 if cfg["dtype"] == "bf16" else 4
+    E16 = (cfg["shape"].E * s + 15) // 16 * 16
+    return cfg["B"] == 1 and cfg["k"] == 1 and E16 == 16 and cfg.get("kind") != "blend"
+
+
 def algorithmic_bytes(cfg, N, traj_mode="stateless", use_cos=False):
     """bytes a scan must stream per launch (store tiles only).
     Session step ell: slab ell-1, the prefix-norm row, and the per-query running
@@ -101,7 +110,11 @@ def algorithmic_bytes(cfg, N, traj_mode="stateless", use_cos=False):
     B = cfg["B"]
     if cfg.get("kind") == "blend":
         traj = {ell: N * (sh.D + ell * sh.E) * s for ell in cfg["ells"]}
-    elif traj_mode == "session" and not batched_session(cfg):
+    elif traj_mode == "sweep" and use_sweep(cfg):
+        # slab + prefix-norm row per step; the running dots live in registers and
+        # are written back once (charged to the last step)
+        traj = {ell: N * (sh.E * s + 4 + (4 * B if ell == sh.L - 1 else 0)) for ell in range(1, sh.L)}
+    elif traj_mode in ("session", "sweep") and not batched_session(cfg):
         traj = {ell: N * (sh.E * s + 4 + 4 * B * (2 if ell > 1 else 1)) for ell in range(1, sh.L)}
     else:
         traj = {ell: N * ell * sh.E * s for ell in range(1, sh.L)}
@@ -175,7 +188,13 @@ class Step:
         self.sh = cfg["shape"]
         # (blend workloads search at fixed prefixes: no trajectory sweep, no session)
         self.sess = (fm.fmoe_traj_session_create(st._h, cfg["B"])
-                     if traj_mode == "session" and cfg.get("kind") != "blend" else None)
+                     if traj_mode in ("session", "sweep") and cfg.get("kind") != "blend" else None)
+        self.sweep = traj_mode == "sweep" and use_sweep(cfg)
+        if self.sweep:
+            n, B = self.sh.L - 1, cfg["B"]
+            self.sw = (torch.empty(n, B, device=st.device), torch.empty(n, B, dtype=torch.int64, device=st.device),
+                       torch.empty(n, B, dtype=torch.int64, device=st.device),
+                       torch.empty(n, B, dtype=torch.int32, device=st.device))
         # semantic cosines kept on the device for the RDY insert (fmoe_store_insert_cos):
         # the iteration's new context carries the embedding its semantic search used
         n = len(st)
@@ -239,6 +258,14 @@ class Step:
             return
         if self.sess is not None:
             fm.fmoe_traj_session_reset(self.sess)        # the store changed at the last insert
+        if self.sweep:
+            # layers 0..L-2 observed; step ell selects target layer ell-1+d (none past L)
+            ql = new_maps[:, :L - 1].permute(1, 0, 2)     # [L-1][1][E]: a contiguous view for B = 1
+            sw_s, sw_i, sw_m, sw_c = self.sw
+            rec("traj_sweep", lambda: fm.fmoe_traj_session_sweep(self.sess, ql, sw_s, sw_i, cfg["delta"], d,
+                                                                 sw_m, sw_c))
+            rec("rdy_insert", lambda: self.insert(h, new_emb, new_maps))
+            return
         for ell in range(1, L):
             pre, lay = q_maps[ell - 1]
             tgt = ell - 1 + d
@@ -274,6 +301,10 @@ class HostStep(Step):
         self.top_s, self.top_i = pin(B), pin(B, dtype=torch.int64)
         self.mask, self.cnt = pin(B, d, dtype=torch.int64), pin(B, d, dtype=torch.int32)
         self.m1, self.c1 = pin(B, 1, dtype=torch.int64), pin(B, 1, dtype=torch.int32)
+        if self.sweep:
+            n = self.sh.L - 1
+            self.sw = (pin(n, B), pin(n, B, dtype=torch.int64), pin(n, B, dtype=torch.int64),
+                       pin(n, B, dtype=torch.int32))
 
     def top1(self, out_s, out_i):
         """Host buffers holding each query's top-1 (score, id) of the last search."""
@@ -312,6 +343,13 @@ class HostStep(Step):
             return float(out_s[0, 0])
         if self.sess is not None:
             fm.fmoe_traj_session_reset(self.sess)
+        if self.sweep:
+            sw_s, sw_i, sw_m, sw_c = self.sw
+            fm.fmoe_traj_session_sweep(self.sess, new_maps[:, :L - 1].permute(1, 0, 2), sw_s, sw_i, cfg["delta"], d,
+                                       sw_m, sw_c)
+            self.insert(h, new_emb, new_maps)
+            torch.cuda.current_stream().synchronize()   # the step's result, read on the host
+            return float(sw_s[-1, 0])
         for ell in range(1, L):
             pre, lay = q_maps[ell - 1]
             tgt = ell - 1 + d
@@ -340,11 +378,14 @@ class HostStep(Step):
             h2d += n_sel * B * 12
             d2h = (1 + len(ells)) * B * k * 12 + B * d * 12 + (n_sel - 1) * B * 12
             return h2d, d2h
-        traj_in = sum(B * (1 if traj_mode == "session" else ell) * sh.E * 4 for ell in range(1, L))
+        inc = traj_mode in ("session", "sweep")
+        traj_in = sum(B * (1 if inc else ell) * sh.E * 4 for ell in range(1, L))
         h2d = B * sh.D * 4 + traj_in + B * (sh.D + L * sh.E) * 4
         n_sel = 1 + sum(1 for ell in range(1, L) if ell - 1 + d < L)
         # map ids + scores into select (a session step selects on the device: no copy)
-        h2d += (1 if traj_mode == "session" else n_sel) * B * (8 + 4)
+        h2d += (1 if inc else n_sel) * B * (8 + 4)
+        if traj_mode == "sweep" and use_sweep(cfg):
+            n_sel = L           # the sweep writes a (zero) mask + count for the steps past the last layer too
         d2h = (L) * B * k * (4 + 8)                                 # search outputs
         d2h += B * d * (8 + 4) + (n_sel - 1) * B * (8 + 4)          # masks + counts
         return h2d, d2h
@@ -517,7 +558,8 @@ def run_fmoe(args, cfg, rank, world, local_rank):
                     "semantic": {"ms": round(kind_ms.get("semantic", 0), 4), "GBps": round(sem_b / kind_ms.get("semantic", 1) / 1e6, 1)},
                     "trajectory_sweep": {"ms": round(traj_ms, 4), "GBps": round(sum(traj_b.values()) / max(traj_ms, 1e-9) / 1e6, 1)},
                     "rdy_insert": {"ms": round(kind_ms.get("rdy_insert", 0), 4), "GBps": round(rdy_b / kind_ms.get("rdy_insert", 1) / 1e6, 1)},
-                    "traj_ell31_GBps": round(traj_b[sh_L(cfg) - 1] / kind_ms.get(f"traj{sh_L(cfg) - 1}", 1) / 1e6, 1),
+                    **({"traj_ell31_GBps": round(traj_b[sh_L(cfg) - 1] / kind_ms[f"traj{sh_L(cfg) - 1}"] / 1e6, 1)}
+                       if f"traj{sh_L(cfg) - 1}" in kind_ms else {}),
                 }}
     # strong scaling: a search covers the whole (sharded) store, so the job
     # completes `searches` per step whatever the number of ranks
@@ -653,7 +695,11 @@ def main():
                    "insert": ("RDY semantic half reused from the step's semantic search (fmoe_store_insert_cos)"
                               if args.cos and world == 1 else "full RDY scan"),
                    "trajectory": ("stateless: one search over the whole prefix per ell"
-                                  if args.traj != "session" or world > 1 else
+                                  if args.traj == "stateless" or world > 1 else
+                                  "session sweep: the L-1 incremental steps of the request in one call "
+                                  "(fmoe_traj_session_sweep: running dots in registers, slab + norm row per step, "
+                                  "per-step top-1 + Eq. 4-6 selection by each step's last block)"
+                                  if args.traj == "sweep" and use_sweep(cfg) else
                                   "batched session: per ell one tcgen05 scan over the whole prefix, seeded with "
                                   "the previous step's rows (fmoe_traj_session_step)" if batched_session(cfg) else
                                   "incremental session: step ell reads slab ell + running dots (SURVEY §8(f) #1)"),

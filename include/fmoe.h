@@ -202,6 +202,27 @@ fmoe_status fmoe_traj_session_step_select(fmoe_traj_session* session, const floa
                                           float* out_score, int64_t* out_id, float delta, int32_t layer_begin,
                                           int32_t layer_end, uint64_t* out_mask, int32_t* out_count,
                                           void* stream);
+/* n_steps consecutive steps of the session in ONE call: step s consumes layer
+ * ell0 + s (ell0 = layers consumed so far) from q_layers [n_steps][B][E] fp32,
+ * writes the top-1 (k = 1, "the highest score is selected") to
+ * out_score / out_id [n_steps][B] and, when out_mask is non-NULL, the Eq. 4-6
+ * selection (delta as in fmoe_select_experts) of target layer
+ * ell0 + s + sel_d to out_mask / out_count [n_steps][B] (mask 0, count 0 when
+ * the target is >= L).  Results are bit-identical to n_steps calls of
+ * fmoe_traj_session_step_select(k = 1).  Fused path (B = 1, 16-byte slab rows
+ * -- bf16 E <= 8 or fp32 E <= 4 -- and n <= 8 * 4 * SMs * 256 rows): one
+ * kernel keeps the running dot products in registers across the steps.
+ * Optional DEVICE flags (fused path only, else FMOE_ERR_UNSUPPORTED):
+ * layer_ready [n_steps] -- step s starts once layer_ready[s] != 0 (written by
+ * the producer of the gates, e.g. the MoE forward; the kernel waits, so the
+ * producer must not need this kernel's SMs to make progress); guidance_ready
+ * [n_steps] -- set to 1 (release) once step s's outputs are written: the
+ * device-side publisher/subscriber of P:528-533.  A layer not ready within
+ * 10 s abandons the sweep (guidance flags stay 0; reset the session). */
+fmoe_status fmoe_traj_session_sweep(fmoe_traj_session* session, const float* q_layers, int32_t n_steps,
+                                    float* out_score, int64_t* out_id, float delta, int32_t sel_d,
+                                    uint64_t* out_mask, int32_t* out_count, const uint32_t* layer_ready,
+                                    uint32_t* guidance_ready, void* stream);
 /* Start a new prefix (next step consumes layer 0); re-validates against the store. */
 fmoe_status fmoe_traj_session_reset(fmoe_traj_session* session);
 void fmoe_traj_session_destroy(fmoe_traj_session* session);

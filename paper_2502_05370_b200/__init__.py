@@ -61,6 +61,7 @@ def _load():
         "fmoe_traj_session_create": (I32, [P, I64, ctypes.POINTER(P)]),
         "fmoe_traj_session_step": (I32, [P, P, I32, P, P, P]),
         "fmoe_traj_session_step_select": (I32, [P, P, I32, P, P, F, I32, I32, P, P, P]),
+        "fmoe_traj_session_sweep": (I32, [P, P, I32, P, P, F, I32, P, P, P, P, P]),
         "fmoe_traj_session_reset": (I32, [P]),
         "fmoe_traj_session_destroy": (None, [P]),
         "fmoe_topk_merge": (I32, [I64, I32, I32, P, P, I32, P, P, ctypes.c_int, P]),
@@ -84,7 +85,7 @@ ABI_SYMBOLS = ("fmoe_store_create", "fmoe_store_destroy", "fmoe_store_size", "fm
                "fmoe_store_insert", "fmoe_store_insert_cos", "fmoe_search_semantic_cos", "fmoe_store_read",
                "fmoe_store_write", "fmoe_resolve_victims", "fmoe_search_semantic", "fmoe_search_trajectory",
                "fmoe_search_blend", "fmoe_select_experts", "fmoe_traj_session_create", "fmoe_traj_session_step",
-               "fmoe_traj_session_step_select",
+               "fmoe_traj_session_step_select", "fmoe_traj_session_sweep",
                "fmoe_traj_session_reset", "fmoe_traj_session_destroy", "fmoe_topk_merge",
                "fmoe_prefetch_plan", "fmoe_eviction_order", "fmoe_expert_hits", "fmoe_status_string",
                "fmoe_last_error", "fmoe_kernel_launch_count", "fmoe_set_host_sync")
@@ -218,6 +219,14 @@ def fmoe_traj_session_step_select(s, q_layer, k, out_score, out_id, delta, layer
                                               _stream(stream)))
 
 
+def fmoe_traj_session_sweep(s, q_layers, out_score, out_id, delta=-1.0, sel_d=-1, out_mask=None, out_count=None,
+                            layer_ready=None, guidance_ready=None, stream=None):
+    """q_layers [n_steps][B][E] -> out_score/out_id [n_steps][B] (+ selection masks/counts)."""
+    _check(_lib.fmoe_traj_session_sweep(s, _ptr(q_layers), q_layers.shape[0], _ptr(out_score), _ptr(out_id), delta,
+                                        sel_d, _ptr(out_mask), _ptr(out_count), _ptr(layer_ready),
+                                        _ptr(guidance_ready), _stream(stream)))
+
+
 def fmoe_set_host_sync(enable):
     """Process-wide: whether calls with host outputs synchronise (see include/fmoe.h).
     Returns the previous setting."""
@@ -344,6 +353,21 @@ class TrajectorySession:
         cnt = torch.empty(self.B, T, dtype=torch.int32, device=dev)
         fmoe_traj_session_step_select(self._s, q_layer.contiguous(), k, s, i, delta, layer_begin, layer_end, mask,
                                       cnt, stream)
+        return s, i, mask, cnt
+
+    def sweep(self, q_layers, delta=-1.0, sel_d=None, layer_ready=None, guidance_ready=None, stream=None):
+        """n = q_layers.shape[0] steps in one call (k = 1): q_layers [n][B][E] -> scores, ids [n][B] and
+        the selection masks / counts [n][B] of target layer (consumed layer + sel_d) (None: no selection)."""
+        dev = self.store.device
+        n = q_layers.shape[0]
+        s = torch.empty(n, self.B, dtype=torch.float32, device=dev)
+        i = torch.empty(n, self.B, dtype=torch.int64, device=dev)
+        mask = cnt = None
+        if sel_d is not None:
+            mask = torch.empty(n, self.B, dtype=torch.int64, device=dev)
+            cnt = torch.empty(n, self.B, dtype=torch.int32, device=dev)
+        fmoe_traj_session_sweep(self._s, q_layers.contiguous(), s, i, delta, -1 if sel_d is None else sel_d, mask,
+                                cnt, layer_ready, guidance_ready, stream)
         return s, i, mask, cnt
 
     def reset(self):

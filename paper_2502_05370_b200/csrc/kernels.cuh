@@ -105,6 +105,31 @@ struct SessionArgs {
 cudaError_t launch_traj_session(const ScanArgs& a, const SessionArgs& s, cudaStream_t stream);
 int traj_session_grid(const ScanArgs& a);
 
+// n session steps of one request (B = 1, k = 1, 16-byte slab rows) in one launch
+struct SweepArgs {
+  StoreView st;
+  int64_t n_rows;
+  uint32_t id_offset;
+  const float* q_layers;            // [n_steps][E] fp32
+  int layer0, n_steps;
+  float* acc;                       // [cap] session accumulators (read if layer0 > 0, written at the end)
+  const double* qn_in;              // running query norm before layer0
+  double* qn_out;                   // after the last step
+  unsigned long long* best;         // [n_steps] zeroed scratch (reset by the kernel)
+  unsigned* tickets;                // [n_steps] zeroed scratch (reset by the kernel)
+  float* out_score;                 // [n_steps]
+  int64_t* out_id;                  // [n_steps]
+  float sel_delta;
+  int sel_K, sel_d;                 // target layer of step s = layer0 + s + sel_d (none if >= L)
+  uint64_t* sel_mask;               // [n_steps] or null (no selection)
+  int32_t* sel_count;               // [n_steps]
+  const unsigned* layer_ready;      // [n_steps] or null: step s waits for layer_ready[s] != 0
+  unsigned* guidance_ready;         // [n_steps] or null: set to 1 when step s's outputs are written
+  unsigned long long timeout_ns;    // give up waiting for a layer after this long
+};
+int traj_sweep_rows(int64_t n_rows, int* grid_out);   // 0: the store is too large for the register sweep
+cudaError_t launch_traj_sweep(const SweepArgs& a, cudaStream_t stream);
+
 // tcgen05 batched scan (scan_umma.cu)
 struct UmmaPlanIn {
   int bf16, nq, k, D, Dp, E, Ep, L, ell;

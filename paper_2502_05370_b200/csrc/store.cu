@@ -661,6 +661,7 @@ struct fmoe_traj_session {
   int prev_k = 0;
   int layer = 0;
   uint64_t gen = 0;
+  void* sweep_scratch = nullptr;   // [L] u64 best keys + [L] u32 tickets (fmoe_traj_session_sweep)
 };
 
 extern "C" {
@@ -697,6 +698,7 @@ void fmoe_traj_session_destroy(fmoe_traj_session* s) {
   cudaFree(s->prefix);
   cudaFree(s->prev);
   cudaFree(s->sctmp);
+  cudaFree(s->sweep_scratch);
   delete s;
 }
 
@@ -853,6 +855,98 @@ fmoe_status fmoe_traj_session_step_select(fmoe_traj_session* ss, const float* q_
   sel.mask = out_mask;
   sel.count = out_count;
   return session_step(ss, q_layer, k, out_score, out_id, sel, stream);
+}
+
+fmoe_status fmoe_traj_session_sweep(fmoe_traj_session* ss, const float* q_layers, int32_t n_steps,
+                                    float* out_score, int64_t* out_id, float delta, int32_t sel_d,
+                                    uint64_t* out_mask, int32_t* out_count, const uint32_t* layer_ready,
+                                    uint32_t* guidance_ready, void* stream) {
+  if (!ss || !q_layers || !out_score || !out_id) return fail(FMOE_ERR_INVALID_ARG, "null argument");
+  const fmoe_store* st = ss->st;
+  const int L = st->cfg.L, E = st->cfg.E;
+  if (n_steps < 1 || ss->layer + n_steps > L) return fail(FMOE_ERR_INVALID_ARG, "1 <= n_steps <= L - layer");
+  if (ss->gen != st->gen) return fail(FMOE_ERR_INVALID_ARG, "store changed since the session was reset");
+  if (!(delta <= 1.f)) return fail(FMOE_ERR_INVALID_ARG, "delta must be <= 1 (negative: dynamic)");
+  if (out_mask && (!out_count || sel_d < 0)) return fail(FMOE_ERR_INVALID_ARG, "selection needs out_count, sel_d >= 0");
+  const int esz = st->bf16 ? 2 : 4;
+  int grid = 1;
+  const bool fused = ss->B == 1 && !ss->batched && st->view().Ep * esz == 16 && st->n > 0 && n_steps <= 64 &&
+                     traj_sweep_rows(st->n, &grid) != 0;
+  if (!fused) {
+    // same results through one step call per layer; device flags cannot gate host-issued steps
+    if (layer_ready || guidance_ready)
+      return fail(FMOE_ERR_UNSUPPORTED, "ready flags need the fused sweep (B = 1, 16-byte slab rows, n <= 8 * 4 * SMs * 256)");
+    const int64_t B = ss->B;
+    for (int s2 = 0; s2 < n_steps; ++s2) {
+      const int layer = ss->layer, tgt = layer + sel_d;
+      StepSelect sel;
+      if (out_mask && tgt < L) {
+        sel.delta = delta; sel.lb = tgt; sel.le = tgt + 1;
+        sel.mask = out_mask + int64_t(s2) * B; sel.count = out_count + int64_t(s2) * B;
+      }
+      fmoe_status r = session_step(ss, q_layers + int64_t(s2) * B * E, 1, out_score + int64_t(s2) * B,
+                                   out_id + int64_t(s2) * B, sel, stream);
+      if (r != FMOE_OK) return r;
+      if (out_mask && tgt >= L) {
+        cudaStream_t s = static_cast<cudaStream_t>(stream);
+        const bool dev = ptr_kind(out_mask, st->device) == 1;
+        if (dev) {
+          DeviceGuard g(st->device);
+          cudaMemsetAsync(out_mask + int64_t(s2) * B, 0, size_t(B) * 8, s);
+          cudaMemsetAsync(out_count + int64_t(s2) * B, 0, size_t(B) * 4, s);
+        } else {
+          memset(out_mask + int64_t(s2) * B, 0, size_t(B) * 8);
+          memset(out_count + int64_t(s2) * B, 0, size_t(B) * 4);
+        }
+      }
+    }
+    return FMOE_OK;
+  }
+  DeviceGuard g(st->device);
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if ((layer_ready && ptr_kind(layer_ready, st->device) != 1) ||
+      (guidance_ready && ptr_kind(guidance_ready, st->device) != 1))
+    return fail(FMOE_ERR_INVALID_ARG, "ready flags must be device memory of the store's device");
+  if (!ss->sweep_scratch) {
+    cudaError_t e = cudaMalloc(&ss->sweep_scratch, size_t(L) * 12);
+    if (e != cudaSuccess) return cuda_fail(e, "sweep scratch");
+  }
+  Staging S(s, st->device);
+  const float* dq = S.in(q_layers, size_t(n_steps) * E);
+  float* ds = S.out(out_score, size_t(n_steps));
+  int64_t* di = S.out(out_id, size_t(n_steps));
+  uint64_t* dm = out_mask ? S.out(out_mask, size_t(n_steps)) : nullptr;
+  int32_t* dc = out_mask ? S.out(out_count, size_t(n_steps)) : nullptr;
+  fmoe_status r = S.check();
+  if (r == FMOE_OK) {
+    cudaError_t e = cudaMemsetAsync(ss->sweep_scratch, 0, size_t(L) * 12, s);
+    SweepArgs a{};
+    a.st = st->view();
+    a.n_rows = st->n;
+    a.id_offset = uint32_t(st->cfg.id_offset);
+    a.q_layers = dq;
+    a.layer0 = ss->layer;
+    a.n_steps = n_steps;
+    a.acc = ss->acc;
+    a.qn_in = ss->qn + (ss->layer & 1);
+    a.qn_out = ss->qn + ((ss->layer + n_steps) & 1);
+    a.best = reinterpret_cast<unsigned long long*>(ss->sweep_scratch);
+    a.tickets = reinterpret_cast<unsigned*>(static_cast<char*>(ss->sweep_scratch) + size_t(L) * 8);
+    a.out_score = ds;
+    a.out_id = di;
+    a.sel_delta = delta;
+    a.sel_K = st->cfg.K;
+    a.sel_d = sel_d;
+    a.sel_mask = dm;
+    a.sel_count = dc;
+    a.layer_ready = layer_ready;
+    a.guidance_ready = guidance_ready;
+    a.timeout_ns = 10ull * 1000 * 1000 * 1000;
+    if (e == cudaSuccess) e = launch_traj_sweep(a, s);
+    if (e != cudaSuccess) r = cuda_fail(e, "sweep launch");
+    else ss->layer += n_steps;
+  }
+  return S.finish(r);
 }
 
 fmoe_status fmoe_resolve_victims(int64_t B, int32_t k, const int64_t* ids, int64_t* out_victim, int device,

@@ -230,4 +230,260 @@ int traj_session_grid(const ScanArgs& a) {
   return int(gsz < 1 ? 1 : gsz);
 }
 
+// ------------------------------------------------------------------ sweep: n session steps, one launch
+// The steps of one request (B = 1, k = 1) over layers layer0 .. layer0+n-1 in
+// ONE launch (fmoe_traj_session_sweep).  Each thread owns up to kSweepRows
+// fixed rows (row = gtid + i * threads) and keeps their running dot products
+// in REGISTERS across the steps, so step ell reads only the 16-byte slab row
+// and the prefix-norm entry (20 B/row instead of the step kernel's 28 B) and
+// the accumulators are written back once at the end.  Blocks never wait for
+// each other: per step, one atomicMax per block into best[s] and a ticket;
+// the last block of step s writes its top-1 and runs the Eq. 4-6 selection
+// of target layer + sel_d (warp_select, as the step kernel), then publishes
+// guidance_ready[s].  Optional layer_ready[s] flags (set by the producer of
+// the gates, e.g. the MoE forward) gate step s: the device-side
+// publisher/subscriber of P:528-533.  Arithmetic (query quantisation, fp64
+// running query norm in the same reduction order, fmaf order over the row,
+// acc + d, acc * r_q * rsqrt(psq)) is the step kernel's, so every output is
+// bit-identical to n calls of fmoe_traj_session_step_select.
+constexpr int kSweepThreads = 256;
+constexpr int kSweepWarps = kSweepThreads / 32;
+
+__device__ __forceinline__ unsigned ld_acquire_u32(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_u32(unsigned* p, unsigned v) {
+  asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ unsigned long long globaltimer_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+
+constexpr int kSweepMaxSteps = 64;
+
+// running query norm of step s from the per-warp partial sums, in the step
+// kernel's order: t = (layer > 0 ? t_prev : 0) + red[0] + ... + red[7]
+__device__ __forceinline__ double sweep_norm(double t_prev, int layer, const double* red) {
+  double t = layer > 0 ? t_prev : 0.0;
+  for (int w = 0; w < kSweepWarps; ++w) t += red[w];
+  return t;
+}
+
+template <class Tag, int R>
+__device__ __forceinline__ void sweep_issue(const StoreView& st, int layer, int gt, int nthr, int n,
+                                            uint4 (&buf)[R], float (&ps)[R]) {
+  const char* slab = static_cast<const char*>(st.maps) + int64_t(layer) * st.cap * 16;
+  const float* psq = st.psq + int64_t(layer) * st.cap;
+#pragma unroll
+  for (int i = 0; i < R; ++i) {
+    const int row = gt + i * nthr;
+    buf[i] = row < n ? ld_stream(slab + int64_t(row) * 16) : make_uint4(0u, 0u, 0u, 0u);
+  }
+#pragma unroll
+  for (int i = 0; i < R; ++i) {
+    const int row = gt + i * nthr;
+    ps[i] = row < n ? __ldcs(psq + row) : 0.f;
+  }
+}
+
+template <class Tag, int R>
+__global__ void __launch_bounds__(kSweepThreads, 4) traj_sweep_kernel(const SweepArgs a) {
+  using ST = StoreT<Tag>;
+  constexpr int EP = ST::kElemsPer16B;
+  __shared__ __align__(16) float qs[kSweepMaxSteps][8];   // query layers (store-dtype values; 16-B rows: E <= 8)
+  __shared__ float rqs[kSweepMaxSteps];
+  __shared__ int valids[kSweepMaxSteps];
+  __shared__ double red[kSweepWarps];
+  __shared__ uint64_t sk[kSweepWarps];
+  __shared__ int s_last, s_abort, s_fin;
+  __shared__ float sel_p[kMaxE];
+  __shared__ int sel_i[kMaxE];
+
+  const StoreView& st = a.st;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int E = st.E;
+  const int n = int(a.n_rows);                      // < 2^31 (the register sweep holds <= 8 rows per thread)
+  const int nthr = int(gridDim.x) * kSweepThreads;
+  const int gt = int(blockIdx.x) * kSweepThreads + tid;
+  const bool flags = a.layer_ready != nullptr;
+  pdl_wait();
+
+  // the first step's store rows are in flight while the queries are staged
+  uint4 buf[R];
+  float ps[R];
+  sweep_issue<Tag, R>(st, a.layer0, gt, nthr, n, buf, ps);
+  float acc[R];
+#pragma unroll
+  for (int i = 0; i < R; ++i) {
+    const int row = gt + i * nthr;
+    acc[i] = (a.layer0 > 0 && row < n) ? __ldcs(a.acc + row) : 0.f;
+  }
+  double qn = a.layer0 > 0 ? a.qn_in[0] : 0.0;
+  if (tid == 0) s_abort = 0;
+
+  // Stage one query layer (thread j < 8 holds entry j: the step kernel's
+  // partial-sum layout, warps 1..7 contribute 0) and its running norm.
+  auto stage = [&](int s) {
+    double part = 0.0;
+    if (tid < 8) {
+      const float v = tid < E ? to_store_value(a.q_layers[int64_t(s) * E + tid], Tag()) : 0.f;
+      qs[s][tid] = v;
+      part = double(v) * double(v);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
+    if (lane == 0) red[warp] = part;
+    __syncthreads();
+    if (tid == 0) {
+      qn = sweep_norm(qn, a.layer0 + s, red);
+      rqs[s] = qn > 0.0 ? float(1.0 / sqrt(qn)) : 0.f;
+      valids[s] = qn > 0.0;
+    }
+    __syncthreads();
+  };
+  if (!flags)   // every layer is already observed: stage them all up front
+    for (int s = 0; s < a.n_steps; ++s) stage(s);
+
+  // top-1 of step f (complete: this block took its last ticket), its Eq. 4-6
+  // selection by warp 0, scratch reset, then guidance_ready[f]
+  auto finalize = [&](int f) {
+    if (warp != 0) return;
+    __threadfence();
+    const uint64_t key = __ldcg(a.best + f);
+    const bool valid = valids[f] != 0;
+    const int64_t id = valid ? key_id(key) : -1;
+    const float score = valid ? key_score(key) : __int_as_float(0x7fc00000);
+    if (lane == 0) {
+      a.out_score[f] = score;
+      a.out_id[f] = id;
+    }
+    const int tgt = a.layer0 + f + a.sel_d;
+    if (a.sel_mask) {
+      const int64_t loc = id - int64_t(a.id_offset);
+      if (tgt >= st.L || id < 0 || loc < 0 || loc >= n) {
+        if (lane == 0) { a.sel_mask[f] = 0ull; a.sel_count[f] = 0; }
+      } else {
+        uint64_t mask;
+        int m;
+        warp_select<Tag>(st, tgt, loc, selection_delta(a.sel_delta, score), a.sel_K, sel_p, sel_i, &mask, &m);
+        if (lane == 0) { a.sel_mask[f] = mask; a.sel_count[f] = m; }
+      }
+    }
+    __syncwarp();
+    if (lane == 0) {
+      a.best[f] = 0ull;
+      a.tickets[f] = 0u;
+      __threadfence();
+      if (a.guidance_ready) st_release_u32(a.guidance_ready + f, 1u);
+    }
+  };
+  unsigned pend_ticket = 0u;   // tid 0: ticket of step pend_s
+  int pend_s = -1;
+
+  for (int s = 0; s < a.n_steps; ++s) {
+    const int layer = a.layer0 + s;
+    if (flags) {
+      if (tid == 0) {
+        const unsigned long long t0 = globaltimer_ns();
+        while (ld_acquire_u32(a.layer_ready + s) == 0u) {
+          __nanosleep(200);
+          if (globaltimer_ns() - t0 > a.timeout_ns) { s_abort = 1; break; }
+        }
+      }
+      __syncthreads();
+      if (s_abort) return;
+      stage(s);
+    }
+    const float rq = rqs[s];
+    const float* qv = qs[s];
+    uint64_t best = 0ull;
+#pragma unroll
+    for (int i = 0; i < R; ++i) {
+      const int row = gt + i * nthr;
+      float x[8];
+      unpack_sess<Tag>(buf[i], x);
+      float d = 0.f;
+#pragma unroll
+      for (int e = 0; e < EP; ++e) d = fmaf(x[e], qv[e], d);
+      acc[i] = acc[i] + d;
+      const float rm = ps[i] > 0.f ? rsqrtf(ps[i]) : 0.f;
+      const float sc = acc[i] * rq * rm;
+      const uint64_t key = row < n ? pack_key(sc, a.id_offset + uint32_t(row)) : 0ull;
+      best = key > best ? key : best;
+    }
+    // the next step's rows load while this step reduces and publishes
+    if (s + 1 < a.n_steps) sweep_issue<Tag, R>(st, layer + 1, gt, nthr, n, buf, ps);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const uint64_t x2 = shfl_u64(best, lane ^ o);
+      best = x2 > best ? x2 : best;
+    }
+    if (lane == 0) sk[warp] = best;
+    __syncthreads();
+    // Ticket of step s is taken here but consumed one step later (tid 0 keeps
+    // it in a register), so the block does not wait for the atomics' round
+    // trip: the last block of step s - 1 finalises it now.
+    uint64_t b = 0ull;
+    if (tid == 0) {
+      for (int w = 0; w < kSweepWarps; ++w) b = b > sk[w] ? b : sk[w];
+      s_last = pend_s >= 0 && pend_ticket == gridDim.x - 1;
+      s_fin = pend_s;
+    }
+    __syncthreads();
+    if (tid == 0) {
+      if (b) atomicMax(a.best + s, static_cast<unsigned long long>(b));
+      __threadfence();
+      pend_ticket = atomicAdd(a.tickets + s, 1u);
+      pend_s = s;
+    }
+    if (s_last) finalize(s_fin);
+  }
+  if (tid == 0) {
+    s_last = pend_s >= 0 && pend_ticket == gridDim.x - 1;
+    s_fin = pend_s;
+  }
+  __syncthreads();
+  if (s_last) finalize(s_fin);
+  pdl_trigger();
+#pragma unroll
+  for (int i = 0; i < R; ++i) {
+    const int row = gt + i * nthr;
+    if (row < n) __stcs(a.acc + row, acc[i]);
+  }
+  if (blockIdx.x == 0 && tid == 0) a.qn_out[0] = qn;
+}
+
+int traj_sweep_rows(int64_t n_rows, int* grid_out) {
+  static int sms = 0;
+  if (!sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  }
+  int64_t grid = int64_t(4) * sms;
+  const int64_t need = (n_rows + kSweepThreads - 1) / kSweepThreads;
+  if (need < grid) grid = need < 1 ? 1 : need;
+  const int64_t rpt = (n_rows + grid * kSweepThreads - 1) / (grid * kSweepThreads);
+  *grid_out = int(grid);
+  return rpt <= 4 ? 4 : (rpt <= 7 ? 7 : (rpt <= 8 ? 8 : 0));   // 0: too many rows for registers
+}
+
+cudaError_t launch_traj_sweep(const SweepArgs& a, cudaStream_t stream) {
+  int grid = 1;
+  const int R = traj_sweep_rows(a.n_rows, &grid);
+  using Fn = void (*)(const SweepArgs);
+  Fn fn = nullptr;
+  if (R == 0) return cudaErrorInvalidValue;
+  if (a.st.bf16) fn = R == 4 ? traj_sweep_kernel<Bf16Tag, 4> : R == 7 ? traj_sweep_kernel<Bf16Tag, 7>
+                                                              : traj_sweep_kernel<Bf16Tag, 8>;
+  else fn = R == 4 ? traj_sweep_kernel<F32Tag, 4> : R == 7 ? traj_sweep_kernel<F32Tag, 7>
+                                                           : traj_sweep_kernel<F32Tag, 8>;
+  count_launch();
+  return launch_pdl(fn, dim3(grid), dim3(kSweepThreads), 0, stream, a);
+}
+
 }  // namespace fmoe

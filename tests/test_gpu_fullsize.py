@@ -150,3 +150,37 @@ def test_c3_insert_batch_of_64_at_capacity(c3):
     e, m = rows_for(sh, victims)
     slot, rep = st.insert(torch.from_numpy(e).cuda(), torch.from_numpy(m).cuda())
     assert slot.cpu().tolist() == victims and rep.cpu().tolist() == victims
+
+
+def test_c2_session_sweep_full_size(c2):
+    """The bench's launch configuration (N = 1M: 592 CTAs, 7 rows per thread in
+    registers): sweep == per-step calls bit for bit; returned scores equal the
+    oracle's for the returned ids; planted queries find their row."""
+    lib, st, sh, N = c2
+    qe, qm, planted = S.queries(sh, SEED + 1, N, 2, device="cuda")
+    L, d = sh.L, 3
+    for x in range(2):
+        ref = st.trajectory_session(1)
+        a = st.trajectory_session(1)
+        try:
+            ql = qm[x:x + 1].permute(1, 0, 2).contiguous()
+            gs, gi, gm, gc = a.sweep(ql[:L - 1], -1.0, d)
+            for ell in range(1, L):
+                tgt = ell - 1 + d
+                if tgt < L:
+                    s, i, m, c = ref.step_select(ql[ell - 1], 1, -1.0, tgt, tgt + 1)
+                    assert torch.equal(m[:, 0], gm[ell - 1]) and torch.equal(c[:, 0], gc[ell - 1])
+                else:
+                    s, i = ref.step(ql[ell - 1], 1)
+                assert torch.equal(i[:, 0], gi[ell - 1]) and torch.equal(s[:, 0], gs[ell - 1]), ell
+                if ell in (1, 2, 16, 31):
+                    pre = qm[x:x + 1, :ell].contiguous()
+                    check_returned_scores(sh, s, i, None, pre, ell, 0.0)
+                    if planted[x] >= 0:
+                        # the planted row scores no higher than the returned top-1
+                        _, m = rows_for(sh, [planted[x].item()])
+                        sp = O.trajectory_scores(O.quantize(pre.cpu().numpy(), "bf16"), O.quantize(m, "bf16"), ell)
+                        assert sp[0, 0] <= s[0, 0].item() + TOL
+        finally:
+            ref.close()
+            a.close()

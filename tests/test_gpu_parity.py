@@ -580,3 +580,94 @@ def test_ablation_variants_match_oracle(setup, variant):
     oh, _ = O.expert_hits(q_maps.double().numpy(), gm.tolist(), sh.K)
     assert hits.cpu().numpy().tolist() == oh
     assert rate == pytest.approx(np.sum(oh) / (B * sh.L * sh.K), abs=0)
+
+
+# ---------------------------------------------------------------- session sweep (n steps, one call)
+def _steps_reference(st, qm, delta, d, ell0=0, n=None):
+    """n calls of step_select (k = 1) from a fresh session, after ell0 plain steps."""
+    L = qm.shape[1]
+    n = L - ell0 if n is None else n
+    ref = st.trajectory_session(qm.shape[0])
+    try:
+        for ell in range(ell0):
+            ref.step(qm[:, ell].contiguous().cuda(), 1)
+        out = []
+        for ell in range(ell0, ell0 + n):
+            lay = qm[:, ell].contiguous().cuda()
+            tgt = ell + d
+            if tgt < L:
+                s, i, m, c = ref.step_select(lay, 1, delta, tgt, tgt + 1)
+            else:
+                s, i = ref.step(lay, 1)
+                m = torch.zeros(qm.shape[0], 1, dtype=torch.int64, device="cuda")
+                c = torch.zeros(qm.shape[0], 1, dtype=torch.int32, device="cuda")
+            out.append((s[:, 0], i[:, 0], m[:, 0], c[:, 0]))
+        return [torch.stack(v) for v in zip(*out)]
+    finally:
+        ref.close()
+
+
+@pytest.mark.parametrize("B,delta", [(1, -1.0), (1, 0.9), (3, -1.0)])
+def test_session_sweep_equals_steps(setup, B, delta):
+    """fmoe_traj_session_sweep = n calls of step_select, bit for bit (fused kernel
+    for B = 1 on 16-byte slab rows -- mixtral_tiny bf16 -- else the per-step
+    path), including a sweep split in three and continued by plain steps; ids
+    follow the Eq. 2 oracle at every prefix."""
+    st, dt, sh = setup["st"], setup["dtype"], setup["shape"]
+    qm = S.queries(sh, 5, setup["N"], B)[1]
+    d, L = 3, sh.L
+    rs, ri, rm, rc = _steps_reference(st, qm, delta, d)
+    ql = qm.permute(1, 0, 2).contiguous().cuda()          # [L][B][E]
+    a = st.trajectory_session(B)
+    try:
+        parts = [(0, 5), (5, 17), (17, L)]
+        got = [a.sweep(ql[b:e], delta, d) for b, e in parts]
+        gs, gi, gm, gc = [torch.cat(v) for v in zip(*got)]
+        assert torch.equal(gi, ri) and torch.equal(gs, rs)
+        assert torch.equal(gm, rm) and torch.equal(gc, rc)
+        with pytest.raises(setup["lib"].FmoeError):       # all L layers consumed
+            a.sweep(ql[:1], delta, d)
+        a.reset()
+        s1, i1, _, _ = a.sweep(ql[:L - 1], delta)           # no selection
+        assert torch.equal(i1, ri[:L - 1]) and torch.equal(s1, rs[:L - 1])
+        s2, i2 = a.step(ql[L - 1], 1)                       # the session state continues
+        assert torch.equal(i2[:, 0], ri[L - 1]) and torch.equal(s2[:, 0], rs[L - 1])
+    finally:
+        a.close()
+    for ell in (1, 2, 9, L):
+        ref = O.trajectory_scores(O.quantize(qm[:, :ell].numpy(), dt), setup["Qm"], ell)
+        check_topk(gs[ell - 1][:, None], gi[ell - 1][:, None], ref, 1)
+
+
+def test_session_sweep_ready_flags(setup):
+    """Device flags: step s waits for layer_ready[s] (set here by DMA copies on
+    another stream after the launch) and publishes guidance_ready[s]; results
+    equal the per-step path.  Flags on a path without the fused kernel fail."""
+    lib, st, sh = setup["lib"], setup["st"], setup["shape"]
+    qm = S.queries(sh, 6, setup["N"], 1)[1]
+    L, d = sh.L, 3
+    ql = qm.permute(1, 0, 2).contiguous().cuda()
+    a = st.trajectory_session(1)
+    ready = torch.zeros(L, dtype=torch.int32, device="cuda")
+    pub = torch.zeros(L, dtype=torch.int32, device="cuda")
+    fused = setup["dtype"] == "bf16" and sh.E <= 8
+    try:
+        if not fused:
+            with pytest.raises(lib.FmoeError):
+                a.sweep(ql, -1.0, d, layer_ready=ready, guidance_ready=pub)
+            return
+        rs, ri, rm, rc = _steps_reference(st, qm, -1.0, d)
+        ones = torch.ones(L, dtype=torch.int32).pin_memory()
+        torch.cuda.synchronize()                            # the zeroed flags are in place
+        side = torch.cuda.Stream()
+        main = torch.cuda.current_stream()
+        gs, gi, gm, gc = a.sweep(ql, -1.0, d, layer_ready=ready, guidance_ready=pub)
+        with torch.cuda.stream(side):
+            for s in range(L):                              # the producer publishes layer by layer
+                ready[s:s + 1].copy_(ones[s:s + 1], non_blocking=True)
+        main.synchronize()
+        side.synchronize()
+        assert pub.cpu().tolist() == [1] * L
+        assert torch.equal(gi, ri) and torch.equal(gs, rs) and torch.equal(gm, rm) and torch.equal(gc, rc)
+    finally:
+        a.close()
