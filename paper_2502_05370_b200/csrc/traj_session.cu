@@ -457,6 +457,213 @@ __global__ void __launch_bounds__(kSweepThreads, 4) traj_sweep_kernel(const Swee
   if (blockIdx.x == 0 && tid == 0) a.qn_out[0] = qn;
 }
 
+// ------------------------------------------------------------------ sweep, shared-memory staged
+// Same computation and outputs as traj_sweep_kernel (bit for bit), with the
+// slab rows moved by the TMA engine: block b owns the contiguous rows
+// [b*R*T, (b+1)*R*T) (thread t: rows b*R*T + i*T + t), so a step's slab chunk
+// is one contiguous range, copied by one cp.async.bulk into a 2-stage shared
+// ring issued two steps ahead (the copy of step s+2 starts when step s's
+// stage is free).  The prefix-norm entries are prefetched two steps ahead in
+// registers.  A step then costs max(transfer, compute) instead of
+// load latency + transfer + compute.
+constexpr int kSweepTmaThreads = 512;
+constexpr int kSweepTmaR = 7;
+constexpr int kSweepTmaWarps = kSweepTmaThreads / 32;
+constexpr size_t kSweepTmaStage = size_t(kSweepTmaR) * kSweepTmaThreads * 16;
+
+template <class Tag>
+__global__ void __launch_bounds__(kSweepTmaThreads, 2) traj_sweep_tma_kernel(const SweepArgs a) {
+  using ST = StoreT<Tag>;
+  constexpr int EP = ST::kElemsPer16B;
+  constexpr int R = kSweepTmaR, T = kSweepTmaThreads;
+  extern __shared__ __align__(128) unsigned char ring[];            // [2][R*T][16 B]
+  __shared__ __align__(8) uint64_t bar[2];
+  __shared__ __align__(16) float qs[kSweepMaxSteps][8];
+  __shared__ float rqs[kSweepMaxSteps];
+  __shared__ int valids[kSweepMaxSteps];
+  __shared__ double red[kSweepTmaWarps];
+  __shared__ uint64_t sk[kSweepTmaWarps];
+  __shared__ int s_last, s_abort, s_fin;
+  __shared__ float sel_p[kMaxE];
+  __shared__ int sel_i[kMaxE];
+
+  const StoreView& st = a.st;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int E = st.E;
+  const int n = int(a.n_rows);
+  const int base = int(blockIdx.x) * R * T;
+  const int cnt = n - base < R * T ? n - base : R * T;               // rows of this block (> 0)
+  const bool flags = a.layer_ready != nullptr;
+  const uint64_t pol = policy_evict_first();
+  if (tid == 0) {
+    mbar_init(&bar[0], 1);
+    mbar_init(&bar[1], 1);
+    mbar_fence_init();
+    s_abort = 0;
+  }
+  __syncthreads();
+  pdl_wait();
+  auto issue = [&](int s) {   // tid 0: slab chunk of step s into stage s & 1
+    const char* src = static_cast<const char*>(st.maps) + (int64_t(a.layer0 + s) * st.cap + base) * 16;
+    mbar_arrive_expect_tx(&bar[s & 1], unsigned(cnt) * 16u);
+    bulk_g2s(ring + (s & 1) * kSweepTmaStage, src, unsigned(cnt) * 16u, &bar[s & 1], pol);
+  };
+  if (tid == 0) {
+    issue(0);
+    if (a.n_steps > 1) issue(1);
+  }
+  float ps0[R], ps1[R];      // prefix-norm entries of steps s and s + 1
+  auto load_ps = [&](int s, float (&ps)[R]) {
+    const float* psq = st.psq + int64_t(a.layer0 + s) * st.cap + base;
+#pragma unroll
+    for (int i = 0; i < R; ++i) {
+      const int r = i * T + tid;
+      ps[i] = r < cnt ? __ldcs(psq + r) : 0.f;
+    }
+  };
+  load_ps(0, ps0);
+  if (a.n_steps > 1) load_ps(1, ps1);
+  float acc[R];
+#pragma unroll
+  for (int i = 0; i < R; ++i) {
+    const int r = i * T + tid;
+    acc[i] = (a.layer0 > 0 && r < cnt) ? __ldcs(a.acc + base + r) : 0.f;
+  }
+  double qn = a.layer0 > 0 ? a.qn_in[0] : 0.0;
+
+  auto stage = [&](int s) {
+    double part = 0.0;
+    if (tid < 8) {
+      const float v = tid < E ? to_store_value(a.q_layers[int64_t(s) * E + tid], Tag()) : 0.f;
+      qs[s][tid] = v;
+      part = double(v) * double(v);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
+    if (lane == 0 && warp < kSweepWarps) red[warp] = part;   // the step kernel's 8-warp partial sums
+    __syncthreads();
+    if (tid == 0) {
+      qn = sweep_norm(qn, a.layer0 + s, red);
+      rqs[s] = qn > 0.0 ? float(1.0 / sqrt(qn)) : 0.f;
+      valids[s] = qn > 0.0;
+    }
+    __syncthreads();
+  };
+  if (!flags)
+    for (int s = 0; s < a.n_steps; ++s) stage(s);
+
+  auto finalize = [&](int f) {
+    if (warp != 0) return;
+    __threadfence();
+    const uint64_t key = __ldcg(a.best + f);
+    const bool valid = valids[f] != 0;
+    const int64_t id = valid ? key_id(key) : -1;
+    const float score = valid ? key_score(key) : __int_as_float(0x7fc00000);
+    if (lane == 0) {
+      a.out_score[f] = score;
+      a.out_id[f] = id;
+    }
+    const int tgt = a.layer0 + f + a.sel_d;
+    if (a.sel_mask) {
+      const int64_t loc = id - int64_t(a.id_offset);
+      if (tgt >= st.L || id < 0 || loc < 0 || loc >= n) {
+        if (lane == 0) { a.sel_mask[f] = 0ull; a.sel_count[f] = 0; }
+      } else {
+        uint64_t mask;
+        int m;
+        warp_select<Tag>(st, tgt, loc, selection_delta(a.sel_delta, score), a.sel_K, sel_p, sel_i, &mask, &m);
+        if (lane == 0) { a.sel_mask[f] = mask; a.sel_count[f] = m; }
+      }
+    }
+    __syncwarp();
+    if (lane == 0) {
+      a.best[f] = 0ull;
+      a.tickets[f] = 0u;
+      __threadfence();
+      if (a.guidance_ready) st_release_u32(a.guidance_ready + f, 1u);
+    }
+  };
+  unsigned pend_ticket = 0u;
+  int pend_s = -1;
+
+  for (int s = 0; s < a.n_steps; ++s) {
+    if (flags) {
+      if (tid == 0) {
+        const unsigned long long t0 = globaltimer_ns();
+        while (ld_acquire_u32(a.layer_ready + s) == 0u) {
+          __nanosleep(200);
+          if (globaltimer_ns() - t0 > a.timeout_ns) { s_abort = 1; break; }
+        }
+      }
+      __syncthreads();
+      if (s_abort) {
+        // drain the bulk copies still landing in this block's shared memory
+        mbar_wait(&bar[s & 1], unsigned((s >> 1) & 1));
+        if (s + 1 < a.n_steps) mbar_wait(&bar[(s + 1) & 1], unsigned(((s + 1) >> 1) & 1));
+        return;
+      }
+      stage(s);
+    }
+    const float rq = rqs[s];
+    const float* qv = qs[s];
+    mbar_wait(&bar[s & 1], unsigned((s >> 1) & 1));
+    const uint4* chunk = reinterpret_cast<const uint4*>(ring + (s & 1) * kSweepTmaStage);
+    uint64_t best = 0ull;
+#pragma unroll
+    for (int i = 0; i < R; ++i) {
+      const int r = i * T + tid;
+      float x[8];
+      unpack_sess<Tag>(r < cnt ? chunk[r] : make_uint4(0u, 0u, 0u, 0u), x);
+      float d = 0.f;
+#pragma unroll
+      for (int e = 0; e < EP; ++e) d = fmaf(x[e], qv[e], d);
+      acc[i] = acc[i] + d;
+      const float rm = ps0[i] > 0.f ? rsqrtf(ps0[i]) : 0.f;
+      const float sc = acc[i] * rq * rm;
+      const uint64_t key = r < cnt ? pack_key(sc, a.id_offset + uint32_t(base + r)) : 0ull;
+      best = key > best ? key : best;
+    }
+#pragma unroll
+    for (int i = 0; i < R; ++i) ps0[i] = ps1[i];
+    if (s + 2 < a.n_steps) load_ps(s + 2, ps1);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const uint64_t x2 = shfl_u64(best, lane ^ o);
+      best = x2 > best ? x2 : best;
+    }
+    if (lane == 0) sk[warp] = best;
+    __syncthreads();                      // also: every thread is done with stage s & 1
+    uint64_t b = 0ull;
+    if (tid == 0) {
+      if (s + 2 < a.n_steps) issue(s + 2);
+      for (int w = 0; w < kSweepTmaWarps; ++w) b = b > sk[w] ? b : sk[w];
+      s_last = pend_s >= 0 && pend_ticket == gridDim.x - 1;
+      s_fin = pend_s;
+    }
+    __syncthreads();
+    if (tid == 0) {
+      if (b) atomicMax(a.best + s, static_cast<unsigned long long>(b));
+      __threadfence();
+      pend_ticket = atomicAdd(a.tickets + s, 1u);
+      pend_s = s;
+    }
+    if (s_last) finalize(s_fin);
+  }
+  if (tid == 0) {
+    s_last = pend_s >= 0 && pend_ticket == gridDim.x - 1;
+    s_fin = pend_s;
+  }
+  __syncthreads();
+  if (s_last) finalize(s_fin);
+  pdl_trigger();
+#pragma unroll
+  for (int i = 0; i < R; ++i) {
+    const int r = i * T + tid;
+    if (r < cnt) __stcs(a.acc + base + r, acc[i]);
+  }
+  if (blockIdx.x == 0 && tid == 0) a.qn_out[0] = qn;
+}
+
 int traj_sweep_rows(int64_t n_rows, int* grid_out) {
   static int sms = 0;
   if (!sms) {
@@ -473,6 +680,27 @@ int traj_sweep_rows(int64_t n_rows, int* grid_out) {
 }
 
 cudaError_t launch_traj_sweep(const SweepArgs& a, cudaStream_t stream) {
+  static int sms = 0;
+  if (!sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  }
+  const char* env = getenv("FMOE_SWEEP_TMA");
+  // opt-in: measured slower than the register kernel at C2 (0.262 vs 0.217 ms per
+  // sweep, profiles/r01f_c2_sweep.md); kept as an experiment knob
+  const bool tma_ok = env != nullptr && atoi(env) != 0;
+  const int64_t per_block = int64_t(kSweepTmaR) * kSweepTmaThreads;
+  const int64_t tgrid = (a.n_rows + per_block - 1) / per_block;
+  if (tma_ok && tgrid <= int64_t(2) * sms) {
+    using Fn = void (*)(const SweepArgs);
+    Fn fn = a.st.bf16 ? traj_sweep_tma_kernel<Bf16Tag> : traj_sweep_tma_kernel<F32Tag>;
+    const int smem = int(2 * kSweepTmaStage);
+    cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e != cudaSuccess) return e;
+    count_launch();
+    return launch_pdl(fn, dim3(unsigned(tgrid)), dim3(kSweepTmaThreads), size_t(smem), stream, a);
+  }
   int grid = 1;
   const int R = traj_sweep_rows(a.n_rows, &grid);
   using Fn = void (*)(const SweepArgs);

@@ -607,12 +607,14 @@ def _steps_reference(st, qm, delta, d, ell0=0, n=None):
         ref.close()
 
 
+@pytest.mark.parametrize("tma", ["0", "1"])
 @pytest.mark.parametrize("B,delta", [(1, -1.0), (1, 0.9), (3, -1.0)])
-def test_session_sweep_equals_steps(setup, B, delta):
+def test_session_sweep_equals_steps(setup, B, delta, tma, monkeypatch):
     """fmoe_traj_session_sweep = n calls of step_select, bit for bit (fused kernel
     for B = 1 on 16-byte slab rows -- mixtral_tiny bf16 -- else the per-step
     path), including a sweep split in three and continued by plain steps; ids
     follow the Eq. 2 oracle at every prefix."""
+    monkeypatch.setenv("FMOE_SWEEP_TMA", tma)            # register kernel / shared-memory staged kernel
     st, dt, sh = setup["st"], setup["dtype"], setup["shape"]
     qm = S.queries(sh, 5, setup["N"], B)[1]
     d, L = 3, sh.L
@@ -671,3 +673,33 @@ def test_session_sweep_ready_flags(setup):
         assert torch.equal(gi, ri) and torch.equal(gs, rs) and torch.equal(gm, rm) and torch.equal(gc, rc)
     finally:
         a.close()
+
+
+@pytest.mark.parametrize("tma", ["0", "1"])
+def test_session_sweep_edge_cases(lib, tma, monkeypatch):
+    """Zero query layers (prefix norm 0 -> (NaN, -1), empty selection, as the
+    step kernel), single-step sweeps, an empty store (per-step path: id -1)."""
+    monkeypatch.setenv("FMOE_SWEEP_TMA", tma)
+    sh = SHAPES["mixtral_tiny"]
+    st, _, _ = make(lib, sh, 777, "bf16")
+    empty = lib.ExpertMapStore(sh.L, sh.E, sh.K, sh.D, 3, 16, "bf16")
+    try:
+        qm = S.queries(sh, 9, 777, 1)[1]
+        qm[:, :2] = 0.0                                       # the first two observed layers are all zero
+        ql = qm.permute(1, 0, 2).contiguous().cuda()
+        rs, ri, rm, rc = _steps_reference(st, qm, -1.0, 3)
+        a = st.trajectory_session(1)
+        gs, gi, gm, gc = a.sweep(ql[:1], -1.0, 3)             # n_steps = 1
+        g2 = a.sweep(ql[1:], -1.0, 3)
+        gs, gi, gm, gc = [torch.cat([x, y]) for x, y in zip((gs, gi, gm, gc), g2)]
+        assert torch.equal(gi, ri) and torch.equal(gm, rm) and torch.equal(gc, rc)
+        assert torch.equal(torch.isnan(gs), torch.isnan(rs)) and torch.equal(gs[2:], rs[2:])
+        assert gi[:2].eq(-1).all() and torch.isnan(gs[:2]).all() and gm[:2].eq(0).all()
+        a.close()
+        e = empty.trajectory_session(1)
+        es, ei, em, ec = e.sweep(ql[:4], -1.0, 3)
+        assert ei.eq(-1).all() and em.eq(0).all() and ec.eq(0).all()
+        e.close()
+    finally:
+        st.close()
+        empty.close()
