@@ -59,6 +59,13 @@ def test_binding_loads_and_reports_errors_without_gpu(libpath):
     assert b"d < L" in fm._lib.fmoe_last_error()
     # null store -> INVALID_ARG
     assert fm._lib.fmoe_search_semantic(None, 1, None, 1, None, None, None) == 1
+    # expert hits: K > E, E > 64, T < 1 are rejected on the host; B = 0 is a no-op
+    assert fm._lib.fmoe_expert_hits(2, 3, 8, 9, None, None, None, None, 0, None) == 1
+    assert fm._lib.fmoe_expert_hits(2, 3, 65, 2, None, None, None, None, 0, None) == 1
+    assert fm._lib.fmoe_expert_hits(2, 0, 8, 2, None, None, None, None, 0, None) == 1
+    assert fm._lib.fmoe_expert_hits(0, 3, 8, 2, None, None, None, None, 0, None) == 0
+    # session sweep: null session / outputs -> INVALID_ARG before any device work
+    assert fm._lib.fmoe_traj_session_sweep(None, None, 1, None, None, -1.0, 3, None, None, None, None, None) == 1
     assert fm._lib.fmoe_kernel_launch_count() == 0
 
 
