@@ -110,6 +110,8 @@ def algorithmic_bytes(cfg, N, traj_mode="stateless", use_cos=False):
     B = cfg["B"]
     if cfg.get("kind") == "blend":
         traj = {ell: N * (sh.D + ell * sh.E) * s for ell in cfg["ells"]}
+        if use_cos:   # fmoe_search_blend_cos: map prefix + the B cached cosines per row
+            traj = {ell: N * (ell * sh.E * s + 4 * B) for ell in cfg["ells"]}
     elif traj_mode == "sweep" and use_sweep(cfg):
         # slab + prefix-norm row per step; the running dots live in registers and
         # are written back once (charged to the last step)
@@ -208,6 +210,13 @@ class Step:
         else:
             self.fm.fmoe_search_semantic(h, q_emb, k, out_s, out_i)
 
+    def blend(self, h, q_emb, pre, ell, k, out_s, out_i):
+        # the semantic half from this iteration's semantic search (same queries, same store)
+        if self.cos is not None:
+            self.fm.fmoe_search_blend_cos(h, self.cos, self.stride, pre, ell, -1.0, k, out_s, out_i)
+        else:
+            self.fm.fmoe_search_blend(h, q_emb, pre, ell, -1.0, k, out_s, out_i)
+
     def insert(self, h, ne, nm):
         if self.cos is not None:
             self.fm.fmoe_store_insert_cos(h, ne, nm, self.cos, self.stride, None, None)
@@ -247,7 +256,7 @@ class Step:
             # blended searches (RDY weighting, w = d/L) at the configured prefixes
             for ell in cfg["ells"]:
                 pre, _ = q_maps[ell - 1]
-                rec(f"traj{ell}", lambda: fm.fmoe_search_blend(h, q_emb, pre, ell, -1.0, k, out_s, out_i))
+                rec(f"traj{ell}", lambda: self.blend(h, q_emb, pre, ell, k, out_s, out_i))
                 tgt = ell - 1 + d
                 if tgt < L:
                     top_i = out_i[:, 0].contiguous()
@@ -332,7 +341,7 @@ class HostStep(Step):
         if cfg.get("kind") == "blend":
             for ell in cfg["ells"]:
                 pre, _ = q_maps[ell - 1]
-                fm.fmoe_search_blend(h, q_emb, pre, ell, -1.0, k, out_s, out_i)
+                self.blend(h, q_emb, pre, ell, k, out_s, out_i)
                 tgt = ell - 1 + d
                 if tgt < L:
                     top_s, top_i = self.top1(out_s, out_i)
@@ -694,6 +703,9 @@ def main():
                    "k": cfg["k"], "store_dtype": cfg["dtype"], "searches_per_step": searches,
                    "insert": ("RDY semantic half reused from the step's semantic search (fmoe_store_insert_cos)"
                               if args.cos and world == 1 else "full RDY scan"),
+                   **({"blend": "semantic half reused from the step's semantic search (fmoe_search_blend_cos)"
+                       if args.cos and world == 1 and cfg["B"] * cfg["N"] * 4 <= (4 << 30)
+                       else "full blended scan (embeddings re-read)"} if cfg.get("kind") == "blend" else {}),
                    "trajectory": ("stateless: one search over the whole prefix per ell"
                                   if args.traj == "stateless" or world > 1 else
                                   "session sweep: the L-1 incremental steps of the request in one call "

@@ -169,6 +169,19 @@ fmoe_status fmoe_search_blend(const fmoe_store* store, int64_t B, const float* q
                               const float* q_prefix, int32_t ell, float w_sem, int32_t k,
                               float* out_score, int64_t* out_id, void* stream);
 
+/* fmoe_search_blend with the semantic half taken from the cosines a
+ * semantic search of the same queries wrote (fmoe_search_semantic_cos:
+ * sem_cos [B][cos_stride], cos_stride >= store size) instead of re-reading
+ * the embeddings (P:544-551 blend): S = w*sem_cos +
+ * (1-w)*S_traj(ell), w = w_sem (< 0 => d/L), 0 <= w < 1.  Equal to
+ * fmoe_search_blend(q_emb, ...) when sem_cos came from
+ * fmoe_search_semantic_cos(q_emb) on the unchanged store.  Query validity is
+ * judged on the trajectory prefix only (a zero-norm embedding was reported by
+ * the semantic search).  Pointers device or host, caller-owned. */
+fmoe_status fmoe_search_blend_cos(const fmoe_store* store, int64_t B, const float* sem_cos, int64_t cos_stride,
+                                  const float* q_prefix, int32_t ell, float w_sem, int32_t k, float* out_score,
+                                  int64_t* out_id, void* stream);
+
 /* ---- incremental trajectory search ---------------- */
 
 /* A session follows B requests through the layers of one inference iteration:

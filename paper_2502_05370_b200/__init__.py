@@ -57,6 +57,7 @@ def _load():
         "fmoe_search_semantic": (I32, [P, I64, P, I32, P, P, P]),
         "fmoe_search_trajectory": (I32, [P, I64, P, I32, I32, P, P, P]),
         "fmoe_search_blend": (I32, [P, I64, P, P, I32, F, I32, P, P, P]),
+        "fmoe_search_blend_cos": (I32, [P, I64, P, I64, P, I32, F, I32, P, P, P]),
         "fmoe_select_experts": (I32, [P, I64, P, P, F, I32, I32, P, P, P]),
         "fmoe_traj_session_create": (I32, [P, I64, ctypes.POINTER(P)]),
         "fmoe_traj_session_step": (I32, [P, P, I32, P, P, P]),
@@ -84,7 +85,7 @@ _lib = _load()
 ABI_SYMBOLS = ("fmoe_store_create", "fmoe_store_destroy", "fmoe_store_size", "fmoe_store_get_config",
                "fmoe_store_insert", "fmoe_store_insert_cos", "fmoe_search_semantic_cos", "fmoe_store_read",
                "fmoe_store_write", "fmoe_resolve_victims", "fmoe_search_semantic", "fmoe_search_trajectory",
-               "fmoe_search_blend", "fmoe_select_experts", "fmoe_traj_session_create", "fmoe_traj_session_step",
+               "fmoe_search_blend", "fmoe_search_blend_cos", "fmoe_select_experts", "fmoe_traj_session_create", "fmoe_traj_session_step",
                "fmoe_traj_session_step_select", "fmoe_traj_session_sweep",
                "fmoe_traj_session_reset", "fmoe_traj_session_destroy", "fmoe_topk_merge",
                "fmoe_prefetch_plan", "fmoe_eviction_order", "fmoe_expert_hits", "fmoe_status_string",
@@ -176,6 +177,11 @@ def fmoe_search_trajectory(h, q_prefix, ell, k, out_score, out_id, stream=None):
 def fmoe_search_blend(h, q_emb, q_prefix, ell, w_sem, k, out_score, out_id, stream=None):
     _check(_lib.fmoe_search_blend(h, q_emb.shape[0], _ptr(_f32(q_emb)), _ptr(_f32(q_prefix)), ell, w_sem, k,
                                   _ptr(out_score), _ptr(out_id), _stream(stream)))
+
+
+def fmoe_search_blend_cos(h, sem_cos, cos_stride, q_prefix, ell, w_sem, k, out_score, out_id, stream=None):
+    _check(_lib.fmoe_search_blend_cos(h, q_prefix.shape[0], _ptr(sem_cos), cos_stride, _ptr(q_prefix), ell, w_sem, k,
+                                      _ptr(out_score), _ptr(out_id), _stream(stream)))
 
 
 def fmoe_select_experts(h, map_id, score, delta, layer_begin, layer_end, out_mask, out_count, stream=None):

@@ -857,6 +857,36 @@ fmoe_status fmoe_traj_session_step_select(fmoe_traj_session* ss, const float* q_
   return session_step(ss, q_layer, k, out_score, out_id, sel, stream);
 }
 
+fmoe_status fmoe_search_blend_cos(const fmoe_store* st, int64_t B, const float* sem_cos, int64_t cos_stride,
+                                  const float* q_prefix, int32_t ell, float w_sem, int32_t k, float* out_score,
+                                  int64_t* out_id, void* stream) {
+  if (!st) return fail(FMOE_ERR_INVALID_ARG, "null store");
+  if (B < 0) return fail(FMOE_ERR_INVALID_ARG, "B < 0");
+  if (k < 1 || k > FMOE_MAX_K) return fail(FMOE_ERR_INVALID_ARG, "k must be in [1, 64]");
+  if (!out_score && !out_id) return fail(FMOE_ERR_INVALID_ARG, "no output");
+  if (!q_prefix || ell < 1 || ell > st->cfg.L) return fail(FMOE_ERR_INVALID_ARG, "need q_prefix and 1 <= ell <= L");
+  const float w = w_sem < 0.f ? float(st->cfg.d) / float(st->cfg.L) : w_sem;
+  if (!(w >= 0.f && w < 1.f)) return fail(FMOE_ERR_INVALID_ARG, "0 <= w_sem < 1 (w = 1: the semantic search itself)");
+  if (B > 0 && (!sem_cos || cos_stride < st->n)) return fail(FMOE_ERR_INVALID_ARG, "sem_cos [B][cos_stride >= n]");
+  if (B == 0) return FMOE_OK;
+  DeviceGuard g(st->device);
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  Staging S(s, st->device);
+  const int E = st->cfg.E;
+  const float* dp = S.in(q_prefix, size_t(B) * ell * E);
+  const float* dc = S.in(sem_cos, size_t(B) * cos_stride);
+  float* ds = S.out(out_score, size_t(B) * k);
+  int64_t* di = S.out(out_id, size_t(B) * k);
+  CosArgs cos;
+  cos.in = dc;
+  cos.stride = cos_stride;
+  fmoe_status r = S.check();
+  if (r == FMOE_OK)
+    r = run_search(st, B, nullptr, dp, int64_t(ell) * E, ell, w, k, st->n, uint32_t(st->cfg.id_offset), s, ds, di,
+                   nullptr, true, cos);
+  return S.finish(r);
+}
+
 fmoe_status fmoe_traj_session_sweep(fmoe_traj_session* ss, const float* q_layers, int32_t n_steps,
                                     float* out_score, int64_t* out_id, float delta, int32_t sel_d,
                                     uint64_t* out_mask, int32_t* out_count, const uint32_t* layer_ready,

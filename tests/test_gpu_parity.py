@@ -703,3 +703,31 @@ def test_session_sweep_edge_cases(lib, tma, monkeypatch):
     finally:
         st.close()
         empty.close()
+
+
+@pytest.mark.parametrize("B,k", [(1, 1), (3, 8), (64, 8)])
+@pytest.mark.parametrize("ell,w", [(5, -1.0), (31, 0.3)])
+def test_blend_cos_equals_blend(setup, B, k, ell, w):
+    """fmoe_search_blend_cos (semantic half from fmoe_search_semantic_cos's
+    cosines) = fmoe_search_blend bit for bit on the test shapes (GEMV for
+    B <= 4, tcgen05 for B = 64 on bf16), and = the oracle blend."""
+    lib, st, sh, dt = setup["lib"], setup["st"], setup["shape"], setup["dtype"]
+    N, ell = setup["N"], min(ell, sh.L)
+    qe, qm, _ = S.queries(sh, 7, N, B)
+    qp = qm[:, :ell].contiguous()
+    stride = (N + 3) // 4 * 4
+    cos = torch.empty(B, stride, device="cuda")
+    s0 = torch.empty(B, k, device="cuda")
+    i0 = torch.empty(B, k, dtype=torch.int64, device="cuda")
+    lib.fmoe_search_semantic_cos(st._h, qe.cuda(), k, s0, i0, cos, stride)
+    s2 = torch.empty(B, k, device="cuda")
+    i2 = torch.empty(B, k, dtype=torch.int64, device="cuda")
+    lib.fmoe_search_blend_cos(st._h, cos, stride, qp.cuda(), ell, w, k, s2, i2)
+    gs, gi = st.search_blend(qe.cuda(), qp.cuda(), ell, w, k)
+    assert torch.equal(gi, i2) and torch.equal(gs, s2)
+    wv = float(np.float32(3 / sh.L)) if w < 0 else float(np.float32(w))
+    ref = (wv * O.semantic_scores(O.quantize(qe.numpy(), dt), setup["Qe"])
+           + (1 - wv) * O.trajectory_scores(O.quantize(qp.numpy(), dt), setup["Qm"], ell))
+    check_topk(s2, i2, ref, k)
+    with pytest.raises(lib.FmoeError):                       # w = 1 is the semantic search itself
+        lib.fmoe_search_blend_cos(st._h, cos, stride, qp.cuda(), ell, 1.0, k, s2, i2)
