@@ -201,8 +201,12 @@ class Step:
         # the iteration's new context carries the embedding its semantic search used
         n = len(st)
         self.stride = (n + 3) // 4 * 4
+        # (B x N fp32; C5: 256 x 16M = 16.4 GB next to the 148 GB store -- allocated
+        # when it leaves >= 6 GB of the device free)
+        cos_b = cfg["B"] * self.stride * 4
+        free = torch.cuda.mem_get_info(st.device)[0] if use_cos else 0
         self.cos = (torch.empty(cfg["B"], self.stride, device=st.device)
-                    if use_cos and cfg["B"] * self.stride * 4 <= (4 << 30) else None)
+                    if use_cos and cos_b + (6 << 30) <= free else None)
 
     def semantic(self, h, q_emb, k, out_s, out_i):
         if self.cos is not None:
@@ -580,6 +584,12 @@ def run_fmoe(args, cfg, rank, world, local_rank):
         for qe, pre, ne, nm in qs:
             hq.append((qe.cpu().pin_memory(), [(p.cpu().pin_memory(), l.cpu().pin_memory()) for p, l in pre],
                        ne.cpu().pin_memory(), nm.cpu().pin_memory()))
+        if getattr(step, "cos", None) is not None:
+            # the host-buffer step allocates its own cosine side output (C5: 16 GB)
+            graphs.clear()
+            step.cos = None
+            torch.cuda.synchronize()
+            torch.cuda.empty_cache()
         hstep = HostStep(fm, st, cfg, args.traj, args.cos)
         for w in range(2):
             hstep.run(*hq[w % pool])
@@ -601,7 +611,17 @@ def run_fmoe(args, cfg, rank, world, local_rank):
             fm.fmoe_traj_session_destroy(obj.sess)
     st.close()
     return dict(value=value, ms_step=ms_step, roofline=roofline, e2e=e2e, clocks=clocks, launches=launches,
-                N_local=N_local)
+                N_local=N_local, cos=getattr(step, "cos", None) is not None)
+
+
+def cos_keys(cfg, cos):
+    """What the step reused from the semantic search's B x N cosine side output."""
+    out = {"insert": "RDY semantic half reused from the step's semantic search (fmoe_store_insert_cos)"
+                     if cos else "full RDY scan"}
+    if cfg.get("kind") == "blend":
+        out["blend"] = ("semantic half reused from the step's semantic search (fmoe_search_blend_cos)"
+                        if cos else "full blended scan (embeddings re-read)")
+    return out
 
 
 def sh_L(cfg):
@@ -703,9 +723,6 @@ def main():
                    "k": cfg["k"], "store_dtype": cfg["dtype"], "searches_per_step": searches,
                    "insert": ("RDY semantic half reused from the step's semantic search (fmoe_store_insert_cos)"
                               if args.cos and world == 1 else "full RDY scan"),
-                   **({"blend": "semantic half reused from the step's semantic search (fmoe_search_blend_cos)"
-                       if args.cos and world == 1 and cfg["B"] * cfg["N"] * 4 <= (4 << 30)
-                       else "full blended scan (embeddings re-read)"} if cfg.get("kind") == "blend" else {}),
                    "trajectory": ("stateless: one search over the whole prefix per ell"
                                   if args.traj == "stateless" or world > 1 else
                                   "session sweep: the L-1 incremental steps of the request in one call "
@@ -750,7 +767,8 @@ def main():
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(res["ms_step"], 4),
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": cfg["dtype"],
             "data": "synthetic (seeded clustered embeddings + softmax gate maps, fmoe_synth)",
-            "config": dict(base_config, parallelism=f"store sharded over {world} GPU(s)" if world > 1 else "1 GPU"),
+            "config": dict(base_config, parallelism=f"store sharded over {world} GPU(s)" if world > 1 else "1 GPU",
+                           **cos_keys(cfg, res["cos"])),
             "roofline": res["roofline"], "cpu_baseline": cpu, "e2e": res["e2e"], "clocks": res["clocks"],
             "gpu_launches": res["launches"]}
     print(json.dumps(line))

@@ -705,7 +705,7 @@ def test_session_sweep_edge_cases(lib, tma, monkeypatch):
         empty.close()
 
 
-@pytest.mark.parametrize("B,k", [(1, 1), (3, 8), (64, 8)])
+@pytest.mark.parametrize("B,k", [(1, 1), (3, 8), (64, 8), (256, 8), (300, 3)])
 @pytest.mark.parametrize("ell,w", [(5, -1.0), (31, 0.3)])
 def test_blend_cos_equals_blend(setup, B, k, ell, w):
     """fmoe_search_blend_cos (semantic half from fmoe_search_semantic_cos's
