@@ -255,8 +255,11 @@ __global__ void __launch_bounds__(32) resolve_kernel(int nrep, int kk, const uin
   pdl_wait();
   if (gate && *gate == 0) return;
   __shared__ int64_t claimed[kMaxK];
+  __shared__ uint64_t ks[kMaxK * kMaxK];   // the candidate lists, staged once (independent, coalesced loads)
   const int lane = threadIdx.x;
   bool need = false;
+  for (int i = lane; i < nrep * kk; i += 32) ks[i] = keys[i];
+  __syncwarp();
   for (int x = lane; x < x0; x += 32) {
     slots_all[x] = first_append_slot + x;
     if (out_slot) out_slot[x] = int64_t(id_offset) + first_append_slot + x;
@@ -268,7 +271,7 @@ __global__ void __launch_bounds__(32) resolve_kernel(int nrep, int kk, const uin
       const int c = c0 + lane;
       int64_t loc = -1;
       if (c < kk) {
-        const uint64_t key = keys[int64_t(j) * kk + c];
+        const uint64_t key = ks[j * kk + c];
         if (key != 0ull) {
           loc = key_id(key);
           for (int i = 0; i < j; ++i)
@@ -282,7 +285,7 @@ __global__ void __launch_bounds__(32) resolve_kernel(int nrep, int kk, const uin
       }
     }
     // exhausted while the list was full: the victim may lie beyond the kk keys
-    if (best < 0 && k_full > kk && keys[int64_t(j) * kk + kk - 1] != 0ull) need = true;
+    if (best < 0 && k_full > kk && ks[j * kk + kk - 1] != 0ull) need = true;
     if (lane == 0) {
       claimed[j] = best >= 0 ? best : -2;
       slots_all[x0 + j] = best;
