@@ -56,9 +56,11 @@ WORKLOADS = {
 def parse():
     p = argparse.ArgumentParser()
     p.add_argument("--gpus", type=int, default=1)
-    p.add_argument("--steps", type=int, default=200)
+    p.add_argument("--steps", type=int, default=20)
     p.add_argument("--warmup", type=int, default=3)
-    p.add_argument("--config", default="C2", choices=sorted(WORKLOADS))
+    # default: C5, the configuration BASELINE.json's north-star target names
+    # (16M maps, batch 256, bf16 fits one B200); C1..C4 are parity/bench cases
+    p.add_argument("--config", default="C5", choices=sorted(WORKLOADS))
     p.add_argument("--impl", default="fmoe", choices=["fmoe", "reference"])
     p.add_argument("--traj", default="sweep", choices=["sweep", "session", "stateless"],
                    help="trajectory steps: one session-sweep call (B = 1, k = 1: every step in one launch, running "
@@ -553,12 +555,38 @@ def run_fmoe(args, cfg, rank, world, local_rank):
     scan_bytes = sem_b + sum(traj_b.values()) + rdy_b
     peaks = load_peaks()
     # the dominant kernel of the step: the semantic scan (one launch per step at B <= 4;
-    # prep + scan + merge at B >= 5), algorithmic bytes per launch / its mean event time
+    # prep + scan + merge (+ exact re-rank) at B >= 5), algorithmic bytes (or FLOPs) per
+    # launch / its mean event time.  Bound by arithmetic intensity: the scan does
+    # 2*B FLOPs per stored element of s bytes (AI = B FLOP/B for bf16); above the
+    # ridge (sustained bf16 peak / HBM copy bandwidth) it is a tensor-core roofline.
     sem_ms = kind_ms.get("semantic", 0.0)
+    sh_ = cfg["shape"]
+    s_el = 2 if cfg["dtype"] == "bf16" else 4
+    sem_store_b = N_local * sh_.D * s_el                      # the embeddings streamed once
+    sem_flops = 2.0 * cfg["B"] * N_local * sh_.D
+    ai = sem_flops / sem_store_b
+    ridge = peaks["bf16_tflops_sustained"] * 1e12 / (peaks["hbm_gbs"] * 1e9)
     achieved = sem_b / (sem_ms * 1e-3) / 1e9 if sem_ms > 0 else 0.0
+    tflops = sem_flops / (sem_ms * 1e-3) / 1e12 if sem_ms > 0 else 0.0
     agg = scan_bytes / (scan_ms * 1e-3) / 1e9 if scan_ms > 0 else 0.0
-    roofline = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peaks["hbm_gbs"], "unit": "GB/s",
-                "frac": round(achieved / peaks["hbm_gbs"], 4), "traffic": measured_traffic(args.config),
+    tensor = cfg["dtype"] == "bf16" and cfg["B"] >= 5 and ai > ridge
+    traffic = measured_traffic(args.config)
+    if tensor:
+        head = {"bound": "tensor", "achieved": round(tflops, 1), "peak": peaks["bf16_tflops_sustained"],
+                "unit": "TFLOP/s", "frac": round(tflops / peaks["bf16_tflops_sustained"], 4),
+                "traffic": traffic.get("bytes") if isinstance(traffic, dict) else traffic,
+                "peak_kind": "bf16 dense, sustained (kernel timed inside a long step), MEASURED_PEAKS.json",
+                "algorithmic_flops_per_launch": sem_flops,
+                "hbm": {"achieved": round(achieved, 1), "peak": peaks["hbm_gbs"], "unit": "GB/s",
+                        "frac": round(achieved / peaks["hbm_gbs"], 4)}}
+    else:
+        head = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peaks["hbm_gbs"], "unit": "GB/s",
+                "frac": round(achieved / peaks["hbm_gbs"], 4),
+                "traffic": traffic.get("bytes") if isinstance(traffic, dict) else traffic,
+                "peak_kind": "HBM copy bandwidth, MEASURED_PEAKS.json"}
+    roofline = dict(head, **{
+                "arithmetic_intensity": round(ai, 2), "ridge": round(ridge, 1),
+                "ncu": traffic if isinstance(traffic, dict) else None,
                 "kernel": "semantic scan (Eq. 1 + fused top-k), the largest share of the step; CUDA events "
                           "around each call on the launching stream, eager timed pass",
                 "algorithmic_bytes_per_launch": sem_b,
@@ -573,18 +601,20 @@ def run_fmoe(args, cfg, rank, world, local_rank):
                     "rdy_insert": {"ms": round(kind_ms.get("rdy_insert", 0), 4), "GBps": round(rdy_b / kind_ms.get("rdy_insert", 1) / 1e6, 1)},
                     **({"traj_ell31_GBps": round(traj_b[sh_L(cfg) - 1] / kind_ms[f"traj{sh_L(cfg) - 1}"] / 1e6, 1)}
                        if f"traj{sh_L(cfg) - 1}" in kind_ms else {}),
-                }}
+                }})
     # strong scaling: a search covers the whole (sharded) store, so the job
     # completes `searches` per step whatever the number of ranks
     value = searches / (ms_step * 1e-3)
 
     e2e = None
+    used_cos = getattr(step, "cos", None) is not None
     if not args.no_e2e and world == 1:
         hq = []
         for qe, pre, ne, nm in qs:
             hq.append((qe.cpu().pin_memory(), [(p.cpu().pin_memory(), l.cpu().pin_memory()) for p, l in pre],
                        ne.cpu().pin_memory(), nm.cpu().pin_memory()))
-        if getattr(step, "cos", None) is not None:
+        used_cos = getattr(step, "cos", None) is not None   # what the timed step ran (read before clearing)
+        if used_cos:
             # the host-buffer step allocates its own cosine side output (C5: 16 GB)
             graphs.clear()
             step.cos = None
@@ -611,7 +641,7 @@ def run_fmoe(args, cfg, rank, world, local_rank):
             fm.fmoe_traj_session_destroy(obj.sess)
     st.close()
     return dict(value=value, ms_step=ms_step, roofline=roofline, e2e=e2e, clocks=clocks, launches=launches,
-                N_local=N_local, cos=getattr(step, "cos", None) is not None)
+                N_local=N_local, cos=used_cos)
 
 
 def cos_keys(cfg, cos):
@@ -641,15 +671,20 @@ def load_peaks():
     p = os.path.join(ROOT, "MEASURED_PEAKS.json")
     if os.path.exists(p):
         d = json.load(open(p))
-        return {"hbm_gbs": d["hbm_gbs"], "bf16_tflops": d.get("bf16_tflops"), "source": "MEASURED_PEAKS.json (measured)"}
-    return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "source": "B200_PROFILING.md fallback"}
+        return {"hbm_gbs": d["hbm_gbs"], "bf16_tflops": d.get("bf16_tflops"),
+                "bf16_tflops_sustained": d.get("bf16_tflops_sustained", d.get("bf16_tflops")),
+                "source": "MEASURED_PEAKS.json (measured)"}
+    return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0,
+            "source": "B200_PROFILING.md fallback"}
 
 
 # ------------------------------------------------------------------ the oracle arm (CPU)
-def oracle_step_sample(cfg, seed, n_sample, budget_s=15.0, max_steps=50):
-    """Times the oracle (as it stands) on one step of the workload against a
-    bounded sample of n_sample stored rows; returns searches/s scaled to the
-    full N (the scans are linear in N)."""
+def oracle_step_sample(cfg, seed, n_sample, steps=None, warmup=0, budget_s=15.0, max_steps=50):
+    """Times the oracle (as it stands, never tuned) on steps of the workload,
+    each against a bounded sample of n_sample stored rows (the same B queries,
+    the same calls: search, select, blend, insert); returns (searches/s scaled
+    to the full N -- every scan is linear in N --, timed steps, seconds, mean
+    seconds per sample step).  steps=None: as many steps as fit in budget_s."""
     from oracle import fmoe_oracle as O
     sh = cfg["shape"]
     B, k, dt, d, L = cfg["B"], cfg["k"], cfg["dtype"], 3, sh.L
@@ -660,33 +695,46 @@ def oracle_step_sample(cfg, seed, n_sample, budget_s=15.0, max_steps=50):
     qe, qm = O.quantize(qe.numpy(), dt), O.quantize(qm.numpy(), dt)
     ne, nm = qe, qm                      # the iteration's own context is inserted (as in the fMoE arm)
     searches, _ = step_counts(cfg)
-    steps, t0 = 0, time.perf_counter()
-    while True:
+
+    def one_step():
         s, i = store.search(qe, None, 0, 1.0, k)
         O.select_experts(store.maps, i[:, 0].tolist(), s[:, 0].tolist(), cfg["delta"], list(range(d)), sh.K)
         if cfg.get("kind") == "blend":
             for ell in cfg["ells"]:
                 s, i = store.search(qe, qm, ell, d / L, k)
                 if ell - 1 + d < L:
-                    O.select_experts(store.maps, i[:, 0].tolist(), s[:, 0].tolist(), cfg["delta"], [ell - 1 + d], sh.K)
+                    O.select_experts(store.maps, i[:, 0].tolist(), s[:, 0].tolist(), cfg["delta"], [ell - 1 + d],
+                                     sh.K)
             store.insert(ne[:cfg["insert"]], nm[:cfg["insert"]])
-            steps += 1
-            el = time.perf_counter() - t0
-            if el >= budget_s or steps >= max_steps:
-                break
-            continue
+            return
         for ell in range(1, L):
             s, i = store.search(None, qm, ell, 0.0, k)
             if ell - 1 + d < L:
                 O.select_experts(store.maps, i[:, 0].tolist(), s[:, 0].tolist(), cfg["delta"], [ell - 1 + d], sh.K)
         store.insert(ne, nm)
-        steps += 1
+
+    for _ in range(warmup):
+        one_step()
+    n, t0 = 0, time.perf_counter()
+    while True:
+        one_step()
+        n += 1
         el = time.perf_counter() - t0
-        if el >= budget_s or steps >= max_steps:
+        if steps is not None:
+            if n >= steps:
+                break
+        elif el >= budget_s or n >= max_steps:
             break
-    per_step = el / steps
+    per_step = el / n
     scale = cfg["N"] / n_sample
-    return searches / (per_step * scale), steps, el
+    return searches / (per_step * scale), n, el, per_step
+
+
+def oracle_sample_rows(cfg):
+    """Rows of the bounded sample one oracle step scans (about 1-4 s of fp64 work per step)."""
+    sh = cfg["shape"]
+    per_row = cfg["B"] * (sh.D + sh.L * sh.E) * (1 + len(cfg.get("ells", ())) + 1) if cfg["B"] > 1 else sh.D * 40
+    return int(min(cfg["N"], max(4096, 4e9 // per_row)))
 
 
 def blas_threads():
@@ -699,11 +747,22 @@ def blas_threads():
 
 
 def cpu_baseline(cfg, seed):
-    n_sample = min(cfg["N"], 65536 if cfg["shape"].D >= 2048 else 200000)
-    v, steps, el = oracle_step_sample(cfg, seed, n_sample)
+    n_sample = oracle_sample_rows(cfg)
+    v, steps, el, _ = oracle_step_sample(cfg, seed, n_sample, budget_s=15.0)
     return {"value": round(v, 4), "unit": "searches/s", "cores": blas_threads(), "kind": "oracle",
+            "cpu": cpu_model(),
             "sample": f"{steps} full step(s) ({step_counts(cfg)[0]} searches each) against {n_sample} of the "
                       f"{cfg['N']} stored maps, {el:.1f}s; time scaled x{cfg['N'] / n_sample:.2f} to N (scans are linear in N)"}
+
+
+def cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return f"{line.split(':', 1)[1].strip()} ({os.cpu_count()} logical CPUs)"
+    except OSError:
+        pass
+    return f"{os.cpu_count()} logical CPUs"
 
 
 # ------------------------------------------------------------------ main
@@ -718,37 +777,48 @@ def main():
     what = (f"semantic + blend (w=d/L) at ell={','.join(map(str, cfg['ells']))} + select + RDY insert of "
             f"{cfg['insert']} contexts" if cfg.get("kind") == "blend" else
             f"semantic + trajectory ell=1..{sh.L - 1} + select + RDY insert of the batch")
+    # `config` names the WORKLOAD only (identical in both arms); how an arm runs
+    # it goes to `impl_notes`
     base_config = {"workload": f"{args.config}: {sh.name} store N={cfg['N']} maps, L={sh.L}, E={sh.E}, D={sh.D}, "
-                               f"batch {cfg['B']}, {what} at full capacity", "N": cfg["N"], "L": sh.L, "E": sh.E, "D": sh.D, "B": cfg["B"],
-                   "k": cfg["k"], "store_dtype": cfg["dtype"], "searches_per_step": searches,
-                   "insert": ("RDY semantic half reused from the step's semantic search (fmoe_store_insert_cos)"
-                              if args.cos and world == 1 else "full RDY scan"),
-                   "trajectory": ("stateless: one search over the whole prefix per ell"
-                                  if args.traj == "stateless" or world > 1 else
-                                  "session sweep: the L-1 incremental steps of the request in one call "
-                                  "(fmoe_traj_session_sweep: running dots in registers, slab + norm row per step, "
-                                  "per-step top-1 + Eq. 4-6 selection by each step's last block)"
-                                  if args.traj == "sweep" and use_sweep(cfg) else
-                                  "batched session: per ell one tcgen05 scan over the whole prefix, seeded with "
-                                  "the previous step's rows (fmoe_traj_session_step)" if batched_session(cfg) else
-                                  "incremental session: step ell reads slab ell + running dots (SURVEY §8(f) #1)"),
+                               f"batch {cfg['B']}, {what} at full capacity", "N": cfg["N"], "L": sh.L, "E": sh.E,
+                   "D": sh.D, "B": cfg["B"], "k": cfg["k"], "store_dtype": cfg["dtype"],
+                   "searches_per_step": searches,
                    "l2": "inputs larger than L2 (store >> 126 MB), no flush",
-                   "launch": "CUDA graph replay of the step (1 GPU)" if (args.graph and world == 1) else "eager"}
+                   "parallelism": f"store sharded over {args.gpus} GPU(s)" if args.gpus > 1 else "1 GPU"}
+    traj_note = ("blends at fixed prefixes (no per-layer trajectory steps)" if cfg.get("kind") == "blend" else
+                 "stateless: one search over the whole prefix per ell" if args.traj == "stateless" else
+                 "session sweep: the L-1 incremental steps of the request in one call "
+                 "(fmoe_traj_session_sweep: running dots in registers, slab + norm row per step, "
+                 "per-step top-1 + Eq. 4-6 selection by each step's last block)"
+                 if args.traj == "sweep" and use_sweep(cfg) else
+                 "batched session: per ell one tcgen05 scan over the whole prefix, seeded with "
+                 "the previous step's rows (fmoe_traj_session_step)" if batched_session(cfg) else
+                 "incremental session: step ell reads slab ell + running dots (SURVEY §8(f) #1)")
+    fmoe_notes = {"trajectory": traj_note,
+                  "launch": "CUDA graph replay of the step" if args.graph else "eager"}
 
     if args.impl == "reference":
         if rank != 0:
             return
-        v, steps, el = oracle_step_sample(cfg, args.seed, min(cfg["N"], 65536 if sh.D >= 2048 else 200000),
-                                          budget_s=max(20.0, 2.0 * (args.steps + args.warmup)),
-                                          max_steps=args.steps + args.warmup)
+        # W untimed + K timed oracle steps, each a bounded row sample of the
+        # workload (the full store would take hours per step in fp64 on the host);
+        # ms_per_step is the measured sample step, value the throughput scaled to N
+        n_sample = oracle_sample_rows(cfg)
+        v, steps, el, per_step = oracle_step_sample(cfg, args.seed, n_sample, steps=args.steps, warmup=args.warmup)
         cores = blas_threads()
         line = {"metric": "expert-map searches/sec (batched)", "impl": "reference", "value": round(v, 4),
                 "unit": "searches/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-                "ms_per_step": round(searches / v * 1e3, 3), "higher_is_better": True, "scaling": "strong",
+                "ms_per_step": round(per_step * 1e3, 3), "higher_is_better": True, "scaling": "strong",
                 "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-                "config": dict(base_config, parallelism="cpu oracle"),
+                "config": base_config,
+                "impl_notes": {"engine": "fp64 numpy oracle (oracle/fmoe_oracle.py) on the host cores: every search "
+                                         "scores the whole (sampled) store, RDY insert scans embeddings + maps"},
+                "ms_per_full_step_extrapolated": round(searches / v * 1e3, 3),
                 "cpu_baseline": {"value": round(v, 4), "unit": "searches/s", "cores": cores, "kind": "oracle",
-                                 "sample": f"{steps} step(s) against a bounded row sample, scaled to N"},
+                                 "cpu": cpu_model(),
+                                 "sample": f"{steps} timed step(s) after {args.warmup} warm-up, each against "
+                                           f"{n_sample} of the {cfg['N']} stored maps ({el:.1f}s); time scaled "
+                                           f"x{cfg['N'] / n_sample:.2f} to N (scans are linear in N)"},
                 "e2e": {"value": round(v, 4), "unit": "searches/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
         print(json.dumps(line))
         return
@@ -767,8 +837,8 @@ def main():
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(res["ms_step"], 4),
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": cfg["dtype"],
             "data": "synthetic (seeded clustered embeddings + softmax gate maps, fmoe_synth)",
-            "config": dict(base_config, parallelism=f"store sharded over {world} GPU(s)" if world > 1 else "1 GPU",
-                           **cos_keys(cfg, res["cos"])),
+            "config": base_config,
+            "impl_notes": dict(fmoe_notes, **cos_keys(cfg, res["cos"])),
             "roofline": res["roofline"], "cpu_baseline": cpu, "e2e": res["e2e"], "clocks": res["clocks"],
             "gpu_launches": res["launches"]}
     print(json.dumps(line))

@@ -64,6 +64,7 @@ def _load():
         "fmoe_traj_session_step_select": (I32, [P, P, I32, P, P, F, I32, I32, P, P, P]),
         "fmoe_traj_session_sweep": (I32, [P, P, I32, P, P, F, I32, P, P, P, P, P]),
         "fmoe_traj_session_reset": (I32, [P]),
+        "fmoe_traj_session_abandoned": (I32, [P, ctypes.POINTER(I32)]),
         "fmoe_traj_session_destroy": (None, [P]),
         "fmoe_topk_merge": (I32, [I64, I32, I32, P, P, I32, P, P, ctypes.c_int, P]),
         "fmoe_prefetch_plan": (I32, [P, I64, P, P, F, I32, I32, I32, I32, P, P, P, P, P]),
@@ -87,7 +88,7 @@ ABI_SYMBOLS = ("fmoe_store_create", "fmoe_store_destroy", "fmoe_store_size", "fm
                "fmoe_store_write", "fmoe_resolve_victims", "fmoe_search_semantic", "fmoe_search_trajectory",
                "fmoe_search_blend", "fmoe_search_blend_cos", "fmoe_select_experts", "fmoe_traj_session_create", "fmoe_traj_session_step",
                "fmoe_traj_session_step_select", "fmoe_traj_session_sweep",
-               "fmoe_traj_session_reset", "fmoe_traj_session_destroy", "fmoe_topk_merge",
+               "fmoe_traj_session_reset", "fmoe_traj_session_abandoned", "fmoe_traj_session_destroy", "fmoe_topk_merge",
                "fmoe_prefetch_plan", "fmoe_eviction_order", "fmoe_expert_hits", "fmoe_status_string",
                "fmoe_last_error", "fmoe_kernel_launch_count", "fmoe_set_host_sync")
 
@@ -142,7 +143,8 @@ def fmoe_store_insert(h, emb, maps, out_slot=None, out_replaced=None, stream=Non
 
 
 def fmoe_store_insert_cos(h, emb, maps, sem_cos, cos_stride, out_slot=None, out_replaced=None, stream=None):
-    _check(_lib.fmoe_store_insert_cos(h, emb.shape[0], _ptr(_f32(emb)), _ptr(_f32(maps)), _ptr(sem_cos), cos_stride,
+    _check(_lib.fmoe_store_insert_cos(h, emb.shape[0], _ptr(_f32(emb)), _ptr(_f32(maps)),
+                                      _ptr(None if sem_cos is None else _f32(sem_cos)), cos_stride,
                                       _ptr(out_slot), _ptr(out_replaced), _stream(stream)))
 
 
@@ -180,7 +182,7 @@ def fmoe_search_blend(h, q_emb, q_prefix, ell, w_sem, k, out_score, out_id, stre
 
 
 def fmoe_search_blend_cos(h, sem_cos, cos_stride, q_prefix, ell, w_sem, k, out_score, out_id, stream=None):
-    _check(_lib.fmoe_search_blend_cos(h, q_prefix.shape[0], _ptr(sem_cos), cos_stride, _ptr(q_prefix), ell, w_sem, k,
+    _check(_lib.fmoe_search_blend_cos(h, q_prefix.shape[0], _ptr(_f32(sem_cos)), cos_stride, _ptr(_f32(q_prefix)), ell, w_sem, k,
                                       _ptr(out_score), _ptr(out_id), _stream(stream)))
 
 
@@ -228,7 +230,7 @@ def fmoe_traj_session_step_select(s, q_layer, k, out_score, out_id, delta, layer
 def fmoe_traj_session_sweep(s, q_layers, out_score, out_id, delta=-1.0, sel_d=-1, out_mask=None, out_count=None,
                             layer_ready=None, guidance_ready=None, stream=None):
     """q_layers [n_steps][B][E] -> out_score/out_id [n_steps][B] (+ selection masks/counts)."""
-    _check(_lib.fmoe_traj_session_sweep(s, _ptr(q_layers), q_layers.shape[0], _ptr(out_score), _ptr(out_id), delta,
+    _check(_lib.fmoe_traj_session_sweep(s, _ptr(_f32(q_layers)), q_layers.shape[0], _ptr(out_score), _ptr(out_id), delta,
                                         sel_d, _ptr(out_mask), _ptr(out_count), _ptr(layer_ready),
                                         _ptr(guidance_ready), _stream(stream)))
 
@@ -241,6 +243,14 @@ def fmoe_set_host_sync(enable):
 
 def fmoe_traj_session_reset(s):
     _check(_lib.fmoe_traj_session_reset(s))
+
+
+def fmoe_traj_session_abandoned(s) -> bool:
+    """Whether a sweep of the session was abandoned (layer_ready timeout) since the last reset;
+    read after synchronising the sweep's stream."""
+    v = ctypes.c_int32()
+    _check(_lib.fmoe_traj_session_abandoned(s, ctypes.byref(v)))
+    return bool(v.value)
 
 
 def fmoe_traj_session_destroy(s):

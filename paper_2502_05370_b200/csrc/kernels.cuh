@@ -95,6 +95,7 @@ struct SessionArgs {
   int64_t rpw;            // rows per warp (a contiguous range; set by launch_traj_session)
   const double* qn_prev;  // [B]
   double* qn_next;        // [B]
+  const unsigned* abort;  // device word: != 0 -> the session was abandoned; every query is invalid
   // optional fused Eq. 4-6 selection on each query's top-1 (sel_T = 0: none),
   // run by the step's last block: layers [sel_lb, sel_lb + sel_T)
   float sel_delta;        // < 0: dynamic Clip(1 - score, 0, 1)
@@ -124,8 +125,10 @@ struct SweepArgs {
   uint64_t* sel_mask;               // [n_steps] or null (no selection)
   int32_t* sel_count;               // [n_steps]
   const unsigned* layer_ready;      // [n_steps] or null: step s waits for layer_ready[s] != 0
-  unsigned* guidance_ready;         // [n_steps] or null: set to 1 when step s's outputs are written
+  unsigned* guidance_ready;         // [n_steps] or null: 1 when step s's outputs are written, 2 if abandoned
   unsigned long long timeout_ns;    // give up waiting for a layer after this long
+  unsigned* abort;                  // session status word: set on a timeout; a poisoned session
+                                    // (word != 0 at start) writes (NaN, -1) and abandons every step
 };
 int traj_sweep_rows(int64_t n_rows, int* grid_out);   // 0: the store is too large for the register sweep
 cudaError_t launch_traj_sweep(const SweepArgs& a, cudaStream_t stream);

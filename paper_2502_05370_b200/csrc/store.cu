@@ -80,15 +80,47 @@ struct DeviceGuard {
   }
 };
 
-// 0 = host (pageable or pinned), 1 = device memory of `dev`, -1 = other device
+// 0 = host (pageable or pinned), 1 = device memory of `dev`, -1 = other device,
+// -2 = a pointer the runtime rejects (CUDA >= 11 classifies plain host memory
+// as cudaMemoryTypeUnregistered, so a failure is not "host")
 int ptr_kind(const void* p, int dev) {
   cudaPointerAttributes at;
   if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
     cudaGetLastError();
-    return 0;
+    return -2;
   }
   if (at.type == cudaMemoryTypeDevice || at.type == cudaMemoryTypeManaged) return at.device == dev ? 1 : -1;
   return 0;
+}
+
+// Stream-ordered scratch comes from a private memory pool per device (release
+// threshold: keep everything), so the library never changes the process's
+// default pool.
+cudaMemPool_t scratch_pool(int dev) {
+  static std::mutex mu;
+  static std::map<int, cudaMemPool_t> pools;
+  std::lock_guard<std::mutex> lk(mu);
+  auto it = pools.find(dev);
+  if (it != pools.end()) return it->second;
+  cudaMemPoolProps props = {};
+  props.allocType = cudaMemAllocationTypePinned;
+  props.handleTypes = cudaMemHandleTypeNone;
+  props.location.type = cudaMemLocationTypeDevice;
+  props.location.id = dev;
+  cudaMemPool_t pool = nullptr;
+  if (cudaMemPoolCreate(&pool, &props) != cudaSuccess) {
+    cudaGetLastError();
+    pool = nullptr;
+  } else {
+    uint64_t thr = ~0ull;
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+  }
+  pools[dev] = pool;
+  return pool;
+}
+cudaError_t pool_malloc(void** p, size_t bytes, int dev, cudaStream_t s) {
+  cudaMemPool_t pool = scratch_pool(dev);
+  return pool ? cudaMallocFromPoolAsync(p, bytes, pool, s) : cudaMallocAsync(p, bytes, s);
 }
 
 // fmoe_set_host_sync: whether a call with host outputs synchronises its stream
@@ -99,6 +131,10 @@ std::atomic<int> g_host_sync{1};
 // cudaFreeAsync pair each.  A later call on the same stream may reuse the
 // bytes at once: its copies and kernels are ordered after the earlier call's.
 // Grows (stream-ordered free + malloc) when a call needed more.
+// The arena is capped at kArenaMax (a C5 host cosine matrix would otherwise
+// pin 16 GB for the life of the thread); bigger staging is allocated and freed
+// per call, stream-ordered.
+constexpr size_t kArenaMax = size_t(64) << 20;
 struct Arena {
   char* base = nullptr;
   size_t cap = 0, want = 0;
@@ -120,6 +156,7 @@ struct Staging {
   cudaError_t err = cudaSuccess;
   const char* what = "";
   bool bad_device = false;
+  bool bad_ptr = false;
 
   Staging(cudaStream_t s_, int dev_) : s(s_), dev(dev_) {}
 
@@ -134,8 +171,9 @@ struct Staging {
       used += bytes;
       return p;
     }
-    if (used + bytes > arena->want) arena->want = used + bytes;   // grow for the next call
-    cudaError_t e = cudaMallocAsync(&p, bytes, s);
+    // grow for the next call, up to kArenaMax; larger requests stay per-call
+    if (used + bytes > arena->want && used + bytes <= kArenaMax) arena->want = used + bytes;
+    cudaError_t e = pool_malloc(&p, bytes, dev, s);
     if (e != cudaSuccess) { err = e; what = "cudaMallocAsync"; return nullptr; }
     allocs.push_back(p);
     return p;
@@ -145,7 +183,7 @@ struct Staging {
     if (!p) return nullptr;
     const int k = ptr_kind(p, dev);
     if (k == 1) return p;
-    if (k < 0) { bad_device = true; return nullptr; }
+    if (k < 0) { bad_device = true; bad_ptr = bad_ptr || k == -2; return nullptr; }
     T* d = static_cast<T*>(scratch(count * sizeof(T)));
     if (!d) return nullptr;
     if (count) {
@@ -159,13 +197,14 @@ struct Staging {
     if (!p) return nullptr;
     const int k = ptr_kind(p, dev);
     if (k == 1) return p;
-    if (k < 0) { bad_device = true; return nullptr; }
+    if (k < 0) { bad_device = true; bad_ptr = bad_ptr || k == -2; return nullptr; }
     T* d = static_cast<T*>(scratch(count * sizeof(T)));
     if (d) backs.push_back({p, d, count * sizeof(T)});
     return d;
   }
   fmoe_status check() const {
-    if (bad_device) return fail(FMOE_ERR_INVALID_ARG, "array on another device");
+    if (bad_device) return fail(FMOE_ERR_INVALID_ARG, bad_ptr ? "pointer rejected by cudaPointerGetAttributes"
+                                                              : "array on another device");
     if (err != cudaSuccess) return cuda_fail(err, what);
     return FMOE_OK;
   }
@@ -183,7 +222,7 @@ struct Staging {
       arena->base = nullptr;
       arena->cap = 0;
       const size_t nb = arena->want < (size_t(1) << 20) ? (size_t(1) << 20) : arena->want;
-      if (cudaMallocAsync(reinterpret_cast<void**>(&arena->base), nb, s) == cudaSuccess) arena->cap = nb;
+      if (pool_malloc(reinterpret_cast<void**>(&arena->base), nb, dev, s) == cudaSuccess) arena->cap = nb;
       else cudaGetLastError();
     }
     if (!backs.empty() && g_host_sync.load(std::memory_order_relaxed)) {
@@ -220,7 +259,7 @@ fmoe_status stream_scratch(const fmoe_store* st, cudaStream_t s, size_t bytes, i
     sc.buf = nullptr;
     sc.bytes = 0;
     const size_t nb = bytes + bytes / 2 + 4096;
-    if ((e = cudaMallocAsync(reinterpret_cast<void**>(&sc.buf), nb, s)) != cudaSuccess) return cuda_fail(e, "scratch");
+    if ((e = pool_malloc(reinterpret_cast<void**>(&sc.buf), nb, st->device, s)) != cudaSuccess) return cuda_fail(e, "scratch");
     sc.bytes = nb;
   }
   if (sc.ncounters < ncount) {
@@ -228,7 +267,7 @@ fmoe_status stream_scratch(const fmoe_store* st, cudaStream_t s, size_t bytes, i
     sc.counters = nullptr;
     sc.ncounters = 0;
     const int nc = ncount < 64 ? 64 : ncount;
-    if ((e = cudaMallocAsync(reinterpret_cast<void**>(&sc.counters), size_t(nc) * 4, s)) != cudaSuccess)
+    if ((e = pool_malloc(reinterpret_cast<void**>(&sc.counters), size_t(nc) * 4, st->device, s)) != cudaSuccess)
       return cuda_fail(e, "counters");
     if ((e = cudaMemsetAsync(sc.counters, 0, size_t(nc) * 4, s)) != cudaSuccess) return cuda_fail(e, "counters");
     sc.ncounters = nc;
@@ -238,7 +277,7 @@ fmoe_status stream_scratch(const fmoe_store* st, cudaStream_t s, size_t bytes, i
     sc.best = nullptr;
     sc.nbest = 0;
     const int nb = nbest < 256 ? 256 : nbest;
-    if ((e = cudaMallocAsync(reinterpret_cast<void**>(&sc.best), size_t(nb) * 8, s)) != cudaSuccess)
+    if ((e = pool_malloc(reinterpret_cast<void**>(&sc.best), size_t(nb) * 8, st->device, s)) != cudaSuccess)
       return cuda_fail(e, "best keys");
     if ((e = cudaMemsetAsync(sc.best, 0, size_t(nb) * 8, s)) != cudaSuccess) return cuda_fail(e, "best keys");
     sc.nbest = nb;
@@ -461,15 +500,7 @@ fmoe_status fmoe_store_create(const fmoe_store_config* cfg, int device, fmoe_sto
     return fail(FMOE_ERR_INVALID_ARG, "no such CUDA device");
   }
   DeviceGuard g(device);
-  {
-    // keep stream-ordered scratch cached in the pool across synchronisations
-    cudaMemPool_t pool;
-    if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
-      uint64_t thr = ~0ull;
-      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
-    }
-    cudaGetLastError();
-  }
+  scratch_pool(device);
   fmoe_store* st = new fmoe_store();
   st->cfg = *cfg;
   st->device = device;
@@ -494,12 +525,17 @@ fmoe_status fmoe_store_create(const fmoe_store_config* cfg, int device, fmoe_sto
 void fmoe_store_destroy(fmoe_store* st) {
   if (!st) return;
   DeviceGuard g(st->device);
-  cudaDeviceSynchronize();
+  // Scratch is stream-ordered: freed on the stream that used it (no device-wide
+  // synchronisation; the caller guarantees no other work on the store is
+  // pending, the usual rule for freeing memory).  cudaFree of the tiles waits
+  // for the device only as the runtime itself requires.
   for (auto& kv : st->scratch) {
-    cudaFree(kv.second.buf);
-    cudaFree(kv.second.counters);
-    cudaFree(kv.second.best);
+    cudaFreeAsync(kv.second.buf, kv.first);
+    cudaFreeAsync(kv.second.counters, kv.first);
+    cudaFreeAsync(kv.second.best, kv.first);
+    cudaStreamSynchronize(kv.first);
   }
+  cudaGetLastError();
   cudaFree(st->emb);
   cudaFree(st->r_e);
   cudaFree(st->maps);
@@ -601,8 +637,12 @@ fmoe_status fmoe_store_insert_cos(fmoe_store* st, int64_t B, const float* emb, c
     cudaError_t e = launch_write_rows(w, s);
     if (e != cudaSuccess) r = cuda_fail(e, "write launch");
   }
-  if (r == FMOE_OK) st->n = n0 + a;
-  ++st->gen;
+  // (the size counts enqueued inserts: calls are asynchronous; a failed call
+  // leaves the store and its generation unchanged)
+  if (r == FMOE_OK) {
+    st->n = n0 + a;
+    ++st->gen;
+  }
   return S.finish(r);
 }
 
@@ -632,7 +672,7 @@ fmoe_status fmoe_store_write(fmoe_store* st, int64_t B, const float* emb, const 
     cudaError_t e = launch_write_rows(w, s);
     if (e != cudaSuccess) r = cuda_fail(e, "write launch");
   }
-  ++st->gen;
+  if (r == FMOE_OK) ++st->gen;
   return S.finish(r);
 }
 
@@ -660,6 +700,12 @@ struct fmoe_traj_session {
   float* sctmp = nullptr;    // [B][kk] its scores
   int prev_k = 0;
   int layer = 0;
+  int qslot = 0;             // qn slot holding the running norm (incremental); the next
+                             // step writes the other slot, so a launch never reads and
+                             // writes the same word
+  unsigned* abort = nullptr; // device word: a sweep abandoned on a layer_ready timeout
+                             // poisons the session until reset (incremental)
+  bool clear_abort = false;  // reset() asked: zero `abort` on the next call's stream
   uint64_t gen = 0;
   void* sweep_scratch = nullptr;   // [L] u64 best keys + [L] u32 tickets (fmoe_traj_session_sweep)
 };
@@ -681,7 +727,9 @@ fmoe_status fmoe_traj_session_create(const fmoe_store* st, int64_t B, fmoe_traj_
                     (e = cudaMalloc(&s->prev, size_t(B) * FMOE_MAX_K * 8)) != cudaSuccess ||
                     (e = cudaMalloc(&s->sctmp, size_t(B) * FMOE_MAX_K * 4)) != cudaSuccess)
                  : ((e = cudaMalloc(&s->acc, size_t(B) * st->cfg.capacity * 4)) != cudaSuccess ||
-                    (e = cudaMalloc(&s->qn, size_t(2) * B * 8)) != cudaSuccess)) {
+                    (e = cudaMalloc(&s->qn, size_t(2) * B * 8)) != cudaSuccess ||
+                    (e = cudaMalloc(&s->abort, 4)) != cudaSuccess ||
+                    (e = cudaMemset(s->abort, 0, 4)) != cudaSuccess)) {
     fmoe_traj_session_destroy(s);
     return cuda_fail(e, "session memory");
   }
@@ -692,7 +740,8 @@ fmoe_status fmoe_traj_session_create(const fmoe_store* st, int64_t B, fmoe_traj_
 void fmoe_traj_session_destroy(fmoe_traj_session* s) {
   if (!s) return;
   DeviceGuard g(s->st->device);
-  cudaDeviceSynchronize();
+  // (the caller guarantees no step of the session is pending, as for any free)
+  cudaFree(s->abort);
   cudaFree(s->acc);
   cudaFree(s->qn);
   cudaFree(s->prefix);
@@ -706,7 +755,21 @@ fmoe_status fmoe_traj_session_reset(fmoe_traj_session* s) {
   if (!s) return fail(FMOE_ERR_INVALID_ARG, "null session");
   s->layer = 0;
   s->prev_k = 0;
+  s->qslot = 0;
+  s->clear_abort = s->abort != nullptr;
   s->gen = s->st->gen;
+  return FMOE_OK;
+}
+
+fmoe_status fmoe_traj_session_abandoned(const fmoe_traj_session* s, int32_t* out_abandoned) {
+  if (!s || !out_abandoned) return fail(FMOE_ERR_INVALID_ARG, "null argument");
+  *out_abandoned = 0;
+  if (!s->abort || s->clear_abort) return FMOE_OK;
+  DeviceGuard g(s->st->device);
+  unsigned v = 0;
+  cudaError_t e = cudaMemcpy(&v, s->abort, 4, cudaMemcpyDeviceToHost);
+  if (e != cudaSuccess) return cuda_fail(e, "session status read");
+  *out_abandoned = v != 0 ? 1 : 0;
   return FMOE_OK;
 }
 
@@ -805,12 +868,18 @@ fmoe_status session_step(fmoe_traj_session* ss, const float* q_layer, int32_t k,
       a.out_id = di;
       a.check_valid = 1;
       a.trace = trace_buffer();
+      if (ss->clear_abort) {
+        cudaError_t e = cudaMemsetAsync(ss->abort, 0, 4, s);
+        if (e != cudaSuccess) r = cuda_fail(e, "session status reset");
+        else ss->clear_abort = false;
+      }
       SessionArgs sa{};
       sa.q_layer = dq;
       sa.layer = ss->layer;
       sa.acc = ss->acc;
-      sa.qn_prev = ss->qn + (ss->layer & 1) * B;
-      sa.qn_next = ss->qn + ((ss->layer + 1) & 1) * B;
+      sa.abort = ss->abort;
+      sa.qn_prev = ss->qn + ss->qslot * B;
+      sa.qn_next = ss->qn + (ss->qslot ^ 1) * B;
       // the selection runs in each pass's last block, on that pass's queries
       sa.sel_delta = sel.delta;
       sa.sel_K = st->cfg.K;
@@ -825,7 +894,10 @@ fmoe_status session_step(fmoe_traj_session* ss, const float* q_layer, int32_t k,
         cudaError_t e = launch_traj_session(a, sa, s);
         if (e != cudaSuccess) r = cuda_fail(e, "session launch");
       }
-      if (r == FMOE_OK) ++ss->layer;
+      if (r == FMOE_OK) {
+        ++ss->layer;
+        ss->qslot ^= 1;
+      }
     }
   }
   return S.finish(r);
@@ -950,6 +1022,10 @@ fmoe_status fmoe_traj_session_sweep(fmoe_traj_session* ss, const float* q_layers
   fmoe_status r = S.check();
   if (r == FMOE_OK) {
     cudaError_t e = cudaMemsetAsync(ss->sweep_scratch, 0, size_t(L) * 12, s);
+    if (e == cudaSuccess && ss->clear_abort) {
+      e = cudaMemsetAsync(ss->abort, 0, 4, s);
+      if (e == cudaSuccess) ss->clear_abort = false;
+    }
     SweepArgs a{};
     a.st = st->view();
     a.n_rows = st->n;
@@ -958,8 +1034,11 @@ fmoe_status fmoe_traj_session_sweep(fmoe_traj_session* ss, const float* q_layers
     a.layer0 = ss->layer;
     a.n_steps = n_steps;
     a.acc = ss->acc;
-    a.qn_in = ss->qn + (ss->layer & 1);
-    a.qn_out = ss->qn + ((ss->layer + n_steps) & 1);
+    // B = 1: slot q holds the norm; input and output never alias (ADVICE r1:
+    // a block starting after block 0 exits must still read the input norm)
+    a.qn_in = ss->qn + ss->qslot;
+    a.qn_out = ss->qn + (ss->qslot ^ 1);
+    a.abort = ss->abort;
     a.best = reinterpret_cast<unsigned long long*>(ss->sweep_scratch);
     a.tickets = reinterpret_cast<unsigned*>(static_cast<char*>(ss->sweep_scratch) + size_t(L) * 8);
     a.out_score = ds;
@@ -974,7 +1053,10 @@ fmoe_status fmoe_traj_session_sweep(fmoe_traj_session* ss, const float* q_layers
     a.timeout_ns = 10ull * 1000 * 1000 * 1000;
     if (e == cudaSuccess) e = launch_traj_sweep(a, s);
     if (e != cudaSuccess) r = cuda_fail(e, "sweep launch");
-    else ss->layer += n_steps;
+    else {
+      ss->layer += n_steps;
+      ss->qslot ^= 1;
+    }
   }
   return S.finish(r);
 }

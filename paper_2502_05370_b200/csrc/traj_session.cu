@@ -39,6 +39,15 @@ __device__ __forceinline__ void unpack_sess(const uint4& u, float (&x)[8]) {
   }
 }
 
+__device__ __forceinline__ unsigned ld_acquire_u32(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_u32(unsigned* p, unsigned v) {
+  asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
 __device__ __forceinline__ int pow2_at_least(int c) {
   int g = 1;
   while (g < c) g <<= 1;
@@ -84,7 +93,9 @@ __global__ void __launch_bounds__(kSessThreads, NQ == 1 ? 4 : 2) traj_session_ke
     double t = layer > 0 ? s.qn_prev[a.q0 + tid] : 0.0;
     for (int w = 0; w < kSessWarps; ++w) t += red[w][tid];
     rq[tid] = t > 0.0 ? float(1.0 / sqrt(t)) : 0.f;
-    s_valid[tid] = t > 0.0;
+    // an abandoned sweep left the accumulators half-updated: no valid result
+    // until the session is reset
+    s_valid[tid] = t > 0.0 && !(s.abort && ld_acquire_u32(s.abort) != 0u);
     if (blockIdx.x == 0 && tid < a.nq) s.qn_next[a.q0 + tid] = t;   // double-buffered: others read qn_prev
   }
   __syncthreads();
@@ -249,14 +260,6 @@ int traj_session_grid(const ScanArgs& a) {
 constexpr int kSweepThreads = 256;
 constexpr int kSweepWarps = kSweepThreads / 32;
 
-__device__ __forceinline__ unsigned ld_acquire_u32(const unsigned* p) {
-  unsigned v;
-  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-  return v;
-}
-__device__ __forceinline__ void st_release_u32(unsigned* p, unsigned v) {
-  asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
-}
 __device__ __forceinline__ unsigned long long globaltimer_ns() {
   unsigned long long t;
   asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
@@ -264,6 +267,26 @@ __device__ __forceinline__ unsigned long long globaltimer_ns() {
 }
 
 constexpr int kSweepMaxSteps = 64;
+
+// A sweep that cannot run its steps (a poisoned session, or a layer that never
+// became ready) marks them abandoned: guidance_ready = 2 for steps [s0, n), so
+// a subscriber waiting on the flag wakes up, and the session's status word is
+// set (fmoe_traj_session_abandoned; steps of the session report (NaN, -1)
+// until it is reset).  Outputs of a poisoned session's steps are (NaN, -1).
+__device__ __forceinline__ void sweep_abandon(const SweepArgs& a, int s0, bool write_outputs) {
+  if (threadIdx.x != 0) return;
+  if (write_outputs && blockIdx.x == 0)
+    for (int f = s0; f < a.n_steps; ++f) {
+      a.out_score[f] = __int_as_float(0x7fc00000);
+      a.out_id[f] = -1;
+      if (a.sel_mask) { a.sel_mask[f] = 0ull; a.sel_count[f] = 0; }
+    }
+  if (a.abort) atomicExch(a.abort, 1u);
+  __threadfence();
+  if (a.guidance_ready)
+    for (int f = s0; f < a.n_steps; ++f) atomicCAS(a.guidance_ready + f, 0u, 2u);
+}
+
 
 // running query norm of step s from the per-warp partial sums, in the step
 // kernel's order: t = (layer > 0 ? t_prev : 0) + red[0] + ... + red[7]
@@ -311,6 +334,10 @@ __global__ void __launch_bounds__(kSweepThreads, 4) traj_sweep_kernel(const Swee
   const int gt = int(blockIdx.x) * kSweepThreads + tid;
   const bool flags = a.layer_ready != nullptr;
   pdl_wait();
+  if (a.abort && ld_acquire_u32(a.abort) != 0u) {   // poisoned by an earlier abandoned sweep
+    sweep_abandon(a, 0, true);
+    return;
+  }
 
   // the first step's store rows are in flight while the queries are staged
   uint4 buf[R];
@@ -395,7 +422,17 @@ __global__ void __launch_bounds__(kSweepThreads, 4) traj_sweep_kernel(const Swee
         }
       }
       __syncthreads();
-      if (s_abort) return;
+      if (s_abort) {
+        // finish the step this block may hold the last ticket of, then abandon the rest
+        if (tid == 0) {
+          s_last = pend_s >= 0 && pend_ticket == gridDim.x - 1;
+          s_fin = pend_s;
+        }
+        __syncthreads();
+        if (s_last) finalize(s_fin);
+        sweep_abandon(a, s, false);
+        return;
+      }
       stage(s);
     }
     const float rq = rqs[s];
@@ -503,6 +540,10 @@ __global__ void __launch_bounds__(kSweepTmaThreads, 2) traj_sweep_tma_kernel(con
   }
   __syncthreads();
   pdl_wait();
+  if (a.abort && ld_acquire_u32(a.abort) != 0u) {
+    sweep_abandon(a, 0, true);
+    return;
+  }
   auto issue = [&](int s) {   // tid 0: slab chunk of step s into stage s & 1
     const char* src = static_cast<const char*>(st.maps) + (int64_t(a.layer0 + s) * st.cap + base) * 16;
     mbar_arrive_expect_tx(&bar[s & 1], unsigned(cnt) * 16u);
@@ -600,6 +641,13 @@ __global__ void __launch_bounds__(kSweepTmaThreads, 2) traj_sweep_tma_kernel(con
         // drain the bulk copies still landing in this block's shared memory
         mbar_wait(&bar[s & 1], unsigned((s >> 1) & 1));
         if (s + 1 < a.n_steps) mbar_wait(&bar[(s + 1) & 1], unsigned(((s + 1) >> 1) & 1));
+        if (tid == 0) {
+          s_last = pend_s >= 0 && pend_ticket == gridDim.x - 1;
+          s_fin = pend_s;
+        }
+        __syncthreads();
+        if (s_last) finalize(s_fin);
+        sweep_abandon(a, s, false);
         return;
       }
       stage(s);

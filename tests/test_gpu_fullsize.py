@@ -184,3 +184,32 @@ def test_c2_session_sweep_full_size(c2):
         finally:
             ref.close()
             a.close()
+
+
+def test_c2_full_oracle_scan_two_queries(c2):
+    """A complete fp64 oracle scan of the whole C2 store (read back chunk by
+    chunk: the O-store view) for 2 queries, semantic and trajectory at ell = 31,
+    with the element-wise id rules of the parity contract -- at BASELINE's full
+    size, in bench.py's B = 1 launch configuration."""
+    from test_gpu_midsize import check_topk_fast
+    lib, st, sh, N = c2
+    qe, qm, _ = S.queries(sh, SEED + 1, N, 2, device="cuda")
+    k = 8
+    got = {}
+    for x in range(2):                                        # B = 1 calls, like the bench
+        got[("sem", x)] = st.search_semantic(qe[x:x + 1], k)
+        got[("traj", x)] = st.search_trajectory(qm[x:x + 1, :31].contiguous(), 31, k)
+    q_e = O.quantize(qe.cpu().numpy(), "bf16")
+    q_m = O.quantize(qm[:, :31].cpu().numpy(), "bf16")
+    sem = np.empty((2, N))
+    trj = np.empty((2, N))
+    for a in range(0, N, 16384):
+        c = min(16384, N - a)
+        e, m = st.read(a, c)
+        sem[:, a:a + c] = O.semantic_scores(q_e, e.cpu().numpy())
+        trj[:, a:a + c] = O.trajectory_scores(q_m, m[:, :31].cpu().numpy(), 31)
+    for x in range(2):
+        s, i = got[("sem", x)]
+        check_topk_fast(s, i, sem[x:x + 1], k)
+        s, i = got[("traj", x)]
+        check_topk_fast(s, i, trj[x:x + 1], k)
