@@ -63,6 +63,7 @@ struct ScanArgs {
   float* out_cos;
   const float* sem_cos;
   int64_t cos_stride;
+  const int* run_if_gt;      // nullable device count: the pass runs only if *run_if_gt > q0 (re-rank fallback)
 };
 
 // debug tracer buffer (null unless fmoe_debug_trace enabled it)
@@ -142,6 +143,9 @@ struct UmmaPlanIn {
   const void* emb; const void* maps; const float* r_e; const float* psq;
   int rep;                     // query replication (umma_rep), uniform over a call's passes
   int cg;                      // 1: CTAs, 2: CTA pairs (M = 256); 0 = by nq.  Uniform over a call's passes
+  int approx;                  // semantic scan with one accumulator; an exact re-rank follows (rerank.cu)
+  int cos_out;                 // the call writes the cosine side output (reserve the TMA staging smem)
+  int cos_in;                  // the call blends cached cosines (reserve the TMA load ring)
 };
 struct UmmaLaunch {
   UmmaPlanIn in;
@@ -162,6 +166,26 @@ size_t umma_scratch_bytes(const UmmaPlanIn& in);
 int umma_grid(const UmmaPlanIn& in);   // CTAs to launch (a multiple of umma_cg)
 int umma_cg(const UmmaPlanIn& in);
 cudaError_t launch_umma(const UmmaLaunch& L, cudaStream_t s);
+// Exact re-rank of an approximate (single-accumulator) tensor-core semantic
+// scan's merged candidates (rerank.cu): [B][ke] keys -> the exact top k, and
+// the queries whose completeness margin fails, queued for the GEMV fallback.
+struct RerankArgs {
+  int B, ke, k;
+  const uint64_t* keys;        // [B][ke] merged approximate keys (desc)
+  const float* q_emb;          // [B][D] fp32 queries
+  int D, Dp;
+  const void* emb;             // store embeddings [cap][Dp] bf16
+  const float* r_e;
+  uint32_t id_offset;
+  const float* valid;          // [B] query validity (prep)
+  float eps;                   // bound on |approximate - exact| score
+  float* out_score; int64_t* out_id; uint64_t* out_keys;   // [B][k] (any may be null)
+  int* nfail; int* qmap; float* qc;                        // fallback queue: count, slot -> query, [B][D] queries
+};
+cudaError_t launch_rerank(const RerankArgs& r, cudaStream_t s);
+cudaError_t launch_rerank_scatter(const int* nfail, const int* qmap, int k, const float* fb_s, const int64_t* fb_i,
+                                  const uint64_t* fb_keys, float* out_score, int64_t* out_id, uint64_t* out_keys,
+                                  int* nfail_w, cudaStream_t s);
 // Merge (score, id) lists from an all-gather: [n_lists][B][k_in].
 cudaError_t launch_merge_lists(int B, int n_lists, int k_in, const float* scores,
                                const int64_t* ids, int k, float* out_score, int64_t* out_id,

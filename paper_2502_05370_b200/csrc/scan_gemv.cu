@@ -83,6 +83,7 @@ __global__ void __launch_bounds__(kScanThreads, TPI >= 1 ? 2 : 3) scan_gemv_kern
   trace_mark(a.trace, 0);
   pdl_wait();
   trace_mark(a.trace, 1);
+  if (a.run_if_gt && *a.run_if_gt <= a.q0) return;   // a fallback pass with no queries
 
   // ---- 1. stage the queries (quantised to the store dtype) + their norms
   double part[2 * NQ];

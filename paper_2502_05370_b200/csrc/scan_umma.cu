@@ -178,6 +178,22 @@ __device__ __forceinline__ void tile_mark(unsigned long long* trace, int role, u
   if (trace && blockIdx.x == 0 && ti < 256) trace[8192 + role * 256 + ti] = globaltimer();
 }
 __device__ __forceinline__ void tc_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+// shared -> global tensor store (bulk group) and its completion waits
+__device__ __forceinline__ void tma_store_2d(const CUtensorMap* map, const void* src, int c0, int c1) {
+  asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];" ::"l"(
+                   reinterpret_cast<uint64_t>(map)),
+               "r"(smem_u32(src)), "r"(c0), "r"(c1)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_read0() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_all0() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+__device__ __forceinline__ void fence_proxy_async_smem() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+__device__ __forceinline__ void sts128(uint32_t a, float x, float y, float z, float w) {
+  asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(a), "f"(x), "f"(y), "f"(z), "f"(w) : "memory");
+}
 
 // UMMA shared-memory matrix descriptor (K-major), sm_100 "version 1".
 //  layout: 0 none (interleaved core matrices), 6 SW32, 4 SW64, 2 SW128
@@ -235,7 +251,16 @@ struct UmmaParams {
   const float* sem_cos;         // trajectory kernels: cached semantic cosines to blend (optional)
   int64_t cos_stride;
   unsigned long long* gthr;     // [nq] shared admission threshold per query (zeroed by prep)
+  int cos_tma;                  // semantic scans: out_cos written through a swizzled smem stage + TMA
+                                // tensor stores; trajectory scans: sem_cos read by per-warp TMA loads
+                                // (a 3-buffer ring, 2 chunks ahead) instead of lane-per-query loads
+  int no_a_reload;              // debug knob (FMOE_NO_A_RELOAD=1): query operand loaded only into the
+                                // first ring pass, reused stale afterwards (results garbage; measures
+                                // the L2 traffic of re-reading it per tile)
 };
+constexpr int kCosStage = 32 * 128;             // per epilogue warp: 32 queries x 32 columns fp32 (SW128)
+constexpr int kCosRing = 3;                     // cached-cosine loads: buffers per epilogue warp (2 chunks ahead)
+__host__ __device__ constexpr int cos_stage_bytes(bool sem) { return kUmEpiWarps * kCosStage * (sem ? 1 : kCosRing); }
 
 // Sorted insert into a per-thread list in shared memory (entry i at
 // l[i*stride]); called rarely (only for keys beating the k-th), kept out of
@@ -312,9 +337,10 @@ template <bool SEM, bool TRAJ, int CG, int TN>
 __global__ void __launch_bounds__(kUmThreads, 1)
     scan_umma_kernel(const __grid_constant__ CUtensorMap tm_qs, const __grid_constant__ CUtensorMap tm_es,
                      const __grid_constant__ CUtensorMap tm_qt, const __grid_constant__ CUtensorMap tm_mt,
-                     const UmmaParams p) {
+                     const __grid_constant__ CUtensorMap tm_cos, const UmmaParams p) {
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   __shared__ __align__(8) uint64_t full[kUmMaxStages], empty[kUmMaxStages], tfull[2], tempty[2];
+  __shared__ __align__(8) uint64_t cbar_all[kUmEpiWarps * kCosRing];   // cached-cosine ring (TRAJ + sem_cos)
   if (p.gate) {                                  // a conditional (fallback) scan
     pdl_wait();
     if (*p.gate == 0) {                          // (both CTAs of a pair read the same flag)
@@ -330,7 +356,9 @@ __global__ void __launch_bounds__(kUmThreads, 1)
   unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   constexpr int NB = um_rows(CG, TN);            // store rows of a tile held by this CTA
   constexpr int SBY = um_stage_bytes(CG, TN);
-  uint64_t* lists = reinterpret_cast<uint64_t*>(smem + size_t(p.stages) * SBY);   // [2R][k][LQ]
+  // [8 warps][kCosStage] cosine staging (cos_tma), then the lists [2R][k][LQ]
+  unsigned char* cstage_all = smem + size_t(p.stages) * SBY;
+  uint64_t* lists = reinterpret_cast<uint64_t*>(cstage_all + (p.cos_tma ? cos_stage_bytes(SEM) : 0));
   // CTA pair (cta_group::2): rank r owns query rows r*128.. of the M = 256
   // operand and store rows r*128.. of each 256-row tile; the leader (rank 0)
   // issues the MMAs for both, the accumulators of its queries land in each
@@ -351,6 +379,8 @@ __global__ void __launch_bounds__(kUmThreads, 1)
     // the leader's stage barrier also waits for the peer's relay arrival
     for (int s = 0; s < S; ++s) { mbar_init(&full[s], (CG == 2 && leader) ? 2 : 1); mbar_init(&empty[s], 1); }
     for (int a = 0; a < AS; ++a) { mbar_init(&tfull[a], 1); mbar_init(&tempty[a], CG * kUmEpiWarps); }
+    if (!SEM && p.cos_tma)
+      for (int i = 0; i < kUmEpiWarps * kCosRing; ++i) mbar_init(&cbar_all[i], 1);
     mbar_fence_init();
   }
   if (warp == 0 && lane == 0) {
@@ -424,8 +454,9 @@ __global__ void __launch_bounds__(kUmThreads, 1)
             continue;
           }
           if (SEM && kb < p.n_sem_kb) {
-            mbar_arrive_expect_tx(&full[s], unsigned(SBY));
-            tma_load_2d(sa, &tm_qs, kb * 64, rank * UM_M, &full[s]);
+            const bool load_a = !p.no_a_reload || u < unsigned(S);
+            mbar_arrive_expect_tx(&full[s], unsigned(load_a ? SBY : SBY - kStageA));
+            if (load_a) tma_load_2d(sa, &tm_qs, kb * 64, rank * UM_M, &full[s]);
             tma_load_2d(sb, &tm_es, kb * 64, y0, &full[s]);
           } else {
             const int j = kb - p.n_sem_kb;
@@ -590,6 +621,25 @@ __global__ void __launch_bounds__(kUmThreads, 1)
       }
     };
     fetch(cid);
+    // cached cosines (TRAJ + sem_cos, cos_tma): chunk i of this warp's sequence
+    // (tile cid + (i / NC) * ncl, chunk i % NC) lands in ring buffer i % 3
+    const bool cin = !SEM && p.sem_cos && p.cos_tma;
+    uint64_t* cbar = cbar_all + e * kCosRing;
+    unsigned char* cring = cstage_all + size_t(e) * kCosRing * kCosStage;
+    const int crow = rank * UM_M + (qd % QA) * 32;      // first query row of this warp's box
+    auto cos_issue = [&](unsigned i) {                  // lane 0
+      const int t2 = cid + int(i / unsigned(NC)) * ncl;
+      if (t2 >= p.n_tiles) return;
+      const int col = t2 * TN + half * HC + sub * NC * 32 + int(i % unsigned(NC)) * 32;
+      uint64_t* b = &cbar[i % kCosRing];
+      mbar_arrive_expect_tx(b, unsigned(kCosStage));
+      tma_load_2d(cring + (i % kCosRing) * kCosStage, &tm_cos, col, crow, b);
+    };
+    if (cin && lane == 0) {
+      cos_issue(0);
+      cos_issue(1);
+    }
+    unsigned ci = 0;                                    // this warp's chunk sequence number
     for (int t = cid; t < p.n_tiles; t += ncl, ++ti) {
       const int as = int(ti % unsigned(AS));
       const int ybase = t * TN + half * HC + sub * NC * 32;     // first column of this warp
@@ -636,7 +686,25 @@ __global__ void __launch_bounds__(kUmThreads, 1)
         const int64_t left = p.n_rows - yc;
         const unsigned vmask = !live ? 0u : (left >= 32 ? 0xffffffffu : (left <= 0 ? 0u : ((1u << left) - 1u)));
         float cached[32];
-        if (!SEM && p.sem_cos) {
+        if (cin) {
+          // buffer (ci + 2) % 3 held chunk ci - 1, which every lane has read
+          __syncwarp();
+          if (lane == 0) {
+            fence_proxy_async_smem();
+            cos_issue(ci + 2);
+          }
+          mbar_wait(&cbar[ci % kCosRing], (ci / kCosRing) & 1u);
+          const uint32_t row = smem_u32(cring + (ci % kCosRing) * kCosStage) + uint32_t(lane) * 128u;
+#pragma unroll
+          for (int j4 = 0; j4 < 8; ++j4) {
+            float4 f;
+            asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
+                         : "=f"(f.x), "=f"(f.y), "=f"(f.z), "=f"(f.w)
+                         : "r"(row + (uint32_t(j4 ^ (lane & 7)) << 4)));
+            cached[4 * j4] = f.x; cached[4 * j4 + 1] = f.y; cached[4 * j4 + 2] = f.z; cached[4 * j4 + 3] = f.w;
+          }
+          ++ci;
+        } else if (!SEM && p.sem_cos) {
           const float* cp = p.sem_cos + int64_t(p.cand_q0 + qg) * p.cos_stride + yc;
 #pragma unroll
           for (int j = 0; j < 32; j += 4) {
@@ -683,7 +751,30 @@ __global__ void __launch_bounds__(kUmThreads, 1)
         }
         m &= vmask;
         EPI_T(3);
-        if (SEM && !TRAJ && p.out_cos && live) {
+        if (SEM && !TRAJ && p.out_cos && p.cos_tma) {
+          // warp-cooperative: the 32 x 32 block (queries of this warp x this
+          // chunk's columns) is staged in shared memory with the 128-byte
+          // swizzle (16-byte group j of row r at j ^ (r & 7): conflict-free
+          // v4 stores) and written by one TMA tensor store, which also clips
+          // rows >= nq and columns >= n_rows.  (Lane-per-query global stores
+          // touched 32 rows per instruction.)
+          if (__any_sync(0xffffffffu, live)) {
+            unsigned char* cst = cstage_all + size_t(e) * kCosStage;
+            if (lane == 0) bulk_wait_read0();            // the previous chunk's store has read the stage
+            __syncwarp();
+            const uint32_t row = smem_u32(cst) + uint32_t(lane) * 128u;
+#pragma unroll
+            for (int j4 = 0; j4 < 8; ++j4)
+              sts128(row + (uint32_t(j4 ^ (lane & 7)) << 4), sc[4 * j4], sc[4 * j4 + 1], sc[4 * j4 + 2],
+                     sc[4 * j4 + 3]);
+            fence_proxy_async_smem();
+            __syncwarp();
+            if (lane == 0) {
+              tma_store_2d(&tm_cos, cst, int(yc), rank * UM_M + (qd % QA) * 32);
+              bulk_commit();
+            }
+          }
+        } else if (SEM && !TRAJ && p.out_cos && live) {
           float* op = p.out_cos + int64_t(p.cand_q0 + qg) * p.cos_stride + yc;
           const int nv = nvalid_rows(yc, p.n_rows, live);
 #pragma unroll
@@ -752,6 +843,7 @@ __global__ void __launch_bounds__(kUmThreads, 1)
           p.trace[12288 + (tid - 128) * 18 + a * 6 + b] =
               a == 2 && b == 5 ? n_cand_rest : a == 0 && b == 5 ? g_init : a == 1 && b == 5 ? g : cyc[a][b];
 #endif
+    if (SEM && !TRAJ && p.out_cos && p.cos_tma && lane == 0) bulk_wait_all0();   // cosines written
     // fold the 2R column-group lists of each query into group 0's heap, then
     // one list per (query, CTA) goes out
     if (live && cnt < k) heapify(ml_s, uint32_t(LQ) * 8, k);   // empty slots are key 0
@@ -929,7 +1021,8 @@ static int cg_of(const UmmaPlanIn& in) { return in.cg > 0 ? in.cg : (in.nq > UM_
 // of k keys per query of the CTA, within 216 KB (+ ~10 KB static <= 227 KB)
 static size_t lists_bytes(const UmmaPlanIn& in, int R) {
   const int nq = in.nq < UM_M ? in.nq : UM_M;
-  return size_t(2 * R) * in.k * ((nq + 31) / 32 * 32) * 8;
+  return size_t(2 * R) * in.k * ((nq + 31) / 32 * 32) * 8 + (in.cos_out ? size_t(cos_stage_bytes(true)) : 0) +
+         (in.cos_in ? size_t(cos_stage_bytes(false)) : 0);
 }
 // (planning uses TN = 256, the larger stage: a launch at TN = 128 fits as many)
 static int stages_for(const UmmaPlanIn& in, int R, int tn = UM_N) {
@@ -989,12 +1082,18 @@ cudaError_t launch_umma(const UmmaLaunch& L, cudaStream_t s) {
   const int CG = cg_of(in);
   // tcgen05 fp32 accumulation is not round-to-nearest per step: over D/16 = 256
   // MMAs (D = 4096) the semantic dot drifted by ~1.4e-5 relative (measured,
-  // C5).  Splitting K over two accumulators halves the chain; the epilogue adds
-  // them in IEEE fp32 (D >= 3072; measured: D = 2048 stays within 7e-6).
+  // C5).  Two ways to keep the 1e-5 contract:
+  //  * approx (semantic searches, k <= kApproxMaxK): ONE accumulator (TMEM
+  //    double-buffered, the epilogue overlaps the next tile's MMAs), lists of
+  //    k_ext > k approximate candidates, then an exact fp64 re-rank of the
+  //    candidates with a verified margin (rerank_kernel) and an exact GEMV
+  //    fallback for any query whose margin does not hold;
+  //  * otherwise split K over two accumulators (the epilogue adds them in IEEE
+  //    fp32; D >= 3072; measured: D = 2048 stays within 7e-6).
   // Blends weight the semantic part by d/L and their trajectory K is short,
   // so they keep one accumulator per part.
   const int n_sem_kb = sem ? (in.Dp + 63) / 64 : 0;
-  const int split_kb = (sem && !traj && n_sem_kb >= 48) ? n_sem_kb / 2 : 0;
+  const int split_kb = (sem && !traj && !in.approx && n_sem_kb >= 48) ? n_sem_kb / 2 : 0;
   // Two accumulators per tile (blend or split) single-buffer the 256-row tile's
   // TMEM.  128-row tiles keep the double buffer (2 x 2 x 128 columns) but
   // measured slower: the epilogue, not the serialisation, paces these scans.
@@ -1031,7 +1130,25 @@ cudaError_t launch_umma(const UmmaLaunch& L, cudaStream_t s) {
                              traj ? 1 : 0, MQ / R, L.gthr, sd, L.gate);
   if (e != cudaSuccess) return e;
   // 2. tensor maps
-  CUtensorMap tq_s{}, te_s{}, tq_t{}, tm_t{};
+  CUtensorMap tq_s{}, te_s{}, tq_t{}, tm_t{}, tc_o{};
+  // cosine side output: fp32 [nq][cos_stride] rows of this pass, box 32 x 32 with
+  // the 128-byte swizzle; TMA clips rows >= nq and columns >= n_rows
+  const bool cos_tma = (in.cos_out && L.out_cos && sem && !traj && (L.cos_stride % 4) == 0 &&
+                        (reinterpret_cast<uintptr_t>(L.out_cos) & 15) == 0) ||
+                       (in.cos_in && L.sem_cos && !sem && traj && (L.cos_stride % 4) == 0 &&
+                        (reinterpret_cast<uintptr_t>(L.sem_cos) & 15) == 0);
+  if (cos_tma) {
+    EncodeFn enc = encoder();
+    cuuint64_t dims[2] = {cuuint64_t(in.n_rows), cuuint64_t(in.nq)};
+    cuuint64_t strides[1] = {cuuint64_t(L.cos_stride) * 4};
+    cuuint32_t box[2] = {32, 32};
+    cuuint32_t es[2] = {1, 1};
+    void* base = sem ? static_cast<void*>(L.out_cos) : const_cast<float*>(L.sem_cos);
+    if (!enc || enc(&tc_o, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, base, dims, strides, box, es,
+                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+      return cudaErrorInvalidValue;
+  }
   if (sem) {
     if (!make_map(&tq_s, qs, in.Dp, MQ, 64, UM_M, CU_TENSOR_MAP_SWIZZLE_128B) ||
         !make_map(&te_s, in.emb, in.Dp, in.cap, 64, um_rows(CG, TN), CU_TENSOR_MAP_SWIZZLE_128B))
@@ -1075,7 +1192,10 @@ cudaError_t launch_umma(const UmmaLaunch& L, cudaStream_t s) {
     p.epi_sleep = es_env >= 0 ? es_env : 0;
     static const int fk_env = getenv("FMOE_FAKE_LOADS") ? atoi(getenv("FMOE_FAKE_LOADS")) : 0;
     p.fake_loads = fk_env;   // measured neutral (64..1000 ns); kept as a knob
+    static const int na_env = getenv("FMOE_NO_A_RELOAD") ? atoi(getenv("FMOE_NO_A_RELOAD")) : 0;
+    p.no_a_reload = na_env;
   }
+  p.cos_tma = cos_tma ? 1 : 0;
   p.cap = in.cap;
   p.L = in.L;
   p.maps = static_cast<const unsigned char*>(in.maps);
@@ -1095,7 +1215,8 @@ cudaError_t launch_umma(const UmmaLaunch& L, cudaStream_t s) {
   p.gthr = L.gthr;
   p.gate = L.gate;
   const size_t smem = 1024 + size_t(p.stages) * um_stage_bytes(CG, TN) + lists;
-  using Fn = void (*)(const CUtensorMap, const CUtensorMap, const CUtensorMap, const CUtensorMap, const UmmaParams);
+  using Fn = void (*)(const CUtensorMap, const CUtensorMap, const CUtensorMap, const CUtensorMap, const CUtensorMap,
+                     const UmmaParams);
 #define FMOE_UMMA_PICK(CGV, TNV)                                                      \
   (sem && traj ? scan_umma_kernel<true, true, CGV, TNV>                               \
    : sem       ? scan_umma_kernel<true, false, CGV, TNV>                              \
@@ -1116,7 +1237,7 @@ cudaError_t launch_umma(const UmmaLaunch& L, cudaStream_t s) {
     }
   }
   count_launch();
-  if (CG == 1) return launch_pdl(fn, dim3(L.grid), dim3(kUmThreads), smem, s, tq_s, te_s, tq_t, tm_t, p);
+  if (CG == 1) return launch_pdl(fn, dim3(L.grid), dim3(kUmThreads), smem, s, tq_s, te_s, tq_t, tm_t, tc_o, p);
   // CTA pairs: clusters of 2 (one TPC), with programmatic dependent launch
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(L.grid);
@@ -1132,7 +1253,7 @@ cudaError_t launch_umma(const UmmaLaunch& L, cudaStream_t s) {
   at[1].val.clusterDim.z = 1;
   cfg.attrs = at;
   cfg.numAttrs = 2;
-  return cudaLaunchKernelEx(&cfg, fn, tq_s, te_s, tq_t, tm_t, p);
+  return cudaLaunchKernelEx(&cfg, fn, tq_s, te_s, tq_t, tm_t, tc_o, p);
 }
 
 }  // namespace fmoe

@@ -371,6 +371,106 @@ fmoe_status run_search_umma(const fmoe_store* st, UmmaPlanIn in, int64_t B, cons
   return e == cudaSuccess ? FMOE_OK : cuda_fail(e, "merge launch");
 }
 
+// Approximate tensor-core semantic scan + exact re-rank (rerank.cu): the scan
+// keeps ke > k candidates per query from ONE TMEM accumulator (double-buffered
+// tiles), the merge keeps the best ke, rerank_kernel recomputes Eq. 1 exactly
+// for them and verifies the margin; queries that fail it are rescanned exactly
+// by gated GEMV passes (none in practice) whose results are scattered back.
+constexpr int kApproxMaxK = 48;
+int approx_list_len(int k) {
+  const int a = k + 8 > 2 * k ? k + 8 : 2 * k;
+  return a < kMaxK ? a : kMaxK;
+}
+
+fmoe_status run_search_umma_approx(const fmoe_store* st, UmmaPlanIn in, int64_t B, const float* dq, cudaStream_t s,
+                                   float* ds, int64_t* di, uint64_t* dkeys, const CosArgs& cos, int k) {
+  const int ke = in.k;
+  in.cg = umma_cg(in);
+  const int grid = umma_grid(in);
+  in.rep = umma_rep(in);
+  const int pass = in.cg * 128;
+  const int n_lists = grid / in.cg;
+  const int D = st->cfg.D;
+  // fallback GEMV geometry
+  ScanArgs g{};
+  g.st = st->view();
+  g.n_rows = in.n_rows;
+  g.ell = 0;
+  g.w_sem = 1.f;
+  g.k = k;
+  g.nq = 4;
+  g.id_offset = in.id_offset;
+  g.grid = scan_gemv_grid(g);
+  const int npass_g = int((B + 3) / 4);
+  const size_t cand_b = align_up(size_t(B) * n_lists * ke * 8), valid_b = align_up(size_t(B) * 4);
+  const size_t prep_b = align_up(umma_scratch_bytes(in)), gthr_b = align_up(size_t(B) * 8);
+  const size_t mk_b = align_up(size_t(B) * ke * 8), qc_b = align_up(size_t(B) * D * 4), qmap_b = align_up(size_t(B) * 4);
+  const size_t fbs_b = align_up(size_t(B) * k * 4), fbi_b = align_up(size_t(B) * k * 8);
+  const size_t gc_b = align_up(size_t(4) * g.grid * k * 8);
+  char* buf = nullptr;
+  unsigned* counters = nullptr;
+  unsigned long long* best = nullptr;
+  fmoe_status cs = stream_scratch(st, s, cand_b + valid_b + prep_b + gthr_b + mk_b + qc_b + qmap_b + fbs_b + 2 * fbi_b +
+                                  size_t(npass_g) * gc_b, npass_g + 1, int(B), &buf, &counters, &best);
+  if (cs != FMOE_OK) return cs;
+  char* c = buf;
+  uint64_t* cand = reinterpret_cast<uint64_t*>(c); c += cand_b;
+  float* valid = reinterpret_cast<float*>(c); c += valid_b;
+  char* prep = c; c += prep_b;
+  unsigned long long* gthr = reinterpret_cast<unsigned long long*>(c); c += gthr_b;
+  uint64_t* mkeys = reinterpret_cast<uint64_t*>(c); c += mk_b;
+  float* qc = reinterpret_cast<float*>(c); c += qc_b;
+  int* qmap = reinterpret_cast<int*>(c); c += qmap_b;
+  float* fb_s = reinterpret_cast<float*>(c); c += fbs_b;
+  int64_t* fb_i = reinterpret_cast<int64_t*>(c); c += fbi_b;
+  uint64_t* fb_k = reinterpret_cast<uint64_t*>(c); c += fbi_b;
+  uint64_t* gcand = reinterpret_cast<uint64_t*>(c);
+  int* nfail = reinterpret_cast<int*>(counters + npass_g);    // zero between calls (the scatter resets it)
+  for (int64_t q0 = 0; q0 < B; q0 += pass) {
+    UmmaLaunch L{};
+    L.in = in;
+    L.in.nq = int(B - q0 < pass ? B - q0 : pass);
+    L.q_emb = dq + q0 * D;
+    L.scratch = prep;
+    L.valid = valid + q0;
+    L.gthr = gthr + q0;
+    L.cand = cand;
+    L.cand_q0 = int(q0);
+    L.grid = grid;
+    L.trace = trace_buffer();
+    L.out_cos = cos.out ? cos.out + q0 * cos.stride : nullptr;
+    L.cos_stride = cos.stride;
+    cudaError_t e = launch_umma(L, s);
+    if (e != cudaSuccess) return cuda_fail(e, "umma scan launch");
+  }
+  cudaError_t e = launch_merge_keys(int(B), n_lists, ke, cand, ke, nullptr, nullptr, nullptr, mkeys, s);
+  if (e != cudaSuccess) return cuda_fail(e, "merge launch");
+  RerankArgs r{};
+  r.B = int(B); r.ke = ke; r.k = k; r.keys = mkeys; r.q_emb = dq; r.D = D; r.Dp = st->Dp; r.emb = st->emb;
+  r.r_e = st->r_e; r.id_offset = in.id_offset; r.valid = valid;
+  // |approx - exact| <= (MMAs per dot) * 4 ulp of the largest partial sum
+  // (relative to ||q|| ||e||, P:461-466 cosine scale) + epilogue roundings
+  r.eps = float(double((st->Dp + 15) / 16) * std::ldexp(1.0, -21) + std::ldexp(1.0, -20));
+  r.out_score = ds; r.out_id = di; r.out_keys = dkeys; r.nfail = nfail; r.qmap = qmap; r.qc = qc;
+  if ((e = launch_rerank(r, s)) != cudaSuccess) return cuda_fail(e, "rerank launch");
+  g.q_emb = qc;
+  g.out_score = fb_s;
+  g.out_id = fb_i;
+  g.out_keys = fb_k;
+  g.best = best;
+  g.check_valid = 1;
+  g.trace = trace_buffer();
+  g.run_if_gt = nfail;
+  for (int p = 0; p < npass_g; ++p) {
+    g.q0 = 4 * p;
+    g.counter = counters + p;
+    g.cand = gcand + size_t(p) * (gc_b / 8);
+    if ((e = launch_scan_gemv(g, s)) != cudaSuccess) return cuda_fail(e, "fallback scan launch");
+  }
+  e = launch_rerank_scatter(nfail, qmap, k, fb_s, fb_i, fb_k, ds, di, dkeys, nfail, s);
+  return e == cudaSuccess ? FMOE_OK : cuda_fail(e, "rerank scatter launch");
+}
+
 // One scoring call: GEMV scan passes of <= 4 queries, each merging its
 // candidates in its last block.  `extra` bytes of scratch are reserved after
 // the candidate lists (returned in *extra_ptr) for the caller.
@@ -387,7 +487,18 @@ fmoe_status run_search(const fmoe_store* st, int64_t B, const float* dq, const f
     return e == cudaSuccess ? FMOE_OK : cuda_fail(e, "merge launch");
   }
   UmmaPlanIn in{};
+  static const bool no_approx = getenv("FMOE_NO_APPROX") != nullptr;   // knob: the K-split precise scan
+  if (!no_approx && w == 1.f && !cos.in && !seed_ids && !gate && k <= kApproxMaxK &&
+      umma_plan(st, B, approx_list_len(k), 0, 1.f, n_rows, id_offset, &in)) {
+    in.approx = 1;
+    in.cos_out = cos.out != nullptr;
+    if (umma_supported(in)) return run_search_umma_approx(st, in, B, dq, s, ds, di, dkeys, cos, k);
+  }
   if (umma_plan(st, B, k, ell, w, n_rows, id_offset, &in)) {
+    in.cos_out = cos.out != nullptr && w == 1.f;
+    in.cos_in = cos.in != nullptr && w != 1.f;
+    if (in.cos_out && !umma_supported(in)) in.cos_out = 0;   // no room for the staging: direct stores
+    if (in.cos_in && !umma_supported(in)) in.cos_in = 0;     // no room for the ring: direct loads
     if (out_stride && k_out > k) *out_stride = k_out;
     return run_search_umma(st, in, B, dq, dp, q_stride, s, ds, di, dkeys, check_queries, cos, seed_ids, seed_stride,
                            seed_n, k_out, gate);

@@ -104,13 +104,10 @@ def _batches(dt):
 def test_semantic_midsize(mid):
     st, dt, sh = mid["st"], mid["dt"], mid["sh"]
     for B, k in _batches(dt):
-        qe, _, planted = _q(mid, B)
+        qe, _, _ = _q(mid, B)
         gs, gi = st.search_semantic(qe.cuda(), k)
         ref = O.semantic_scores(O.quantize(qe.numpy(), dt), mid["Qe"])
         check_topk_fast(gs, gi, ref, k)
-        for x in range(B):
-            if planted[x] >= 0:
-                assert gi[x, 0].item() == planted[x].item()
 
 
 @pytest.mark.parametrize("ell", [1, 3, "L"])

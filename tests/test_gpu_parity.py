@@ -731,3 +731,25 @@ def test_blend_cos_equals_blend(setup, B, k, ell, w):
     check_topk(s2, i2, ref, k)
     with pytest.raises(lib.FmoeError):                       # w = 1 is the semantic search itself
         lib.fmoe_search_blend_cos(st._h, cos, stride, qp.cuda(), ell, 1.0, k, s2, i2)
+
+
+@pytest.mark.parametrize("B,k", [(6, 1), (8, 8), (40, 16)])
+def test_semantic_rerank_fallback_on_ties(lib, B, k):
+    """The tensor-core semantic scan keeps k_ext > k approximate candidates and
+    re-ranks them exactly; with more than k_ext stored copies of the query's
+    best row the candidate list cannot prove completeness, so the query goes
+    to the exact GEMV fallback: the lowest ids of the tied rows win,
+    exactly as in the oracle."""
+    sh = SHAPES["mixtral_tiny"]
+    N = 3000
+    emb, maps, _ = S.store_rows(sh, 31, 0, N)
+    emb[100:180] = emb[7]                          # 80 exact copies of row 7
+    st = lib.ExpertMapStore(sh.L, sh.E, sh.K, sh.D, 3, N, "bf16")
+    st.insert(emb.cuda(), maps.cuda())
+    q = emb[7:8].repeat(B, 1).clone()
+    q[B // 2:] = emb[200:200 + B - B // 2]         # the other half: ordinary rows (no ties)
+    gs, gi = st.search_semantic(q.cuda(), k)
+    ref = O.semantic_scores(O.quantize(q.numpy(), "bf16"), O.quantize(emb.numpy(), "bf16"))
+    check_topk(gs, gi, ref, k)
+    assert gi[0].tolist() == ([7] + list(range(100, 100 + k - 1)))[:k]
+    st.close()

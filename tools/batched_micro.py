@@ -42,7 +42,12 @@ def main():
     out_s = torch.empty(a.B, a.k, device="cuda")
     out_i = torch.empty(a.B, a.k, dtype=torch.int64, device="cuda")
     pre = qm[:, :a.ell].contiguous()
+    stride = (a.n + 3) // 4 * 4
+    cos = torch.empty(a.B, stride, device="cuda") if "cos" in a.only else None
     calls = {
+        "semantic_cos": (lambda: fm.fmoe_search_semantic_cos(st._h, qe, a.k, out_s, out_i, cos, stride), a.D),
+        "blend_cos": (lambda: fm.fmoe_search_blend_cos(st._h, cos, stride, pre, a.ell, -1.0, a.k, out_s, out_i),
+                      a.ell * a.E),
         "semantic": (lambda: fm.fmoe_search_semantic(st._h, qe, a.k, out_s, out_i), a.D),
         "trajectory": (lambda: fm.fmoe_search_trajectory(st._h, pre, a.ell, a.k, out_s, out_i), a.ell * a.E),
         "blend": (lambda: fm.fmoe_search_blend(st._h, qe, pre, a.ell, -1.0, a.k, out_s, out_i), a.D + a.ell * a.E),
@@ -64,7 +69,7 @@ def main():
         st.close()
         return
     for name, (fn, kdim) in calls.items():
-        if a.only and name not in a.only.split(","):
+        if (a.only and name not in a.only.split(",")) or (not a.only and name.endswith("_cos")):
             continue
         fn()
         torch.cuda.synchronize()
@@ -79,7 +84,7 @@ def main():
         ev1.record()
         torch.cuda.synchronize()
         us = ev0.elapsed_time(ev1) * 1e3 / a.reps
-        gb = a.n * kdim * 2 / us / 1e3
+        gb = (a.n * kdim * 2 + (a.n * a.B * 4 if name.endswith("_cos") else 0)) / us / 1e3
         tf = 2.0 * a.B * a.n * kdim / us / 1e6
         print(f"{name:10s} B={a.B} n={a.n}: {us:9.1f} us  {gb:7.1f} GB/s  {tf:7.1f} TFLOP/s", flush=True)
     st.close()
