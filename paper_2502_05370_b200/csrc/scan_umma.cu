@@ -234,6 +234,10 @@ struct UmmaParams {
   int L;                // map layers (slabs)
   const unsigned char* maps;   // map slabs (bulk-copy path, RB = 16)
   const unsigned char* qt;     // trajectory query operand [CG][ell_pad][128][Ep] (bulk-copy path)
+  const unsigned char* qs;     // semantic query operand, UMMA-tiled [CG][n_sem_kb][128][128 B] (SW128 image)
+  const void* emb_raw;         // experiment knob FMOE_TILED_B_EXP
+  size_t emb_bytes;
+  int tiled_b_exp;
   uint32_t id_offset;
   const float* rq_s;    // [128] query inverse norms (0 for padding rows)
   const float* rq_t;
@@ -254,6 +258,8 @@ struct UmmaParams {
   int cos_tma;                  // semantic scans: out_cos written through a swizzled smem stage + TMA
                                 // tensor stores; trajectory scans: sem_cos read by per-warp TMA loads
                                 // (a 3-buffer ring, 2 chunks ahead) instead of lane-per-query loads
+  int no_epi;                   // debug knob (FMOE_NO_EPI=1): the epilogue only hands the accumulators
+                                // back (measures the MMA + feed pipeline alone; results garbage)
   int no_a_reload;              // debug knob (FMOE_NO_A_RELOAD=1): query operand loaded only into the
                                 // first ring pass, reused stale afterwards (results garbage; measures
                                 // the L2 traffic of re-reading it per tile)
@@ -384,7 +390,7 @@ __global__ void __launch_bounds__(kUmThreads, 1)
     mbar_fence_init();
   }
   if (warp == 0 && lane == 0) {
-    if (SEM) { tma_prefetch(&tm_qs); tma_prefetch(&tm_es); }
+    if (SEM) tma_prefetch(&tm_es);
     if (TRAJ) { tma_prefetch(&tm_qt); tma_prefetch(&tm_mt); }
   }
   if (warp == 2) {
@@ -447,6 +453,7 @@ __global__ void __launch_bounds__(kUmThreads, 1)
             if (++pkb == n_kb) { pkb = 0; pt += ncl; }
           }
           mbar_wait(&empty[s], ((u / unsigned(S)) & 1u) ^ 1u);
+          if (p.trace && blockIdx.x == 0 && u < 1024u) p.trace[16384 + u] = globaltimer();
           unsigned char* sa = smem + size_t(s) * SBY;
           unsigned char* sb = sa + kStageA;
           if (p.fake_loads) {                    // debug: MMAs on stale smem (feed excluded)
@@ -456,7 +463,19 @@ __global__ void __launch_bounds__(kUmThreads, 1)
           if (SEM && kb < p.n_sem_kb) {
             const bool load_a = !p.no_a_reload || u < unsigned(S);
             mbar_arrive_expect_tx(&full[s], unsigned(load_a ? SBY : SBY - kStageA));
-            if (load_a) tma_load_2d(sa, &tm_qs, kb * 64, rank * UM_M, &full[s]);
+            if (load_a) bulk_g2s_plain(sa, p.qs + (size_t(rank) * p.n_sem_kb + kb) * kStageA, kStageA, &full[s]);
+            if constexpr (TN == 512) {
+              // two 128-row boxes: the halves this CTA feeds to the two N = 256 MMAs
+              // (rows t*512 + g*256 + rank*128: TMEM column g*256 + j is row t*512 + g*256 + j)
+              tma_load_2d(sb, &tm_es, kb * 64, t * TN + rank * UM_M, &full[s]);
+              tma_load_2d(sb + UM_M * 128, &tm_es, kb * 64, t * TN + 256 + rank * UM_M, &full[s]);
+            } else if (p.tiled_b_exp) {
+              // experiment: the same bytes as contiguous 16 KB blocks (results garbage)
+              const unsigned char* eb = static_cast<const unsigned char*>(p.emb_raw);
+              for (int h = 0; h < NB / 128; ++h)
+                bulk_g2s(sb + h * 16384, eb + ((size_t(y0 / 128 + h) * p.n_sem_kb + kb) * 16384) % p.emb_bytes,
+                         16384u, &full[s], pol);
+            } else
             tma_load_2d(sb, &tm_es, kb * 64, y0, &full[s]);
           } else {
             const int j = kb - p.n_sem_kb;
@@ -509,7 +528,7 @@ __global__ void __launch_bounds__(kUmThreads, 1)
   } else if (warp == 1) {
     // ---------------------------------------------------------------- MMA issuer
     if (lane == 0) {
-      constexpr uint32_t idesc = umma_idesc(UM_M * CG, TN);
+      constexpr uint32_t idesc = umma_idesc(UM_M * CG, TN > 256 ? 256 : TN);
       unsigned u = 0, ti = 0;
       for (int t = cid; t < p.n_tiles; t += ncl, ++ti) {
         const int as = int(ti % unsigned(AS));
@@ -520,6 +539,7 @@ __global__ void __launch_bounds__(kUmThreads, 1)
         for (int kb = 0; kb < n_kb; ++kb, ++u) {
           const int s = int(u % unsigned(S));
           mbar_wait(&full[s], (u / unsigned(S)) & 1u);
+          if (p.trace && blockIdx.x == 0 && u < 1024u) p.trace[17408 + u] = globaltimer();
           tc_fence_after();
           const unsigned char* sa = smem + size_t(s) * SBY;
           const unsigned char* sb = sa + kStageA;
@@ -528,9 +548,13 @@ __global__ void __launch_bounds__(kUmThreads, 1)
             const uint32_t d = hi ? d_trj : d_sem;
             const int kb0 = hi ? p.split_kb : 0;
 #pragma unroll
-            for (int kk = 0; kk < 4; ++kk)
+            for (int kk = 0; kk < 4; ++kk) {
               tc_mma<CG>(d, umma_desc(sa + kk * 32, 16, 1024, 2), umma_desc(sb + kk * 32, 16, 1024, 2), idesc,
                          (kb != kb0 || kk) ? 1u : 0u);
+              if constexpr (TN == 512)      // second N = 256 column group, same A
+                tc_mma<CG>(d + 256, umma_desc(sa + kk * 32, 16, 1024, 2),
+                           umma_desc(sb + UM_M * 128 + kk * 32, 16, 1024, 2), idesc, (kb != kb0 || kk) ? 1u : 0u);
+            }
           } else {
             const int j = kb - p.n_sem_kb;
             const int l0 = j * p.lc;
@@ -640,7 +664,19 @@ __global__ void __launch_bounds__(kUmThreads, 1)
       cos_issue(1);
     }
     unsigned ci = 0;                                    // this warp's chunk sequence number
-    for (int t = cid; t < p.n_tiles; t += ncl, ++ti) {
+    if (p.no_epi) {
+      for (int t = cid; t < p.n_tiles; t += ncl, ++ti) {
+        const int as = int(ti % unsigned(AS));
+        mbar_wait(&tfull[as], (ti / unsigned(AS)) & 1u);
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) {
+          if (CG == 2 && !leader) mbar_arrive_remote(mapa_rank(&tempty[as], 0));
+          else mbar_arrive(&tempty[as]);
+        }
+      }
+    }
+    for (int t = p.no_epi ? p.n_tiles : cid; t < p.n_tiles; t += ncl, ++ti) {
       const int as = int(ti % unsigned(AS));
       const int ybase = t * TN + half * HC + sub * NC * 32;     // first column of this warp
       // this warp's copy of the half tile's row scales, read back as broadcast
@@ -910,9 +946,16 @@ __global__ void __launch_bounds__(256) umma_prep_kernel(const float* __restrict_
   const bool live = x < nq;
   double a = 0.0, b = 0.0;
   if (sem) {
-    for (int e = tid; e < Dp; e += 256) {
+    // UMMA-tiled: [q / 128][k-block][128 rows][128 B], 16-byte groups swizzled
+    // within each 8-row atom (group c of row r at c ^ (r & 7), the SWIZZLE_128B
+    // K-major image), so a k-block of 128 query rows is one contiguous 16 KB
+    // block that one 1-D bulk copy moves (a 2-D tensor box costs one TMA
+    // request per 128-byte row)
+    const int nkb = (Dp + 63) / 64, half = q / UM_M, r = q % UM_M;
+    for (int e = tid; e < nkb * 64; e += 256) {
       const float v = (live && e < D) ? __bfloat162float(__float2bfloat16_rn(q_emb[int64_t(x) * D + e])) : 0.f;
-      qs[int64_t(q) * Dp + e] = __float2bfloat16_rn(v);
+      const int kb = e >> 6, c = (e & 63) >> 3;
+      qs[((int64_t(half) * nkb + kb) * UM_M + r) * 64 + ((c ^ (r & 7)) << 3) + (e & 7)] = __float2bfloat16_rn(v);
       a += double(v) * double(v);
     }
   }
@@ -1025,13 +1068,24 @@ static size_t lists_bytes(const UmmaPlanIn& in, int R) {
          (in.cos_in ? size_t(cos_stage_bytes(false)) : 0);
 }
 // (planning uses TN = 256, the larger stage: a launch at TN = 128 fits as many)
+// Semantic-only approximate scans on CTA pairs use 512-row tiles: two N = 256
+// MMAs per K step share the query operand A, so a stage carries 16 KB of A for
+// 32 KB of store rows (per CTA) instead of 16 + 16 -- the scan is paced by the
+// bytes the L2 delivers per SM, and A is re-read for every tile.  The 512 TMEM
+// columns then hold one tile (single-buffered accumulator).
+static int umma_tn(const UmmaPlanIn& in, int cg) {
+  static const int tn_env = getenv("FMOE_UMMA_TN") ? atoi(getenv("FMOE_UMMA_TN")) : 0;
+  if (tn_env == 128) return 128;
+  if (tn_env != 256 && cg == 2 && in.approx && in.w_sem == 1.f) return 512;
+  return UM_N;
+}
 static int stages_for(const UmmaPlanIn& in, int R, int tn = UM_N) {
   const size_t l = lists_bytes(in, R);
   if (l + 1024 > 216 * 1024) return 0;
   const int cg = cg_of(in);
   const int S = int((216 * 1024 - 1024 - l) / size_t(um_stage_bytes(cg, tn)));
   static const int env = getenv("FMOE_UMMA_STAGES") ? atoi(getenv("FMOE_UMMA_STAGES")) : 0;
-  const int cap = env > 0 ? env : (tn == UM_N ? (cg == 2 ? 6 : 4) : kUmMaxStages);
+  const int cap = env > 0 ? env : (tn == 512 ? 4 : tn == UM_N ? (cg == 2 ? 6 : 4) : kUmMaxStages);
   return S > cap ? cap : S;
 }
 // Query replication: nq <= 32 uses one TMEM lane quadrant, nq <= 64 two; the
@@ -1056,7 +1110,7 @@ bool umma_supported(const UmmaPlanIn& in) {
 // scratch layout (MQ = 256 rows, enough for either CTA mode):
 //   qs [MQ][Dp] bf16 | qt [CG][ell+2][128][Ep] bf16 | rq_s, rq_t [MQ] f32
 constexpr int kMQ = 2 * UM_M;
-static size_t qt_offset(const UmmaPlanIn& in) { return size_t(kMQ) * in.Dp * 2; }
+static size_t qt_offset(const UmmaPlanIn& in) { return size_t(kMQ) * ((in.Dp + 63) / 64 * 64) * 2; }
 static size_t rq_offset(const UmmaPlanIn& in) { return qt_offset(in) + size_t(in.ell + 2) * kMQ * in.Ep * 2; }
 size_t umma_scratch_bytes(const UmmaPlanIn& in) { return rq_offset(in) + 2 * kMQ * 4 + 256; }
 
@@ -1069,7 +1123,8 @@ int umma_grid(const UmmaPlanIn& in) {
   }
   // one CTA (or CTA pair) per SM (pair of SMs), persistent over the tiles
   const int cg = cg_of(in);
-  const int64_t tiles = (in.n_rows + UM_N - 1) / UM_N;
+  const int tn = umma_tn(in, cg);
+  const int64_t tiles = (in.n_rows + tn - 1) / tn;
   const int64_t units = sms / cg;
   return cg * int(tiles < units ? (tiles < 1 ? 1 : tiles) : units);
 }
@@ -1101,8 +1156,7 @@ cudaError_t launch_umma(const UmmaLaunch& L, cudaStream_t s) {
   // and 0.68 at 128 rows; B = 256 on CTA pairs went 5.5 -> 13.1 ms.  Kept as an
   // experiment knob (FMOE_UMMA_TN=128).
   const bool nacc2 = (sem && traj) || split_kb > 0;
-  static const int tn_env = getenv("FMOE_UMMA_TN") ? atoi(getenv("FMOE_UMMA_TN")) : 0;
-  const int TN = tn_env == 128 ? 128 : UM_N;
+  const int TN = umma_tn(in, CG);
   int R = CG == 2 || in.rep < 1 ? 1 : in.rep;
   if (TN == 128 && R > 2) R = 2;                  // >= one 32-column chunk per replica
   const int MQ = UM_M * CG;
@@ -1150,8 +1204,7 @@ cudaError_t launch_umma(const UmmaLaunch& L, cudaStream_t s) {
       return cudaErrorInvalidValue;
   }
   if (sem) {
-    if (!make_map(&tq_s, qs, in.Dp, MQ, 64, UM_M, CU_TENSOR_MAP_SWIZZLE_128B) ||
-        !make_map(&te_s, in.emb, in.Dp, in.cap, 64, um_rows(CG, TN), CU_TENSOR_MAP_SWIZZLE_128B))
+    if (!make_map(&te_s, in.emb, in.Dp, in.cap, 64, TN == 512 ? UM_M : um_rows(CG, TN), CU_TENSOR_MAP_SWIZZLE_128B))
       return cudaErrorInvalidValue;
   }
   int tmode = 0, lc = 0, n_traj_kb = 0;
@@ -1184,7 +1237,7 @@ cudaError_t launch_umma(const UmmaLaunch& L, cudaStream_t s) {
   if (p.stages < 2) return cudaErrorInvalidValue;
   p.rep = R;
   p.split_kb = split_kb;
-  p.acc_stages = nacc2 && TN == UM_N ? 1 : 2;
+  p.acc_stages = (nacc2 && TN == UM_N) || TN == 512 ? 1 : 2;
   {
     static const int pf_env = getenv("FMOE_L2PF") ? atoi(getenv("FMOE_L2PF")) : -1;
     p.l2pf = pf_env >= 0 ? pf_env : 0;   // measured: no gain at either CTA mode (kept as a knob)
@@ -1194,12 +1247,21 @@ cudaError_t launch_umma(const UmmaLaunch& L, cudaStream_t s) {
     p.fake_loads = fk_env;   // measured neutral (64..1000 ns); kept as a knob
     static const int na_env = getenv("FMOE_NO_A_RELOAD") ? atoi(getenv("FMOE_NO_A_RELOAD")) : 0;
     p.no_a_reload = na_env;
+    static const int ne_env = getenv("FMOE_NO_EPI") ? atoi(getenv("FMOE_NO_EPI")) : 0;
+    p.no_epi = ne_env;
   }
   p.cos_tma = cos_tma ? 1 : 0;
   p.cap = in.cap;
   p.L = in.L;
   p.maps = static_cast<const unsigned char*>(in.maps);
   p.qt = reinterpret_cast<const unsigned char*>(qt);
+  p.qs = reinterpret_cast<const unsigned char*>(qs);
+  p.emb_raw = in.emb;
+  p.emb_bytes = size_t(in.cap) * in.Dp * 2 / 16384 * 16384;
+  {
+    static const int tb_env = getenv("FMOE_TILED_B_EXP") ? atoi(getenv("FMOE_TILED_B_EXP")) : 0;
+    p.tiled_b_exp = tb_env;
+  }
   p.id_offset = in.id_offset;
   p.rq_s = rq_s;
   p.rq_t = rq_t;
@@ -1221,7 +1283,8 @@ cudaError_t launch_umma(const UmmaLaunch& L, cudaStream_t s) {
   (sem && traj ? scan_umma_kernel<true, true, CGV, TNV>                               \
    : sem       ? scan_umma_kernel<true, false, CGV, TNV>                              \
                : scan_umma_kernel<false, true, CGV, TNV>)
-  const Fn fn = CG == 2 ? (TN == 128 ? FMOE_UMMA_PICK(2, 128) : FMOE_UMMA_PICK(2, 256))
+  const Fn fn = CG == 2 ? (TN == 512 ? scan_umma_kernel<true, false, 2, 512>
+                         : TN == 128 ? FMOE_UMMA_PICK(2, 128) : FMOE_UMMA_PICK(2, 256))
                         : (TN == 128 ? FMOE_UMMA_PICK(1, 128) : FMOE_UMMA_PICK(1, 256));
 #undef FMOE_UMMA_PICK
   {

@@ -95,6 +95,16 @@ def main():
         print("  CTA 0 per-tile timeline (us from kernel start): tile | tma_issued | mma_committed | epi_got | epi_done")
         for i in range(min(ntile, 12)):
             print("   ", i, " ".join(f"{(roles[r, i] - t0) / 1e3:8.2f}" for r in range(4)))
+        iss = flat[16384:16384 + 1024].astype(np.int64)
+        got = flat[17408:17408 + 1024].astype(np.int64)
+        nk = int((iss > 0).sum())
+        if nk:
+            lat = (got[:nk] - iss[:nk]) / 1e3
+            gap = np.diff(got[:nk]) / 1e3
+            print(f"  CTA 0 stages: n={nk} load issue->MMA-got latency med {np.median(lat):.2f} p10 {np.percentile(lat,10):.2f}"
+                  f" p90 {np.percentile(lat,90):.2f} us; MMA-got interval med {np.median(gap):.3f} us")
+            print("   first 24 (issue, got) us:", [(round((iss[i]-t0)/1e3,2), round((got[i]-t0)/1e3,2)) for i in range(min(24,nk))])
+            print("   steady 200..212:", [(round((iss[i]-t0)/1e3,2), round((got[i]-t0)/1e3,2)) for i in range(200, min(212,nk))])
         cy = flat[12288:12288 + 256 * 18].reshape(256, 3, 6).astype(np.int64)
         if cy.any():      # library built with -DFMOE_EPI_PROFILE
             print("  epilogue kcycles of lane 0 per warp [tfull bar tmem_ld fast rare other] (rest: other = candidates of the warp, tiles >= 2):")
