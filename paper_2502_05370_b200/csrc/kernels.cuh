@@ -159,6 +159,7 @@ struct UmmaLaunch {
   int seed_stride, seed_n;
   uint64_t* cand; int cand_q0; int grid;
   unsigned long long* trace;
+  int keep_gthr;               // 1: gthr already holds a valid admission bound (sample pass); prep keeps it
 };
 bool umma_supported(const UmmaPlanIn& in);
 int umma_rep(const UmmaPlanIn& in);
@@ -166,6 +167,7 @@ size_t umma_scratch_bytes(const UmmaPlanIn& in);
 int umma_grid(const UmmaPlanIn& in);   // CTAs to launch (a multiple of umma_cg)
 int umma_cg(const UmmaPlanIn& in);
 cudaError_t launch_umma(const UmmaLaunch& L, cudaStream_t s);
+cudaError_t launch_seed_from_sample(int B, int ke, const uint64_t* keys, unsigned long long* gthr, cudaStream_t s);
 // Exact re-rank of an approximate (single-accumulator) tensor-core semantic
 // scan's merged candidates (rerank.cu): [B][ke] keys -> the exact top k, and
 // the queries whose completeness margin fails, queued for the GEMV fallback.

@@ -852,6 +852,15 @@ __global__ void __launch_bounds__(kUmThreads, 1)
         }
         EPI_T(4);
       }
+      // hand the accumulator stage back first: the arrive is a release, and
+      // placed after the threshold's global red it would wait for that red's
+      // round trip (the MMA warp, not this warp, is what waits on it)
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) {                            // the leader's MMA waits for both CTAs' epilogues
+        if (CG == 2 && !leader) mbar_arrive_remote(mapa_rank(&tempty[as], 0));
+        else mbar_arrive(&tempty[as]);
+      }
       // publish this list's bound once per tile (atomics per insert contended
       // at k = 64), then take the shared one read at the start of this tile
       if (g > published) {
@@ -861,12 +870,6 @@ __global__ void __launch_bounds__(kUmThreads, 1)
       if (g_new > g) {
         g = g_new;
         thr_s = key_score(g);
-      }
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) {                            // the leader's MMA waits for both CTAs' epilogues
-        if (CG == 2 && !leader) mbar_arrive_remote(mapa_rank(&tempty[as], 0));
-        else mbar_arrive(&tempty[as]);
       }
       if (ti == 0 && tid == 128) trace_mark_here(p.trace, 1);
       if (tid == 128) tile_mark(p.trace, 3, ti);
@@ -937,7 +940,7 @@ __global__ void __launch_bounds__(256) umma_prep_kernel(const float* __restrict_
                                                         int ell_pad, __nv_bfloat16* qs, __nv_bfloat16* qt, float* rq_s,
                                                         float* rq_t, float* valid, int sem, int traj, int qper,
                                                         unsigned long long* gthr, const SeedArgs sd,
-                                                        const int* gate) {
+                                                        const int* gate, int keep_gthr) {
   pdl_wait();
   if (gate && *gate == 0) return;
   __shared__ double red[2][8];
@@ -983,7 +986,7 @@ __global__ void __launch_bounds__(256) umma_prep_kernel(const float* __restrict_
     rq_s[q] = sa > 0.0 ? float(1.0 / sqrt(sa)) : 0.f;
     rq_t[q] = sb > 0.0 ? float(1.0 / sqrt(sb)) : 0.f;
     if (live && q == x) valid[q] = ((!sem || sa > 0.0) && (!traj || sb > 0.0)) ? 1.f : 0.f;
-    if (live && q == x) gthr[q] = 0ull;
+    if (live && q == x && !keep_gthr) gthr[q] = 0ull;   // keep: seeded by a sample pass
     red[0][0] = sb > 0.0 ? 1.0 / sqrt(sb) : 0.0;
   }
   if (!(sd.ids && traj && !sem && live && q == x && sd.k > 0 && sd.n >= sd.k && sd.n <= 64)) return;
@@ -1022,6 +1025,20 @@ __global__ void __launch_bounds__(256) umma_prep_kernel(const float* __restrict_
       gthr[q] = uint64_t(orderable(lo)) << 32;    // below every key of score >= lo
     }
   }
+}
+
+// Admission bound from a sample pass (approx semantic scans): the ke-th best
+// approximate key of rows [0, S) -- those rows get bit-identical keys in the
+// full scan, so the full scan's ke-th best key is >= this one.
+__global__ void seed_from_sample_kernel(int B, int ke, const uint64_t* __restrict__ keys,
+                                        unsigned long long* gthr) {
+  pdl_wait();
+  const int x = blockIdx.x * blockDim.x + threadIdx.x;
+  if (x < B) gthr[x] = keys[int64_t(x) * ke + ke - 1];
+}
+cudaError_t launch_seed_from_sample(int B, int ke, const uint64_t* keys, unsigned long long* gthr, cudaStream_t s) {
+  count_launch();
+  return launch_pdl(seed_from_sample_kernel, dim3((B + 127) / 128), dim3(128), 0, s, B, ke, keys, gthr);
 }
 
 // ------------------------------------------------------------------ host side
@@ -1181,7 +1198,7 @@ cudaError_t launch_umma(const UmmaLaunch& L, cudaStream_t s) {
   count_launch();
   cudaError_t e = launch_pdl(umma_prep_kernel, dim3(MQ), dim3(256), 0, s, L.q_emb, L.q_prefix, L.q_stride, in.nq,
                              in.D, in.Dp, in.E, in.Ep, in.ell, ell_pad, qs, qt, rq_s, rq_t, L.valid, sem ? 1 : 0,
-                             traj ? 1 : 0, MQ / R, L.gthr, sd, L.gate);
+                             traj ? 1 : 0, MQ / R, L.gthr, sd, L.gate, L.keep_gthr);
   if (e != cudaSuccess) return e;
   // 2. tensor maps
   CUtensorMap tq_s{}, te_s{}, tq_t{}, tm_t{}, tc_o{};
