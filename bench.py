@@ -201,7 +201,8 @@ class Step:
                        torch.empty(n, B, dtype=torch.int32, device=st.device))
         # semantic cosines kept on the device for the RDY insert (fmoe_store_insert_cos):
         # the iteration's new context carries the embedding its semantic search used
-        n = len(st)
+        # (a sharded store's cosine side output holds this rank's local columns)
+        n = getattr(st, "cap_local", None) or len(st)
         self.stride = (n + 3) // 4 * 4
         # (B x N fp32; C5: 256 x 16M = 16.4 GB next to the 148 GB store -- allocated
         # when it leaves >= 6 GB of the device free)
@@ -418,65 +419,35 @@ def make_queries(cfg, N, pool, seed, dev):
     return qs
 
 
-class ShardedStep(Step):
-    """The same step on a store sharded over the ranks (paper_2502_05370_b200.dist):
-    local scans + one all-gather + merge kernel per search, all-reduce per select."""
-
-    def __init__(self, sst, cfg):
-        self.sst, self.cfg, self.sh = sst, cfg, cfg["shape"]
-
-    def run(self, q_emb, q_maps, new_emb, new_maps, ev=None):
-        sst, cfg, L, d, k = self.sst, self.cfg, self.sh.L, 3, self.cfg["k"]
-        out = {}
-
-        def rec(kind, fn):
-            if ev is None:
-                out["r"] = fn()
-                return
-            a = torch.cuda.Event(enable_timing=True)
-            b = torch.cuda.Event(enable_timing=True)
-            a.record()
-            out["r"] = fn()
-            b.record()
-            ev.setdefault(kind, []).append((a, b))
-
-        rec("semantic", lambda: sst.search_semantic(q_emb, k))
-        s, i = out["r"]
-        sst.select_experts(i[:, 0].contiguous(), s[:, 0].contiguous(), cfg["delta"], 0, d)
-        for ell in range(1, L):
-            pre, _ = q_maps[ell - 1]
-            rec(f"traj{ell}", lambda: sst.search_trajectory(pre, ell, k))
-            tgt = ell - 1 + d
-            if tgt < L:
-                s, i = out["r"]
-                sst.select_experts(i[:, 0].contiguous(), s[:, 0].contiguous(), cfg["delta"], tgt, tgt + 1)
-        rec("rdy_insert", lambda: sst.insert(new_emb, new_maps))
-
-
 def build_sharded(cfg, rank, world, dev, seed):
+    """The store sharded over the ranks by the library (fmoe_store_create_sharded):
+    every rank makes the same collective insert calls; each writes only its slots."""
     from paper_2502_05370_b200 import dist as fdist
     sh = cfg["shape"]
-    sst = fdist.ShardedExpertMapStore(sh.L, sh.E, sh.K, sh.D, 3, cfg["N"], cfg["dtype"], device=dev.index)
+    transport = os.environ.get("FMOE_DIST_TRANSPORT", "nccl")
+    sst = fdist.ShardedExpertMapStore(sh.L, sh.E, sh.K, sh.D, 3, cfg["N"], cfg["dtype"], device=dev.index,
+                                      transport=transport)
     chunk = 65536
-    for a in range(0, sst.cap_local, chunk):
-        c = min(chunk, sst.cap_local - a)
-        e, m, _ = S.store_rows(sh, seed, sst.offset + a, c, device=dev)
-        sst.b.append(e, m)                     # each rank fills its own slot range
-    sst.n_total = cfg["N"]
+    for a in range(0, cfg["N"], chunk):
+        c = min(chunk, cfg["N"] - a)
+        e, m, _ = S.store_rows(sh, seed, a, c, device=dev)
+        sst.insert(e, m)
     torch.cuda.synchronize(dev)
     return sst
 
 
 def run_fmoe(args, cfg, rank, world, local_rank):
     import paper_2502_05370_b200 as fm
-    dev = torch.device("cuda", local_rank)
+    dev = torch.device("cuda", bench_device(local_rank))
     torch.cuda.set_device(dev)
     N_total = cfg["N"]
     if world > 1:
-        sst = build_sharded(cfg, rank, world, dev, args.seed)
-        st = sst.b.store
-        N_local = sst.cap_local
-        step = ShardedStep(sst, cfg)
+        # the same Step: every ABI call on a sharded store is collective (local
+        # kernels + one in-library all-gather + merge), so N > 1 runs exactly
+        # the N = 1 calls (session sweep, cached cosines, blend, RDY insert)
+        st = build_sharded(cfg, rank, world, dev, args.seed)
+        N_local = st.cap_local
+        step = Step(fm, st, cfg, args.traj, args.cos)
     else:
         N_local = N_total
         st = build_store(fm, cfg, N_local, 0, dev, args.seed)
@@ -484,10 +455,10 @@ def run_fmoe(args, cfg, rank, world, local_rank):
     pool = 4
     qs = make_queries(cfg, N_total, pool, args.seed, dev)
     searches, n_traj = step_counts(cfg)
-    sem_b, traj_b, rdy_b = algorithmic_bytes(cfg, N_local, args.traj if world == 1 else "stateless",
-                                             getattr(step, "cos", None) is not None)
+    sem_b, traj_b, rdy_b = algorithmic_bytes(cfg, N_local, args.traj, getattr(step, "cos", None) is not None)
 
-    use_graph = args.graph and world == 1
+    # graphs at N > 1 need the NCCL transport (the HOST transport synchronises)
+    use_graph = args.graph and (world == 1 or os.environ.get("FMOE_DIST_TRANSPORT", "nccl") == "nccl")
     run_stream = torch.cuda.Stream(device=dev) if use_graph else torch.cuda.current_stream(dev)
     with torch.cuda.stream(run_stream):
         for w in range(args.warmup):               # also creates this stream's scratch
@@ -542,7 +513,7 @@ def run_fmoe(args, cfg, rank, world, local_rank):
     launches = int(round(launches_per_step * args.steps))
     clocks = clk.stop() if clk else None
     if world > 1:
-        t = torch.tensor([ms], device=dev)
+        t = torch.tensor([ms], device=dev if os.environ.get("FMOE_DIST_TRANSPORT", "nccl") == "nccl" else "cpu")
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
         ms = float(t.item())
         torch.distributed.barrier()
@@ -652,6 +623,11 @@ def cos_keys(cfg, cos):
         out["blend"] = ("semantic half reused from the step's semantic search (fmoe_search_blend_cos)"
                         if cos else "full blended scan (embeddings re-read)")
     return out
+
+
+def bench_device(local_rank):
+    """CUDA device of this rank: LOCAL_RANK, or FMOE_BENCH_DEVICE (ranks sharing one GPU, tests only)."""
+    return int(os.environ.get("FMOE_BENCH_DEVICE", local_rank))
 
 
 def sh_L(cfg):
@@ -824,8 +800,12 @@ def main():
         return
 
     if world > 1:
-        torch.cuda.set_device(local_rank)
-        torch.distributed.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        torch.cuda.set_device(bench_device(local_rank))
+        if os.environ.get("FMOE_DIST_TRANSPORT", "nccl") == "host":
+            # ranks sharing a GPU (tests): gloo for the plumbing and the store's HOST transport
+            torch.distributed.init_process_group("gloo")
+        else:
+            torch.distributed.init_process_group("nccl", device_id=torch.device("cuda", bench_device(local_rank)))
     res = run_fmoe(args, cfg, rank, world, local_rank)
     if rank != 0:
         torch.distributed.destroy_process_group()

@@ -82,11 +82,56 @@ typedef struct {
  * "HBM layout").  Errors: SHAPE for an illegal config, OOM, CUDA. */
 fmoe_status fmoe_store_create(const fmoe_store_config* cfg, int device, fmoe_store** out);
 
-/* Free the store and its tiles (device-synchronous).  NULL is a no-op. */
+/* Free the store and its tiles.  The caller guarantees that no work on the
+ * store is pending (as for any free); the store's scratch is released on the
+ * streams that used it.  NULL is a no-op. */
 void fmoe_store_destroy(fmoe_store* store);
 
-/* Number of occupied slots |S| (host counter; inserts update it when enqueued). */
+/* Number of occupied slots |S| (host counter; inserts update it when enqueued,
+ * a call that fails leaves it unchanged).  Sharded store: the GLOBAL size. */
 fmoe_status fmoe_store_size(const fmoe_store* store, int64_t* out_n);
+
+/* ---- sharded store over several GPUs ----------------------
+ * Rank r of G holds the global slots [r*P, min((r+1)*P, C)), P = ceil(C/G);
+ * store rows are independent, so every call is the single-GPU kernels on the
+ * local slots followed by ONE all-gather of a packed per-rank result and a
+ * merge on every rank: outputs are replicated on every rank and bit-identical
+ * to the unsharded store (a row's score does not depend on its rank; ties
+ * break by global id).  On a sharded store every call below is COLLECTIVE:
+ * every rank calls it, in the same order, with the same arguments (replicated
+ * queries / contexts, same k, ell, delta ...), except the cosine side outputs
+ * and inputs (fmoe_search_semantic_cos, fmoe_search_blend_cos,
+ * fmoe_store_insert_cos), which hold this rank's LOCAL columns
+ * [0, local size), and fmoe_store_read / fmoe_store_write, which are local
+ * (global slots; read needs a range inside this rank's shard).
+ * fmoe_prefetch_plan returns FMOE_ERR_UNSUPPORTED on a sharded store. */
+typedef enum {
+  FMOE_TRANSPORT_NCCL = 0,   /* ncclAllGather on the call's stream (NVLink / NVSwitch; CUDA-graph capturable) */
+  FMOE_TRANSPORT_HOST = 1    /* the caller's host all-gather (synchronous; e.g. gloo, or ranks sharing one GPU) */
+} fmoe_transport;
+
+/* HOST transport: gather `bytes` bytes of every rank's send (host memory) into
+ * recv [world][bytes] in rank order; return 0 on success. */
+typedef int32_t (*fmoe_allgather_fn)(const void* send, void* recv, int64_t bytes, void* user);
+
+typedef struct {
+  int32_t rank, world;            /* 0 <= rank < world                                       */
+  int32_t transport;              /* fmoe_transport                                          */
+  const void* nccl_unique_id;     /* NCCL: the 128 bytes of fmoe_get_nccl_unique_id, the same
+                                     on every rank (the caller distributes them)             */
+  fmoe_allgather_fn allgather;    /* HOST: the exchange                                       */
+  void* allgather_user;
+} fmoe_dist_config;
+
+/* 128 bytes identifying a new NCCL communicator (call on one rank, share). */
+fmoe_status fmoe_get_nccl_unique_id(void* out_128_bytes);
+
+/* Create this rank's shard of a store of cfg->capacity GLOBAL slots
+ * (cfg->id_offset must be 0; capacity >= world).  Collective (NCCL: every rank
+ * initialises the communicator).  Errors: as fmoe_store_create; FMOE_ERR_CUDA
+ * with the NCCL message when the communicator cannot be created. */
+fmoe_status fmoe_store_create_sharded(const fmoe_store_config* cfg, const fmoe_dist_config* dist, int device,
+                                      fmoe_store** out);
 
 /* Copy the configuration the store was created with. */
 fmoe_status fmoe_store_get_config(const fmoe_store* store, fmoe_store_config* out_cfg);
@@ -231,7 +276,9 @@ fmoe_status fmoe_traj_session_step_select(fmoe_traj_session* session, const floa
  * producer must not need this kernel's SMs to make progress); guidance_ready
  * [n_steps] -- set to 1 (release) once step s's outputs are written: the
  * device-side publisher/subscriber of P:528-533.  A layer not ready within
- * 10 s abandons the sweep (guidance flags stay 0; reset the session). */
+ * 10 s abandons the sweep: the steps not finished publish guidance_ready = 2
+ * (so a subscriber never waits forever), the session is poisoned until reset
+ * (fmoe_traj_session_abandoned).  Sharded store: ready flags are unsupported. */
 fmoe_status fmoe_traj_session_sweep(fmoe_traj_session* session, const float* q_layers, int32_t n_steps,
                                     float* out_score, int64_t* out_id, float delta, int32_t sel_d,
                                     uint64_t* out_mask, int32_t* out_count, const uint32_t* layer_ready,
@@ -325,6 +372,13 @@ fmoe_status fmoe_resolve_victims(int64_t B, int32_t k, const int64_t* ids, int64
  * the same stream: the copies are stream-ordered.  Process-wide; returns the
  * previous setting. */
 int32_t fmoe_set_host_sync(int32_t enable);
+
+/* Whether a session sweep with device flags was abandoned (a layer_ready flag
+ * not set within 10 s) since the session's last reset: the steps it did not
+ * finish published guidance_ready = 2, and every later step of the session
+ * reports (NaN, -1) until fmoe_traj_session_reset.  Reads a device word: call
+ * after synchronising the sweep's stream. */
+fmoe_status fmoe_traj_session_abandoned(const fmoe_traj_session* session, int32_t* out_abandoned);
 
 /* ---- diagnostics --------------------------------------------------------- */
 const char* fmoe_status_string(fmoe_status s);

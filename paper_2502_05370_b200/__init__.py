@@ -37,6 +37,16 @@ class fmoe_store_config(ctypes.Structure):
                 ("id_offset", ctypes.c_int64)]
 
 
+# fmoe_allgather_fn (HOST transport of a sharded store): (send, recv, bytes, user) -> 0 on success
+ALLGATHER_FN = ctypes.CFUNCTYPE(ctypes.c_int32, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64, ctypes.c_void_p)
+FMOE_TRANSPORT_NCCL, FMOE_TRANSPORT_HOST = 0, 1
+
+
+class fmoe_dist_config(ctypes.Structure):
+    _fields_ = [("rank", ctypes.c_int32), ("world", ctypes.c_int32), ("transport", ctypes.c_int32),
+                ("nccl_unique_id", ctypes.c_void_p), ("allgather", ALLGATHER_FN), ("allgather_user", ctypes.c_void_p)]
+
+
 def _load():
     if not os.path.exists(LIB_PATH):
         raise ImportError(f"{LIB_PATH} missing: run `python -m paper_2502_05370_b200.build` "
@@ -45,6 +55,9 @@ def _load():
     P, I32, I64, F = ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64, ctypes.c_float
     sig = {
         "fmoe_store_create": (I32, [ctypes.POINTER(fmoe_store_config), ctypes.c_int, ctypes.POINTER(P)]),
+        "fmoe_store_create_sharded": (I32, [ctypes.POINTER(fmoe_store_config), ctypes.POINTER(fmoe_dist_config),
+                                            ctypes.c_int, ctypes.POINTER(P)]),
+        "fmoe_get_nccl_unique_id": (I32, [P]),
         "fmoe_store_destroy": (None, [P]),
         "fmoe_store_size": (I32, [P, ctypes.POINTER(I64)]),
         "fmoe_store_get_config": (I32, [P, ctypes.POINTER(fmoe_store_config)]),
@@ -83,7 +96,7 @@ def _load():
 
 
 _lib = _load()
-ABI_SYMBOLS = ("fmoe_store_create", "fmoe_store_destroy", "fmoe_store_size", "fmoe_store_get_config",
+ABI_SYMBOLS = ("fmoe_store_create", "fmoe_store_create_sharded", "fmoe_get_nccl_unique_id", "fmoe_store_destroy", "fmoe_store_size", "fmoe_store_get_config",
                "fmoe_store_insert", "fmoe_store_insert_cos", "fmoe_search_semantic_cos", "fmoe_store_read",
                "fmoe_store_write", "fmoe_resolve_victims", "fmoe_search_semantic", "fmoe_search_trajectory",
                "fmoe_search_blend", "fmoe_search_blend_cos", "fmoe_select_experts", "fmoe_traj_session_create", "fmoe_traj_session_step",
@@ -124,6 +137,27 @@ def fmoe_store_create(L, E, K, D, d, capacity, dtype="bf16", device=0, id_offset
     cfg = fmoe_store_config(L, E, K, D, d, FMOE_BF16 if dtype == "bf16" else FMOE_F32, capacity, id_offset)
     h = ctypes.c_void_p()
     _check(_lib.fmoe_store_create(ctypes.byref(cfg), int(device), ctypes.byref(h)))
+    return h
+
+
+def fmoe_get_nccl_unique_id() -> bytes:
+    buf = ctypes.create_string_buffer(128)
+    _check(_lib.fmoe_get_nccl_unique_id(buf))
+    return buf.raw
+
+
+def fmoe_store_create_sharded(L, E, K, D, d, capacity_total, dtype="bf16", device=0, rank=0, world=1,
+                              transport="nccl", nccl_unique_id=None, host_allgather=None):
+    """This rank's shard of a store of capacity_total global slots (collective).
+    transport "nccl": nccl_unique_id = the 128 bytes of fmoe_get_nccl_unique_id (same on
+    every rank); "host": host_allgather = an object whose .cfn is an ALLGATHER_FN."""
+    cfg = fmoe_store_config(L, E, K, D, d, FMOE_BF16 if dtype == "bf16" else FMOE_F32, capacity_total, 0)
+    uid = ctypes.create_string_buffer(nccl_unique_id, 128) if nccl_unique_id is not None else None
+    dc = fmoe_dist_config(rank, world, FMOE_TRANSPORT_NCCL if transport == "nccl" else FMOE_TRANSPORT_HOST,
+                          ctypes.cast(uid, ctypes.c_void_p) if uid is not None else None,
+                          host_allgather.cfn if host_allgather is not None else ALLGATHER_FN(), None)
+    h = ctypes.c_void_p()
+    _check(_lib.fmoe_store_create_sharded(ctypes.byref(cfg), ctypes.byref(dc), int(device), ctypes.byref(h)))
     return h
 
 

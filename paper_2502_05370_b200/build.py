@@ -32,9 +32,22 @@ def nvcc() -> str:
     raise RuntimeError("nvcc not found")
 
 
+def nccl_include() -> list:
+    """nccl.h for the types of the run-time-loaded NCCL (dist.cu): the pip
+    nvidia-nccl wheel PyTorch ships, else the system header."""
+    try:
+        import nvidia.nccl as n
+        d = os.path.join(list(n.__path__)[0], "include")
+        if os.path.exists(os.path.join(d, "nccl.h")):
+            return ["-I" + d]
+    except ImportError:
+        pass
+    return []
+
+
 def _flags():
     return ARCH + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xptxas", "-v",
-                   "--expt-relaxed-constexpr", "-I" + os.path.join(ROOT, "include"), "-I" + CSRC] + \
+                   "--expt-relaxed-constexpr", "-I" + os.path.join(ROOT, "include"), "-I" + CSRC] + nccl_include() + \
         os.environ.get("FMOE_NVCC_EXTRA", "").split()     # e.g. -DFMOE_EPI_PROFILE (tools/trace.py)
 
 
@@ -73,7 +86,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
         for _, log in results:
             sys.stderr.write(log)
     tmp = LIB + ".tmp"
-    cmd = [nvcc()] + ARCH + ["-shared", "-o", tmp] + objs + ["--cudart", "shared",
+    cmd = [nvcc()] + ARCH + ["-shared", "-o", tmp] + objs + ["-ldl", "--cudart", "shared",
                                                             "-Xlinker", "-rpath=/usr/local/cuda/lib64"]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:

@@ -2,6 +2,7 @@
 #pragma once
 #include <cstdint>
 #include <cuda_runtime.h>
+#include <string>
 #include <utility>
 
 namespace fmoe {
@@ -197,7 +198,8 @@ cudaError_t launch_merge_lists(int B, int n_lists, int k_in, const float* scores
 cudaError_t launch_select(const StoreView& st, int B, const int64_t* map_id, const float* score,
                           float delta, int K, int layer_begin, int layer_end, int64_t id_offset,
                           int64_t n_rows, uint64_t* out_mask, int32_t* out_count, cudaStream_t s,
-                          int stride = 1);   // map_id[q * stride], score[q * stride]
+                          int stride = 1,    // map_id[q * stride], score[q * stride]
+                          int layer_step = 0);   // row q selects layers + q * layer_step (>= L: none)
 
 // Expert-cache priorities: prefetch plan per query, eviction order.
 cudaError_t launch_prefetch_plan(const StoreView& st, int B, const int64_t* map_id, const float* score, float delta,
@@ -243,6 +245,34 @@ cudaError_t launch_append_ids(int n, int64_t first_slot, uint32_t id_offset, int
 // Read back rows as fp32.
 cudaError_t launch_read_rows(const StoreView& st, int64_t slot0, int64_t count, float* out_emb,
                              float* out_maps, cudaStream_t s);
+
+// ---- sharded store: the exchange step (dist.cu)
+constexpr int kTransportNccl = 0;
+constexpr int kTransportHost = 1;
+using AllGatherFn = int32_t (*)(const void* send, void* recv, int64_t bytes, void* user);
+struct Comm {
+  int rank = 0, world = 1, transport = kTransportNccl;
+  void* comm = nullptr;                 // ncclComm_t
+  AllGatherFn host_fn = nullptr;
+  void* host_user = nullptr;
+  void* h_send = nullptr;               // HOST transport: pinned staging
+  void* h_recv = nullptr;
+  size_t h_bytes = 0;
+  bool init(int rank, int world, int transport, const void* nccl_uid, AllGatherFn fn, void* user, std::string* err);
+  void destroy();
+  // recv [world][bytes] <- every rank's send [bytes], rank order (stream-ordered for NCCL)
+  bool allgather(const void* dsend, void* drecv, size_t bytes, cudaStream_t s, std::string* err);
+};
+bool nccl_unique_id(void* out128, std::string* err);
+// local top-k [B][k] -> payload [B*k keys | B validity flags]
+cudaError_t launch_pack_topk(int B, int k, const float* sc, const int64_t* id, uint64_t* payload, cudaStream_t s);
+// gathered payloads [G][B*k_in + B] -> global top k (NaN, -1 where a rank flags the query invalid)
+cudaError_t launch_merge_gathered(int G, int B, int k_in, int k, const uint64_t* g, float* out_score,
+                                  int64_t* out_id, uint64_t* out_keys, cudaStream_t s);
+// selection payload [2][n] (masks, counts) and its OR / sum over [G] ranks
+cudaError_t launch_pack_select(int n, const uint64_t* mask, const int32_t* count, uint64_t* payload, cudaStream_t s);
+cudaError_t launch_combine_select(int G, int n, const uint64_t* g, uint64_t* out_mask, int32_t* out_count,
+                                  cudaStream_t s);
 
 // launch counter (for the bench's gpu_launches)
 void count_launch(int n = 1);

@@ -129,18 +129,19 @@ template <class Tag>
 __global__ void __launch_bounds__(kSelWarps * 32) select_kernel(StoreView st, int B, const int64_t* __restrict__ map_id,
                                                                 const float* __restrict__ score, float delta, int K,
                                                                 int lb, int T, int64_t id_offset, int64_t n_rows,
-                                                                uint64_t* out_mask, int32_t* out_count, int stride) {
+                                                                uint64_t* out_mask, int32_t* out_count, int stride,
+                                                                int layer_step) {
   pdl_wait();
   __shared__ float sp[kSelWarps][kMaxE];
   __shared__ int si[kSelWarps][kMaxE];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int64_t gw = int64_t(blockIdx.x) * kSelWarps + warp;
   if (gw >= int64_t(B) * T) return;
-  const int q = int(gw / T), tt = int(gw % T), t = lb + tt;
+  const int q = int(gw / T), tt = int(gw % T), t = lb + tt + q * layer_step;
   const int64_t id = map_id[int64_t(q) * stride];
   const int64_t loc = id - id_offset;
   const int64_t o = int64_t(q) * T + tt;
-  if (id < 0 || loc < 0 || loc >= n_rows) {
+  if (id < 0 || loc < 0 || loc >= n_rows || t >= st.L) {
     if (lane == 0) { out_mask[o] = 0ull; out_count[o] = 0; }
     return;
   }
@@ -156,17 +157,17 @@ __global__ void __launch_bounds__(kSelWarps * 32) select_kernel(StoreView st, in
 
 cudaError_t launch_select(const StoreView& st, int B, const int64_t* map_id, const float* score, float delta, int K,
                           int layer_begin, int layer_end, int64_t id_offset, int64_t n_rows, uint64_t* out_mask,
-                          int32_t* out_count, cudaStream_t s, int stride) {
+                          int32_t* out_count, cudaStream_t s, int stride, int layer_step) {
   const int T = layer_end - layer_begin;
   const int64_t warps = int64_t(B) * T;
   if (warps <= 0) return cudaSuccess;
   const int grid = int((warps + kSelWarps - 1) / kSelWarps);
   if (st.bf16)
     return count_launch(), launch_pdl(select_kernel<Bf16Tag>, dim3(grid), dim3(kSelWarps * 32), 0, s, st, B, map_id, score,
-                                      delta, K, layer_begin, T, id_offset, n_rows, out_mask, out_count, stride);
+                                      delta, K, layer_begin, T, id_offset, n_rows, out_mask, out_count, stride, layer_step);
   else
     return count_launch(), launch_pdl(select_kernel<F32Tag>, dim3(grid), dim3(kSelWarps * 32), 0, s, st, B, map_id, score,
-                                      delta, K, layer_begin, T, id_offset, n_rows, out_mask, out_count, stride);
+                                      delta, K, layer_begin, T, id_offset, n_rows, out_mask, out_count, stride, layer_step);
   count_launch();
   return cudaGetLastError();
 }

@@ -45,6 +45,11 @@ struct fmoe_store {
   float* psq = nullptr;
   int64_t n = 0;
   uint64_t gen = 0;       // bumped by every insert/write (invalidates trajectory sessions)
+  struct Dist {           // sharded store (fmoe_store_create_sharded)
+    fmoe::Comm comm;
+    int64_t cap_total = 0, per = 0, n_total = 0;
+  };
+  Dist* dist = nullptr;
 
   StoreView view() const {
     StoreView v;
@@ -158,13 +163,22 @@ struct Staging {
   bool bad_device = false;
   bool bad_ptr = false;
 
-  Staging(cudaStream_t s_, int dev_) : s(s_), dev(dev_) {}
+  bool own_only = false;   // every buffer is a per-call allocation (a sharded call nests a local call,
+                           // whose own Staging carves the thread's arena from offset 0)
+
+  Staging(cudaStream_t s_, int dev_, bool own = false) : s(s_), dev(dev_), own_only(own) {}
 
   void* scratch(size_t bytes) {
     if (err != cudaSuccess) return nullptr;
     void* p = nullptr;
     if (bytes == 0) bytes = 16;
     bytes = (bytes + 255) & ~size_t(255);
+    if (own_only) {
+      cudaError_t e = pool_malloc(&p, bytes, dev, s);
+      if (e != cudaSuccess) { err = e; what = "cudaMallocAsync"; return nullptr; }
+      allocs.push_back(p);
+      return p;
+    }
     if (!arena) arena = &staging_arena(dev, s);
     if (used + bytes <= arena->cap) {
       p = arena->base + used;
@@ -234,6 +248,26 @@ struct Staging {
 };
 
 int round_up(int x, int m) { return (x + m - 1) / m * m; }
+
+// Sharded stores: a public call dispatches to its collective version, which
+// runs the same public call on the local shard inside a LocalScope (no
+// re-dispatch) with device outputs, then exchanges and merges.
+thread_local int g_local_depth = 0;
+struct LocalScope {
+  LocalScope() { ++g_local_depth; }
+  ~LocalScope() { --g_local_depth; }
+};
+bool sharded(const fmoe_store* st) { return st && st->dist && g_local_depth == 0; }
+fmoe_status sharded_search(const fmoe_store* st, int64_t B, const float* q_emb, const float* q_prefix, int32_t ell,
+                           float w, int32_t k, float* out_score, int64_t* out_id, void* stream, float* out_cos,
+                           int64_t cos_stride);
+fmoe_status sharded_blend_cos(const fmoe_store* st, int64_t B, const float* sem_cos, int64_t cos_stride,
+                              const float* q_prefix, int32_t ell, float w_sem, int32_t k, float* out_score,
+                              int64_t* out_id, void* stream);
+fmoe_status sharded_select(const fmoe_store* st, int64_t B, const int64_t* map_id, const float* score, float delta,
+                           int32_t lb, int32_t le, uint64_t* out_mask, int32_t* out_count, void* stream);
+fmoe_status sharded_insert(fmoe_store* st, int64_t B, const float* emb, const float* maps, const float* sem_cos,
+                           int64_t cos_stride, int64_t* out_slot, int64_t* out_replaced, void* stream);
 
 fmoe_status check_cfg(const fmoe_store_config* c) {
   if (!c) return fail(FMOE_ERR_INVALID_ARG, "null config");
@@ -596,6 +630,7 @@ fmoe_status search_common(const fmoe_store* st, int64_t B, const float* q_emb, c
   if (traj && (!q_prefix || ell < 1 || ell > st->cfg.L)) return fail(FMOE_ERR_INVALID_ARG, "need q_prefix and 1 <= ell <= L");
   if (!(w >= 0.f && w <= 1.f)) return fail(FMOE_ERR_INVALID_ARG, "w_sem");
   if (B == 0) return FMOE_OK;
+  if (sharded(st)) return sharded_search(st, B, q_emb, q_prefix, ell, w, k, out_score, out_id, stream, out_cos, cos_stride);
   DeviceGuard g(st->device);
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   Staging S(s, st->device);
@@ -676,6 +711,11 @@ void fmoe_store_destroy(fmoe_store* st) {
   // synchronisation; the caller guarantees no other work on the store is
   // pending, the usual rule for freeing memory).  cudaFree of the tiles waits
   // for the device only as the runtime itself requires.
+  if (st->dist) {
+    st->dist->comm.destroy();
+    delete st->dist;
+    st->dist = nullptr;
+  }
   for (auto& kv : st->scratch) {
     cudaFreeAsync(kv.second.buf, kv.first);
     cudaFreeAsync(kv.second.counters, kv.first);
@@ -692,7 +732,7 @@ void fmoe_store_destroy(fmoe_store* st) {
 
 fmoe_status fmoe_store_size(const fmoe_store* st, int64_t* out_n) {
   if (!st || !out_n) return fail(FMOE_ERR_INVALID_ARG, "null argument");
-  *out_n = st->n;
+  *out_n = st->dist ? st->dist->n_total : st->n;
   return FMOE_OK;
 }
 
@@ -715,6 +755,7 @@ fmoe_status fmoe_store_insert_cos(fmoe_store* st, int64_t B, const float* emb, c
   if (B < 0 || B > (int64_t(1) << 30)) return fail(FMOE_ERR_INVALID_ARG, "B");
   if (B == 0) return FMOE_OK;
   if (!emb || !maps) return fail(FMOE_ERR_INVALID_ARG, "null emb/maps");
+  if (sharded(st)) return sharded_insert(st, B, emb, maps, sem_cos, cos_stride, out_slot, out_replaced, stream);
   const int64_t cap = st->cfg.capacity, n0 = st->n;
   const int64_t a = B < cap - n0 ? B : cap - n0;   // appended rows
   const int64_t nrep = B - a;                        // rows needing a victim
@@ -1049,12 +1090,19 @@ fmoe_status session_step(fmoe_traj_session* ss, const float* q_layer, int32_t k,
   }
   return S.finish(r);
 }
+fmoe_status sharded_session_step(fmoe_traj_session* ss, const float* q_layer, int32_t k, float* out_score,
+                                 int64_t* out_id, const StepSelect& sel, void* stream);
+fmoe_status sharded_sweep(fmoe_traj_session* ss, const float* q_layers, int32_t n_steps, float* out_score,
+                          int64_t* out_id, float delta, int32_t sel_d, uint64_t* out_mask, int32_t* out_count,
+                          void* stream);
 }  // namespace
 
 extern "C" {
 
 fmoe_status fmoe_traj_session_step(fmoe_traj_session* ss, const float* q_layer, int32_t k, float* out_score,
                                    int64_t* out_id, void* stream) {
+  if (ss && sharded(ss->st) && q_layer && k >= 1 && k <= FMOE_MAX_K && (out_score || out_id))
+    return sharded_session_step(ss, q_layer, k, out_score, out_id, StepSelect(), stream);
   return session_step(ss, q_layer, k, out_score, out_id, StepSelect(), stream);
 }
 
@@ -1073,6 +1121,8 @@ fmoe_status fmoe_traj_session_step_select(fmoe_traj_session* ss, const float* q_
   sel.le = layer_end;
   sel.mask = out_mask;
   sel.count = out_count;
+  if (sharded(ss->st) && q_layer && k >= 1 && k <= FMOE_MAX_K)
+    return sharded_session_step(ss, q_layer, k, out_score, out_id, sel, stream);
   return session_step(ss, q_layer, k, out_score, out_id, sel, stream);
 }
 
@@ -1088,6 +1138,7 @@ fmoe_status fmoe_search_blend_cos(const fmoe_store* st, int64_t B, const float* 
   if (!(w >= 0.f && w < 1.f)) return fail(FMOE_ERR_INVALID_ARG, "0 <= w_sem < 1 (w = 1: the semantic search itself)");
   if (B > 0 && (!sem_cos || cos_stride < st->n)) return fail(FMOE_ERR_INVALID_ARG, "sem_cos [B][cos_stride >= n]");
   if (B == 0) return FMOE_OK;
+  if (sharded(st)) return sharded_blend_cos(st, B, sem_cos, cos_stride, q_prefix, ell, w_sem, k, out_score, out_id, stream);
   DeviceGuard g(st->device);
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   Staging S(s, st->device);
@@ -1117,6 +1168,10 @@ fmoe_status fmoe_traj_session_sweep(fmoe_traj_session* ss, const float* q_layers
   if (ss->gen != st->gen) return fail(FMOE_ERR_INVALID_ARG, "store changed since the session was reset");
   if (!(delta <= 1.f)) return fail(FMOE_ERR_INVALID_ARG, "delta must be <= 1 (negative: dynamic)");
   if (out_mask && (!out_count || sel_d < 0)) return fail(FMOE_ERR_INVALID_ARG, "selection needs out_count, sel_d >= 0");
+  if (sharded(st)) {
+    if (layer_ready || guidance_ready) return fail(FMOE_ERR_UNSUPPORTED, "ready flags on a sharded store");
+    return sharded_sweep(ss, q_layers, n_steps, out_score, out_id, delta, sel_d, out_mask, out_count, stream);
+  }
   const int esz = st->bf16 ? 2 : 4;
   int grid = 1;
   const bool fused = ss->B == 1 && !ss->batched && st->view().Ep * esz == 16 && st->n > 0 && n_steps <= 64 &&
@@ -1229,6 +1284,7 @@ fmoe_status fmoe_resolve_victims(int64_t B, int32_t k, const int64_t* ids, int64
 fmoe_status fmoe_store_read(const fmoe_store* st, int64_t slot_begin, int64_t count, float* out_emb, float* out_maps,
                             void* stream) {
   if (!st) return fail(FMOE_ERR_INVALID_ARG, "null store");
+  if (st->dist) slot_begin -= st->cfg.id_offset;     // sharded: global slots of this rank's shard
   if (slot_begin < 0 || count < 0 || slot_begin + count > st->n) return fail(FMOE_ERR_INVALID_ARG, "slot range");
   if (count == 0) return FMOE_OK;
   DeviceGuard g(st->device);
@@ -1278,6 +1334,7 @@ fmoe_status fmoe_select_experts(const fmoe_store* st, int64_t B, const int64_t* 
   if (!(delta <= 1.f)) return fail(FMOE_ERR_INVALID_ARG, "delta must be <= 1 (negative = dynamic)");
   if (delta < 0.f && !score) return fail(FMOE_ERR_INVALID_ARG, "dynamic delta needs score");
   if (B == 0) return FMOE_OK;
+  if (sharded(st)) return sharded_select(st, B, map_id, score, delta, layer_begin, layer_end, out_mask, out_count, stream);
   const int T = layer_end - layer_begin;
   DeviceGuard g(st->device);
   cudaStream_t s = static_cast<cudaStream_t>(stream);
@@ -1301,6 +1358,7 @@ fmoe_status fmoe_prefetch_plan(const fmoe_store* st, int64_t B, const int64_t* m
                                void* stream) {
   if (!st || !map_id || !out_layer || !out_expert || !out_priority || !out_njobs)
     return fail(FMOE_ERR_INVALID_ARG, "null argument");
+  if (st->dist) return fail(FMOE_ERR_UNSUPPORTED, "prefetch plan on a sharded store");
   if (B < 0 || max_jobs < 1) return fail(FMOE_ERR_INVALID_ARG, "B / max_jobs");
   if (layer_begin < 0 || layer_begin >= layer_end || layer_end > st->cfg.L || l_now >= layer_begin)
     return fail(FMOE_ERR_INVALID_ARG, "need l_now < layer_begin < layer_end <= L");
@@ -1388,6 +1446,296 @@ fmoe_status fmoe_topk_merge(int64_t B, int32_t n_lists, int32_t k_in, const floa
     if (e != cudaSuccess) r = cuda_fail(e, "merge launch");
   }
   return S.finish(r);
+}
+
+}  // extern "C"
+
+// ============================================================================
+// Sharded store: collective versions of the calls.  Each runs
+// the single-GPU call on the local shard (LocalScope: no re-dispatch) with
+// device outputs, then ONE all-gather of a packed payload and a merge kernel.
+// ============================================================================
+namespace {
+
+// local top-k (score, id) [B][k] device -> replicated global top-k
+fmoe_status exchange_topk(const fmoe_store* st, Staging& S, int64_t B, int k, const float* ls, const int64_t* li,
+                          float* ds, int64_t* di, uint64_t* dkeys, cudaStream_t s) {
+  const int G = st->dist->comm.world;
+  const size_t pay_b = size_t(B) * (k + 1) * 8;
+  uint64_t* pay = static_cast<uint64_t*>(S.scratch(pay_b));
+  uint64_t* gat = static_cast<uint64_t*>(S.scratch(pay_b * G));
+  fmoe_status r = S.check();
+  if (r != FMOE_OK) return r;
+  cudaError_t e = launch_pack_topk(int(B), k, ls, li, pay, s);
+  if (e != cudaSuccess) return cuda_fail(e, "pack launch");
+  std::string err;
+  if (!st->dist->comm.allgather(pay, gat, pay_b, s, &err)) return fail(FMOE_ERR_CUDA, err);
+  e = launch_merge_gathered(G, int(B), k, k, gat, ds, di, dkeys, s);
+  return e == cudaSuccess ? FMOE_OK : cuda_fail(e, "merge launch");
+}
+
+// the owner's Eq. 4-6 selection (other ranks contribute mask 0, count 0) -> replicated
+fmoe_status exchange_select(const fmoe_store* st, Staging& S, int64_t B, const int64_t* did, const float* dsc,
+                            int stride, float delta, int lb, int le, int layer_step, uint64_t* dm, int32_t* dc,
+                            cudaStream_t s) {
+  const int G = st->dist->comm.world;
+  const int64_t n = B * (le - lb);
+  uint64_t* lm = static_cast<uint64_t*>(S.scratch(size_t(n) * 8));
+  int32_t* lc = static_cast<int32_t*>(S.scratch(size_t(n) * 4));
+  uint64_t* pay = static_cast<uint64_t*>(S.scratch(size_t(n) * 16));
+  uint64_t* gat = static_cast<uint64_t*>(S.scratch(size_t(n) * 16 * G));
+  fmoe_status r = S.check();
+  if (r != FMOE_OK) return r;
+  cudaError_t e = launch_select(st->view(), int(B), did, dsc, delta, st->cfg.K, lb, le, st->cfg.id_offset, st->n, lm,
+                                lc, s, stride, layer_step);
+  if (e == cudaSuccess) e = launch_pack_select(int(n), lm, lc, pay, s);
+  if (e != cudaSuccess) return cuda_fail(e, "select launch");
+  std::string err;
+  if (!st->dist->comm.allgather(pay, gat, size_t(n) * 16, s, &err)) return fail(FMOE_ERR_CUDA, err);
+  e = launch_combine_select(G, int(n), gat, dm, dc, s);
+  return e == cudaSuccess ? FMOE_OK : cuda_fail(e, "combine launch");
+}
+
+// run `local(ls, li)` (device [B][k]) then exchange into the caller's outputs
+template <class F>
+fmoe_status sharded_topk(const fmoe_store* st, int64_t B, int k, float* out_score, int64_t* out_id, void* stream,
+                         F&& local) {
+  if (B == 0) return FMOE_OK;
+  DeviceGuard g(st->device);
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  Staging S(s, st->device, true);
+  float* ds = S.out(out_score, size_t(B) * k);
+  int64_t* di = S.out(out_id, size_t(B) * k);
+  float* ls = static_cast<float*>(S.scratch(size_t(B) * k * 4));
+  int64_t* li = static_cast<int64_t*>(S.scratch(size_t(B) * k * 8));
+  fmoe_status r = S.check();
+  if (r == FMOE_OK) {
+    LocalScope ls_scope;
+    r = local(ls, li, s);
+  }
+  if (r == FMOE_OK) r = exchange_topk(st, S, B, k, ls, li, ds, di, nullptr, s);
+  return S.finish(r);
+}
+
+fmoe_status sharded_search(const fmoe_store* st, int64_t B, const float* q_emb, const float* q_prefix, int32_t ell,
+                           float w, int32_t k, float* out_score, int64_t* out_id, void* stream, float* out_cos,
+                           int64_t cos_stride) {
+  return sharded_topk(st, B, k, out_score, out_id, stream, [&](float* ls, int64_t* li, cudaStream_t s) {
+    return search_common(st, B, q_emb, q_prefix, ell, w, k, ls, li, s, out_cos, cos_stride);
+  });
+}
+
+fmoe_status sharded_blend_cos(const fmoe_store* st, int64_t B, const float* sem_cos, int64_t cos_stride,
+                              const float* q_prefix, int32_t ell, float w_sem, int32_t k, float* out_score,
+                              int64_t* out_id, void* stream) {
+  return sharded_topk(st, B, k, out_score, out_id, stream, [&](float* ls, int64_t* li, cudaStream_t s) {
+    return fmoe_search_blend_cos(st, B, sem_cos, cos_stride, q_prefix, ell, w_sem, k, ls, li, s);
+  });
+}
+
+fmoe_status sharded_select(const fmoe_store* st, int64_t B, const int64_t* map_id, const float* score, float delta,
+                           int32_t lb, int32_t le, uint64_t* out_mask, int32_t* out_count, void* stream) {
+  DeviceGuard g(st->device);
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  Staging S(s, st->device, true);
+  const int T = le - lb;
+  const int64_t* did = S.in(map_id, size_t(B));
+  const float* dsc = delta < 0.f ? S.in(score, size_t(B)) : nullptr;
+  uint64_t* dm = S.out(out_mask, size_t(B) * T);
+  int32_t* dc = S.out(out_count, size_t(B) * T);
+  fmoe_status r = S.check();
+  if (r == FMOE_OK) r = exchange_select(st, S, B, did, dsc, 1, delta, lb, le, 0, dm, dc, s);
+  return S.finish(r);
+}
+
+// Insert (Reading R8) on a sharded store: appends go to the ranks
+// owning slots n0, n0+1, ...; once full, every rank finds its local RDY top-kk
+// over the contexts present before the call, the lists are all-gathered and
+// merged, the victims are resolved in batch order on every rank (same result
+// everywhere), and each rank writes the rows whose slot it owns.
+fmoe_status sharded_insert(fmoe_store* st, int64_t B, const float* emb, const float* maps, const float* sem_cos,
+                           int64_t cos_stride, int64_t* out_slot, int64_t* out_replaced, void* stream) {
+  fmoe_store::Dist& ds_ = *st->dist;
+  const int64_t C = ds_.cap_total, n0 = ds_.n_total, off = st->cfg.id_offset, capl = st->cfg.capacity;
+  const int64_t a = B < C - n0 ? B : C - n0, nrep = B - a;
+  if (nrep > FMOE_MAX_K) return fail(FMOE_ERR_INVALID_ARG, "more than 64 rows of one insert need replacement");
+  const int L = st->cfg.L, E = st->cfg.E, D = st->cfg.D;
+  DeviceGuard g(st->device);
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  Staging S(s, st->device, true);
+  const int64_t n_loc0 = n0 - off < 0 ? 0 : (n0 - off > capl ? capl : n0 - off);   // local rows before the call
+  const float* de = S.in(emb, size_t(B) * D);
+  const float* dm = S.in(maps, size_t(B) * L * E);
+  const float* dcos = sem_cos && nrep > 0 && n_loc0 > 0 ? S.in(sem_cos, size_t(B) * cos_stride) : nullptr;
+  int64_t* dslot = S.out(out_slot, size_t(B));
+  int64_t* drep = S.out(out_replaced, size_t(B));
+  int64_t* slots_all = static_cast<int64_t*>(S.scratch(size_t(B) * 8));
+  const int kk = int(nrep < n0 ? nrep : n0) > 0 ? int(nrep < n0 ? nrep : n0) : 1;
+  float* ls = static_cast<float*>(S.scratch(size_t(nrep > 0 ? nrep : 1) * kk * 4));
+  int64_t* li = static_cast<int64_t*>(S.scratch(size_t(nrep > 0 ? nrep : 1) * kk * 8));
+  uint64_t* mkeys = static_cast<uint64_t*>(S.scratch(size_t(nrep > 0 ? nrep : 1) * kk * 8));
+  fmoe_status r = S.check();
+  if (r == FMOE_OK && nrep > 0) {
+    if (n_loc0 > 0) {
+      CosArgs cos;
+      cos.in = dcos ? dcos + a * cos_stride : nullptr;
+      cos.stride = cos_stride;
+      // RDY = d/L sem + (L-d)/L traj over full maps, unchecked queries
+      r = run_search(st, nrep, de + a * D, dm + a * int64_t(L) * E, int64_t(L) * E, L, float(st->cfg.d) / float(L),
+                     kk, n_loc0, uint32_t(off), s, ls, li, nullptr, false, cos);
+    } else {
+      cudaError_t e = launch_merge_keys(int(nrep), 0, kk, nullptr, kk, nullptr, ls, li, nullptr, s);
+      if (e != cudaSuccess) r = cuda_fail(e, "merge launch");
+    }
+    if (r == FMOE_OK) r = exchange_topk(st, S, nrep, kk, ls, li, nullptr, nullptr, mkeys, s);
+  }
+  if (r == FMOE_OK) {
+    // keys hold global ids; appended rows get global slots n0 + x
+    cudaError_t e = launch_resolve(int(nrep), kk, mkeys, 0u, slots_all, int(a), n0, dslot, drep, s);
+    if (e != cudaSuccess) r = cuda_fail(e, "resolve launch");
+  }
+  if (r == FMOE_OK) {
+    WriteArgs w{};
+    w.emb = st->emb; w.r_e = st->r_e; w.maps = st->maps; w.psq = st->psq;
+    w.cap = capl; w.L = L; w.E = E; w.D = D; w.Dp = st->Dp; w.Ep = st->Ep; w.bf16 = st->bf16;
+    w.in_emb = de; w.in_maps = dm;
+    w.B = int(B);
+    w.slots = slots_all;
+    w.slot_offset = off;
+    w.slot_limit = capl;          // this rank's rows: appends and victims it owns
+    cudaError_t e = launch_write_rows(w, s);
+    if (e != cudaSuccess) r = cuda_fail(e, "write launch");
+  }
+  if (r == FMOE_OK) {
+    ds_.n_total = n0 + a;
+    const int64_t nl = ds_.n_total - off;
+    st->n = nl < 0 ? 0 : (nl > capl ? capl : nl);
+    ++st->gen;
+  }
+  return S.finish(r);
+}
+
+fmoe_status sharded_session_step(fmoe_traj_session* ss, const float* q_layer, int32_t k, float* out_score,
+                                 int64_t* out_id, const StepSelect& sel, void* stream) {
+  const fmoe_store* st = ss->st;
+  const int64_t B = ss->B;
+  DeviceGuard g(st->device);
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  Staging S(s, st->device, true);
+  const int T = sel.le - sel.lb;
+  float* ds = S.out(out_score, size_t(B) * k);
+  int64_t* di = S.out(out_id, size_t(B) * k);
+  uint64_t* dm = T > 0 ? S.out(sel.mask, size_t(B) * T) : nullptr;
+  int32_t* dc = T > 0 ? S.out(sel.count, size_t(B) * T) : nullptr;
+  float* ls = static_cast<float*>(S.scratch(size_t(B) * k * 4));
+  int64_t* li = static_cast<int64_t*>(S.scratch(size_t(B) * k * 8));
+  // merged outputs in device memory (the selection reads the merged top-1)
+  float* ms = static_cast<float*>(S.scratch(size_t(B) * k * 4));
+  int64_t* mi = static_cast<int64_t*>(S.scratch(size_t(B) * k * 8));
+  fmoe_status r = S.check();
+  if (r == FMOE_OK) {
+    LocalScope scope;
+    r = session_step(ss, q_layer, k, ls, li, StepSelect(), s);
+  }
+  if (r == FMOE_OK) r = exchange_topk(st, S, B, k, ls, li, ms, mi, nullptr, s);
+  if (r == FMOE_OK && T > 0)
+    r = exchange_select(st, S, B, mi, ms, k, sel.delta, sel.lb, sel.le, 0, dm, dc, s);
+  if (r == FMOE_OK) {
+    cudaError_t e = cudaSuccess;
+    if (ds) e = cudaMemcpyAsync(ds, ms, size_t(B) * k * 4, cudaMemcpyDeviceToDevice, s);
+    if (e == cudaSuccess && di) e = cudaMemcpyAsync(di, mi, size_t(B) * k * 8, cudaMemcpyDeviceToDevice, s);
+    if (e != cudaSuccess) r = cuda_fail(e, "session output copy");
+  }
+  return S.finish(r);
+}
+
+fmoe_status sharded_sweep(fmoe_traj_session* ss, const float* q_layers, int32_t n_steps, float* out_score,
+                          int64_t* out_id, float delta, int32_t sel_d, uint64_t* out_mask, int32_t* out_count,
+                          void* stream) {
+  const fmoe_store* st = ss->st;
+  const int64_t B = ss->B, n = int64_t(n_steps) * B;
+  const int layer0 = ss->layer;
+  DeviceGuard g(st->device);
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  Staging S(s, st->device, true);
+  float* ds = S.out(out_score, size_t(n));
+  int64_t* di = S.out(out_id, size_t(n));
+  uint64_t* dm = out_mask ? S.out(out_mask, size_t(n)) : nullptr;
+  int32_t* dc = out_mask ? S.out(out_count, size_t(n)) : nullptr;
+  float* ls = static_cast<float*>(S.scratch(size_t(n) * 4));
+  int64_t* li = static_cast<int64_t*>(S.scratch(size_t(n) * 8));
+  float* ms = static_cast<float*>(S.scratch(size_t(n) * 4));
+  int64_t* mi = static_cast<int64_t*>(S.scratch(size_t(n) * 8));
+  fmoe_status r = S.check();
+  if (r == FMOE_OK) {
+    LocalScope scope;
+    r = fmoe_traj_session_sweep(ss, q_layers, n_steps, ls, li, delta, sel_d, nullptr, nullptr, nullptr, nullptr, s);
+  }
+  // every (step, query) row is a top-1 search: one exchange for the whole sweep
+  if (r == FMOE_OK) r = exchange_topk(st, S, n, 1, ls, li, ms, mi, nullptr, s);
+  // row (step s, query x) selects target layer layer0 + s + sel_d (none past L)
+  if (r == FMOE_OK && dm) {
+    if (B == 1) r = exchange_select(st, S, n, mi, ms, 1, delta, layer0 + sel_d, layer0 + sel_d + 1, 1, dm, dc, s);
+    else
+      for (int st2 = 0; st2 < n_steps && r == FMOE_OK; ++st2) {
+        const int tgt = layer0 + st2 + sel_d;
+        r = exchange_select(st, S, B, mi + int64_t(st2) * B, ms + int64_t(st2) * B, 1, delta, tgt, tgt + 1, 0,
+                            dm + int64_t(st2) * B, dc + int64_t(st2) * B, s);
+      }
+  }
+  if (r == FMOE_OK) {
+    cudaError_t e = cudaMemcpyAsync(ds, ms, size_t(n) * 4, cudaMemcpyDeviceToDevice, s);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(di, mi, size_t(n) * 8, cudaMemcpyDeviceToDevice, s);
+    if (e != cudaSuccess) r = cuda_fail(e, "sweep output copy");
+  }
+  return S.finish(r);
+}
+
+}  // namespace
+
+extern "C" {
+
+fmoe_status fmoe_get_nccl_unique_id(void* out_128_bytes) {
+  if (!out_128_bytes) return fail(FMOE_ERR_INVALID_ARG, "null out");
+  std::string err;
+  if (!nccl_unique_id(out_128_bytes, &err)) return fail(FMOE_ERR_UNSUPPORTED, err);
+  return FMOE_OK;
+}
+
+fmoe_status fmoe_store_create_sharded(const fmoe_store_config* cfg, const fmoe_dist_config* dist, int device,
+                                      fmoe_store** out) {
+  if (!out || !cfg || !dist) return fail(FMOE_ERR_INVALID_ARG, "null argument");
+  *out = nullptr;
+  if (dist->world < 1 || dist->rank < 0 || dist->rank >= dist->world)
+    return fail(FMOE_ERR_INVALID_ARG, "need 0 <= rank < world");
+  if (dist->transport != FMOE_TRANSPORT_NCCL && dist->transport != FMOE_TRANSPORT_HOST)
+    return fail(FMOE_ERR_INVALID_ARG, "transport");
+  if (cfg->id_offset != 0) return fail(FMOE_ERR_INVALID_ARG, "sharded: cfg->id_offset must be 0");
+  if (cfg->capacity < dist->world) return fail(FMOE_ERR_SHAPE, "sharded: capacity < world");
+  const int64_t per = (cfg->capacity + dist->world - 1) / dist->world;
+  const int64_t off = per * dist->rank;
+  const int64_t capl = cfg->capacity - off < per ? cfg->capacity - off : per;
+  if (capl < 1) return fail(FMOE_ERR_SHAPE, "sharded: a rank would hold no slots (capacity too small)");
+  fmoe_store_config lc = *cfg;
+  lc.capacity = capl;
+  lc.id_offset = off;
+  fmoe_store* st = nullptr;
+  fmoe_status r = fmoe_store_create(&lc, device, &st);
+  if (r != FMOE_OK) return r;
+  st->dist = new fmoe_store::Dist();
+  st->dist->cap_total = cfg->capacity;
+  st->dist->per = per;
+  std::string err;
+  {
+    DeviceGuard g(device);
+    if (!st->dist->comm.init(dist->rank, dist->world, dist->transport, dist->nccl_unique_id,
+                             reinterpret_cast<AllGatherFn>(dist->allgather), dist->allgather_user, &err)) {
+      fmoe_store_destroy(st);
+      return fail(FMOE_ERR_CUDA, err);
+    }
+  }
+  *out = st;
+  return FMOE_OK;
 }
 
 }  // extern "C"

@@ -1,9 +1,16 @@
-"""World-size-2 gloo tests of the sharded store's host-side logic (CPU, no GPU).
+"""World-size-2 gloo tests of the sharded store's exchange protocol (CPU, no GPU).
 
-The local shard operations use the CPU oracle as the backend (tests only); the
-collectives (all-gather of candidate lists, all-reduce of selections) are real
-torch.distributed gloo calls.  Pins SURVEY §8(c) c9: merged per-shard results
-equal the unsharded store's, for search, selection and RDY insertion."""
+The library's sharded calls (fmoe_store_create_sharded, csrc/dist.cu and
+store.cu) run on the GPU; here the SAME protocol -- local top-k with global
+ids, a packed payload of keys plus a per-query validity flag, ONE all-gather,
+a (score desc, global id asc) merge; selections by the owner combined by
+OR / sum; inserts appended in slot order, RDY candidates gathered and merged,
+victims resolved in batch order, owners write -- is modelled with the CPU
+oracle as the local engine (tests only) and real torch.distributed gloo
+collectives, and pinned to the unsharded oracle store.  The
+product's HOST-transport callback (paper_2502_05370_b200/dist.py) is tested
+with gloo too."""
+import ctypes
 import os
 import socket
 
@@ -17,6 +24,13 @@ import fmoe_synth as S
 from oracle import fmoe_oracle as O
 
 SH = S.Shape("dist", 6, 8, 2, 24, n_clusters=4)
+
+
+def shard_range(n_total, rank, world):
+    """The library's shard map: contiguous ranges of P = ceil(C / G) slots."""
+    per = (n_total + world - 1) // world
+    lo = min(rank * per, n_total)
+    return min(lo + per, n_total) - lo, lo
 
 
 class OracleBackend:
@@ -64,16 +78,93 @@ class OracleBackend:
         pass
 
 
+class ShardProtocolModel:
+    """The sharded store's collective protocol (store.cu's sharded_* functions)."""
+
+    def __init__(self, C, dtype):
+        self.rank, self.world = dist.get_rank(), dist.get_world_size()
+        self.C = C
+        self.cap, self.off = shard_range(C, self.rank, self.world)
+        self.b = OracleBackend(self.cap, self.off, dtype)
+        self.n_total = 0
+
+    def _exchange(self, s, i):
+        """pack [B][k] keys + [B] flags -> all-gather -> merge (validity: every rank's flag)."""
+        B, k = s.shape
+        pay = torch.zeros(B * k * 2 + B, dtype=torch.float64)
+        pay[:B * k] = torch.from_numpy(np.nan_to_num(s.numpy().ravel(), nan=-np.inf))
+        pay[B * k:2 * B * k] = torch.from_numpy(i.numpy().ravel().astype(np.float64))
+        pay[2 * B * k:] = torch.from_numpy((~np.isnan(s.numpy()[:, 0])).astype(np.float64))
+        out = torch.empty(self.world * pay.numel(), dtype=torch.float64)
+        dist.all_gather_into_tensor(out, pay)
+        out = out.view(self.world, -1)
+        gs = out[:, :B * k].view(self.world, B, k).numpy()
+        gi = out[:, B * k:2 * B * k].view(self.world, B, k).numpy().astype(np.int64)
+        valid = out[:, 2 * B * k:].numpy().min(axis=0) > 0
+        ms, mi = O.merge_topk([gs[g] for g in range(self.world)], [gi[g] for g in range(self.world)], k)
+        ms[~valid], mi[~valid] = np.nan, -1
+        return torch.from_numpy(ms), torch.from_numpy(mi)
+
+    def search(self, q_emb, q_prefix, ell, w, k):
+        s, i = self.b.search(q_emb, q_prefix, ell, w, k)
+        return self._exchange(s, i)
+
+    def search_semantic(self, q_emb, k=1):
+        return self.search(q_emb, None, 0, 1.0, k)
+
+    def search_trajectory(self, q_prefix, ell, k=1):
+        return self.search(None, q_prefix[:, :ell].contiguous(), ell, 0.0, k)
+
+    def search_blend(self, q_emb, q_prefix, ell, w_sem=-1.0, k=1):
+        return self.search(q_emb, q_prefix[:, :ell].contiguous(), ell, 3 / SH.L if w_sem < 0 else w_sem, k)
+
+    def select_experts(self, map_id, score, delta=-1.0, lb=0, le=None):
+        mask, cnt = self.b.select(map_id, score, delta, lb, le)     # owner non-zero, others zero
+        both = torch.cat([mask, cnt.to(torch.int64)], dim=1)
+        out = torch.empty(self.world, *both.shape, dtype=torch.int64)
+        dist.all_gather_into_tensor(out.view(-1), both.view(-1))
+        T = mask.shape[1]
+        m = out[:, :, :T]
+        comb = m[0]
+        for g in range(1, self.world):
+            comb = comb | m[g]
+        return comb, out[:, :, T:].sum(0).to(torch.int32)
+
+    def insert(self, emb, maps):
+        B, n0 = emb.shape[0], self.n_total
+        a = min(B, self.C - n0)
+        nrep = B - a
+        slots = list(range(n0, n0 + a)) + [-1] * nrep
+        if nrep > 0 and n0 > 0:
+            kk = min(nrep, n0)
+            q_e, q_m = emb[a:], maps[a:]
+            n_loc0 = min(max(n0 - self.off, 0), self.cap)
+            if n_loc0 > 0:
+                s, i = self.b.search(q_e, q_m, SH.L, 3 / SH.L, kk)   # RDY over the rows present before
+            else:
+                s, i = torch.full((nrep, kk), -np.inf, dtype=torch.float64), torch.full((nrep, kk), -1)
+            _, mi = self._exchange(s, i)
+            victims = self.b.resolve(mi)
+            slots[a:] = victims.tolist()
+        # every rank writes the rows whose global slot it owns (appends and victims)
+        for x, y in enumerate(slots):
+            if self.off <= y < self.off + self.cap:
+                if y - self.off == self.b.st.n:
+                    self.b.append(emb[x:x + 1], maps[x:x + 1])
+                else:
+                    self.b.write(emb[x:x + 1], maps[x:x + 1], torch.tensor([y]))
+        self.n_total = n0 + a
+        rep = [-1] * a + slots[a:]
+        return torch.tensor(slots), torch.tensor(rep)
+
+
 def _worker(rank, world, port, dtype, q):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     import datetime
     dist.init_process_group("gloo", rank=rank, world_size=world, timeout=datetime.timedelta(seconds=60))
-    from paper_2502_05370_b200 import dist as fd
     try:
         C = 103                                  # not a multiple of world: ragged last shard
-        cap, off = fd.shard_range(C, rank, world)
-        st = fd.ShardedExpertMapStore(SH.L, SH.E, SH.K, SH.D, 3, C, dtype,
-                                      backend=OracleBackend(cap, off, dtype))
+        st = ShardProtocolModel(C, dtype)
         emb, maps, _ = S.store_rows(SH, 5, 0, C + 40)
         res = {}
         res["ins0"] = st.insert(emb[:60], maps[:60])          # appends on rank 0 only
@@ -149,8 +240,44 @@ def test_shard_range_partitions_the_store():
     for n in (1, 7, 100, 16_000_000):
         for G in (1, 2, 3, 4, 8):
             spans = [fd.shard_range(n, r, G) for r in range(G)]
+            assert spans == [shard_range(n, r, G) for r in range(G)]
             assert sum(c for c, _ in spans) == n
             pos = 0
             for c, off in spans:
                 assert off == pos or c == 0
                 pos = off + c if c else pos
+
+
+def _ag_worker(rank, world, port, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    import datetime
+    dist.init_process_group("gloo", rank=rank, world_size=world, timeout=datetime.timedelta(seconds=60))
+    from paper_2502_05370_b200 import dist as fd
+    try:
+        ag = fd._HostAllGather()
+        n = 37
+        send = (ctypes.c_uint8 * n)(*[(rank * 50 + j) % 256 for j in range(n)])
+        recv = (ctypes.c_uint8 * (n * world))()
+        rc = ag.cfn(ctypes.addressof(send), ctypes.addressof(recv), n, None)   # through the C function pointer
+        q.put((rank, rc, bytes(recv)))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_host_transport_allgather_callback():
+    """The product's fmoe_allgather_fn for the HOST transport: recv[world][bytes]
+    in rank order, called through its C function pointer as the library does."""
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_ag_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    out = dict((r, (rc, b)) for r, rc, b in (q.get(timeout=120) for _ in range(world)))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    want = bytes([(r * 50 + j) % 256 for r in range(world) for j in range(37)])
+    for r in range(world):
+        assert out[r][0] == 0 and out[r][1] == want
