@@ -541,7 +541,7 @@ def run_fmoe(args, cfg, rank, world, local_rank):
     tflops = sem_flops / (sem_ms * 1e-3) / 1e12 if sem_ms > 0 else 0.0
     agg = scan_bytes / (scan_ms * 1e-3) / 1e9 if scan_ms > 0 else 0.0
     tensor = cfg["dtype"] == "bf16" and cfg["B"] >= 5 and ai > ridge
-    traffic = measured_traffic(args.config)
+    traffic = measured_traffic(args.config) if world == 1 else None   # the ncu capture is of the 1-GPU launch
     if tensor:
         head = {"bound": "tensor", "achieved": round(tflops, 1), "peak": peaks["bf16_tflops_sustained"],
                 "unit": "TFLOP/s", "frac": round(tflops / peaks["bf16_tflops_sustained"], 4),
@@ -612,7 +612,7 @@ def run_fmoe(args, cfg, rank, world, local_rank):
             fm.fmoe_traj_session_destroy(obj.sess)
     st.close()
     return dict(value=value, ms_step=ms_step, roofline=roofline, e2e=e2e, clocks=clocks, launches=launches,
-                N_local=N_local, cos=used_cos)
+                N_local=N_local, cos=used_cos, graph=bool(graphs) or (use_graph and world == 1))
 
 
 def cos_keys(cfg, cos):
@@ -818,7 +818,8 @@ def main():
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": cfg["dtype"],
             "data": "synthetic (seeded clustered embeddings + softmax gate maps, fmoe_synth)",
             "config": base_config,
-            "impl_notes": dict(fmoe_notes, **cos_keys(cfg, res["cos"])),
+            "impl_notes": dict(fmoe_notes, launch="CUDA graph replay of the step" if res["graph"] else "eager",
+                               **cos_keys(cfg, res["cos"])),
             "roofline": res["roofline"], "cpu_baseline": cpu, "e2e": res["e2e"], "clocks": res["clocks"],
             "gpu_launches": res["launches"]}
     print(json.dumps(line))
