@@ -65,6 +65,7 @@ struct ScanArgs {
   const float* sem_cos;
   int64_t cos_stride;
   const int* run_if_gt;      // nullable device count: the pass runs only if *run_if_gt > q0 (re-rank fallback)
+  const uint32_t* excl;      // nullable bitmap over local rows: set bits are no candidates (insert sub-batches)
 };
 
 // debug tracer buffer (null unless fmoe_debug_trace enabled it)
@@ -161,6 +162,7 @@ struct UmmaLaunch {
   uint64_t* cand; int cand_q0; int grid;
   unsigned long long* trace;
   int keep_gthr;               // 1: gthr already holds a valid admission bound (sample pass); prep keeps it
+  const uint32_t* excl;        // nullable bitmap over rows: set bits are no candidates (insert sub-batches)
 };
 bool umma_supported(const UmmaPlanIn& in);
 int umma_rep(const UmmaPlanIn& in);
@@ -236,7 +238,12 @@ cudaError_t launch_write_rows(const WriteArgs& w, cudaStream_t s);
 cudaError_t launch_resolve(int nrep, int kk, const uint64_t* keys, uint32_t id_offset,
                            int64_t* victims, int x0, int64_t first_append_slot,
                            int64_t* out_slot, int64_t* out_replaced, cudaStream_t s,
-                           int* need_full = nullptr, int k_full = 0, const int* gate = nullptr);
+                           int* need_full = nullptr, int k_full = 0, const int* gate = nullptr,
+                           int mark_append = -1);   // rows [0, mark_append) are appends (-1: x0)
+// Exclusion bitmap of an insert's sub-batches: set / clear the bits of the
+// victims slots[x] (global ids; local bit = id - offset if in [0, limit)).
+cudaError_t launch_excl(uint32_t* excl, const int64_t* slots, int n, int64_t offset, int64_t limit, int set,
+                        cudaStream_t s);
 // Victim resolution from merged candidate ids [B][k] (best first).
 cudaError_t launch_resolve_ids(int B, int k, const int64_t* ids, int64_t* out_victim, cudaStream_t s);
 cudaError_t launch_append_ids(int n, int64_t first_slot, uint32_t id_offset, int64_t* out_slot,

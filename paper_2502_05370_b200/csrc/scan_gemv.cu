@@ -328,7 +328,8 @@ __global__ void __launch_bounds__(kScanThreads, TPI >= 1 ? 2 : 3) scan_gemv_kern
 
     // ---- epilogue: lane r scores row y0 + r and offers it to the lists
     const int64_t y = y0 + lane;
-    const bool ok = y < n_rows;
+    // rows claimed by an earlier sub-batch of the same insert (R8) are no candidates
+    const bool ok = y < n_rows && !(a.excl && ((__ldg(a.excl + (y >> 5)) >> (y & 31)) & 1u));
     const float re = (SEM && ok) ? st.r_e[y] : 0.f;
     const float rm = (TRAJ && msq > 0.f) ? rsqrtf(msq) : 0.f;
 #pragma unroll

@@ -255,6 +255,7 @@ struct UmmaParams {
   const float* sem_cos;         // trajectory kernels: cached semantic cosines to blend (optional)
   int64_t cos_stride;
   unsigned long long* gthr;     // [nq] shared admission threshold per query (zeroed by prep)
+  const uint32_t* excl;         // nullable bitmap over rows: no candidates (insert sub-batches)
   int cos_tma;                  // semantic scans: out_cos written through a swizzled smem stage + TMA
                                 // tensor stores; trajectory scans: sem_cos read by per-warp TMA loads
                                 // (a 3-buffer ring, 2 chunks ahead) instead of lane-per-query loads
@@ -786,6 +787,7 @@ __global__ void __launch_bounds__(kUmThreads, 1)
           for (int j = 0; j < 32; ++j) m |= (sc[j] >= thr_s ? 1u : 0u) << j;
         }
         m &= vmask;
+        if (m && p.excl) m &= ~__ldg(p.excl + (yc >> 5));   // rows claimed by an earlier insert sub-batch
         EPI_T(3);
         if (SEM && !TRAJ && p.out_cos && p.cos_tma) {
           // warp-cooperative: the 32 x 32 block (queries of this warp x this
@@ -1292,6 +1294,7 @@ cudaError_t launch_umma(const UmmaLaunch& L, cudaStream_t s) {
   p.sem_cos = L.sem_cos;
   p.cos_stride = L.cos_stride;
   p.gthr = L.gthr;
+  p.excl = L.excl;
   p.gate = L.gate;
   const size_t smem = 1024 + size_t(p.stages) * um_stage_bytes(CG, TN) + lists;
   using Fn = void (*)(const CUtensorMap, const CUtensorMap, const CUtensorMap, const CUtensorMap, const CUtensorMap,

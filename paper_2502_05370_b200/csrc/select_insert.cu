@@ -252,7 +252,7 @@ __global__ void __launch_bounds__(32) resolve_kernel(int nrep, int kk, const uin
                                                      uint32_t id_offset, int64_t* slots_all, int x0,
                                                      int64_t first_append_slot, int64_t* out_slot,
                                                      int64_t* out_replaced, int* need_full, int k_full,
-                                                     const int* gate) {
+                                                     const int* gate, int mark_append) {
   pdl_wait();
   if (gate && *gate == 0) return;
   __shared__ int64_t claimed[kMaxK];
@@ -261,7 +261,7 @@ __global__ void __launch_bounds__(32) resolve_kernel(int nrep, int kk, const uin
   bool need = false;
   for (int i = lane; i < nrep * kk; i += 32) ks[i] = keys[i];
   __syncwarp();
-  for (int x = lane; x < x0; x += 32) {
+  for (int x = lane; x < mark_append; x += 32) {
     slots_all[x] = first_append_slot + x;
     if (out_slot) out_slot[x] = int64_t(id_offset) + first_append_slot + x;
     if (out_replaced) out_replaced[x] = -1;
@@ -300,12 +300,32 @@ __global__ void __launch_bounds__(32) resolve_kernel(int nrep, int kk, const uin
 
 cudaError_t launch_resolve(int nrep, int kk, const uint64_t* keys, uint32_t id_offset, int64_t* slots_all, int x0,
                            int64_t first_append_slot, int64_t* out_slot, int64_t* out_replaced, cudaStream_t s,
-                           int* need_full, int k_full, const int* gate) {
+                           int* need_full, int k_full, const int* gate, int mark_append) {
   count_launch();
   return launch_pdl(resolve_kernel, dim3(1), dim3(32), 0, s, nrep, kk, keys, id_offset, slots_all, x0,
-                    first_append_slot, out_slot, out_replaced, need_full, k_full, gate);
+                    first_append_slot, out_slot, out_replaced, need_full, k_full, gate,
+                    mark_append < 0 ? x0 : mark_append);
   count_launch();
   return cudaGetLastError();
+}
+
+__global__ void excl_kernel(uint32_t* excl, const int64_t* __restrict__ slots, int n, int64_t offset, int64_t limit,
+                            int set) {
+  pdl_wait();
+  const int x = blockIdx.x * blockDim.x + threadIdx.x;
+  if (x >= n) return;
+  const int64_t v = slots[x] - offset;
+  if (slots[x] < 0 || v < 0 || v >= limit) return;
+  const uint32_t bit = 1u << (v & 31);
+  if (set) atomicOr(excl + (v >> 5), bit);
+  else atomicAnd(excl + (v >> 5), ~bit);
+}
+
+cudaError_t launch_excl(uint32_t* excl, const int64_t* slots, int n, int64_t offset, int64_t limit, int set,
+                        cudaStream_t s) {
+  if (n <= 0) return cudaSuccess;
+  count_launch();
+  return launch_pdl(excl_kernel, dim3((n + 127) / 128), dim3(128), 0, s, excl, slots, n, offset, limit, set);
 }
 
 __global__ void __launch_bounds__(32) resolve_ids_kernel(int B, int k, const int64_t* __restrict__ ids,

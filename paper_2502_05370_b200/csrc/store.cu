@@ -50,6 +50,7 @@ struct fmoe_store {
     int64_t cap_total = 0, per = 0, n_total = 0;
   };
   Dist* dist = nullptr;
+  uint32_t* excl = nullptr;   // [cap / 32] claimed-slot bitmap of an insert's sub-batches (zero between calls)
 
   StoreView view() const {
     StoreView v;
@@ -333,6 +334,16 @@ int umma_min_batch() {
 // RDY insert: candidates kept per row by the first pass (see fmoe_store_insert_cos)
 constexpr int kRdyFirst = 8;
 
+// The claimed-slot bitmap of an insert's sub-batches, allocated zeroed on the
+// first insert that needs more than one sub-batch.
+fmoe_status ensure_excl(fmoe_store* st, int64_t nrep) {
+  if (nrep <= FMOE_MAX_K || st->excl) return FMOE_OK;
+  const size_t words = size_t(st->cfg.capacity + 31) / 32 + 1;
+  cudaError_t e = cudaMalloc(&st->excl, words * 4);
+  if (e == cudaSuccess) e = cudaMemset(st->excl, 0, words * 4);
+  return e == cudaSuccess ? FMOE_OK : cuda_fail(e, "insert bitmap");
+}
+
 // Whether a search of B queries with list length k runs on the tensor cores
 // (fills *in when it does).
 bool umma_plan(const fmoe_store* st, int64_t B, int k, int ell, float w, int64_t n_rows, uint32_t id_offset,
@@ -353,6 +364,7 @@ struct CosArgs {
   float* out = nullptr;          // semantic scans: write the cosines
   const float* in = nullptr;     // RDY / blend scans: blend these instead of re-reading embeddings
   int64_t stride = 0;
+  const uint32_t* excl = nullptr;   // RDY scans of a later insert sub-batch: rows already claimed
 };
 
 fmoe_status run_search_umma(const fmoe_store* st, UmmaPlanIn in, int64_t B, const float* dq, const float* dp,
@@ -397,6 +409,7 @@ fmoe_status run_search_umma(const fmoe_store* st, UmmaPlanIn in, int64_t B, cons
     L.out_cos = cos.out ? cos.out + q0 * cos.stride : nullptr;
     L.sem_cos = cos.in ? cos.in + q0 * cos.stride : nullptr;
     L.cos_stride = cos.stride;
+    L.excl = cos.excl;
     cudaError_t e = launch_umma(L, s);
     if (e != cudaSuccess) return cuda_fail(e, "umma scan launch");
   }
@@ -608,6 +621,7 @@ fmoe_status run_search(const fmoe_store* st, int64_t B, const float* dq, const f
   a.out_cos = cos.out;
   a.sem_cos = cos.in;
   a.cos_stride = cos.stride;
+  a.excl = cos.excl;
   for (int p = 0; p < npass; ++p) {
     a.q0 = 4 * p;
     a.nq = int(B - a.q0 < 4 ? B - a.q0 : 4);
@@ -723,6 +737,7 @@ void fmoe_store_destroy(fmoe_store* st) {
     cudaStreamSynchronize(kv.first);
   }
   cudaGetLastError();
+  cudaFree(st->excl);
   cudaFree(st->emb);
   cudaFree(st->r_e);
   cudaFree(st->maps);
@@ -759,8 +774,9 @@ fmoe_status fmoe_store_insert_cos(fmoe_store* st, int64_t B, const float* emb, c
   const int64_t cap = st->cfg.capacity, n0 = st->n;
   const int64_t a = B < cap - n0 ? B : cap - n0;   // appended rows
   const int64_t nrep = B - a;                        // rows needing a victim
-  if (nrep > FMOE_MAX_K) return fail(FMOE_ERR_INVALID_ARG, "more than 64 rows of one insert need replacement");
   const int L = st->cfg.L, E = st->cfg.E, D = st->cfg.D;
+  fmoe_status xs = ensure_excl(st, nrep);
+  if (xs != FMOE_OK) return xs;
   DeviceGuard g(st->device);
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   Staging S(s, st->device);
@@ -773,40 +789,58 @@ fmoe_status fmoe_store_insert_cos(fmoe_store* st, int64_t B, const float* emb, c
   fmoe_status r = S.check();
   const uint32_t off = uint32_t(st->cfg.id_offset);
   if (r == FMOE_OK && nrep > 0) {
-    // Row j (batch order) takes its best candidate not claimed by rows < j, so
-    // kk = min(nrep, n0) candidates per row always suffice.  Most batches need
-    // far fewer: a first pass keeps kRdyFirst, and only when some row finds
-    // all of them claimed does a second, gated pass (device flag, no host
-    // sync) rescan with kk and redo the resolution -- same result either way.
-    const int kk = int(nrep < n0 ? nrep : n0);
+    // Row j (batch order) takes its best candidate not claimed by rows < j.
+    // Rows go in sub-batches of <= 64 (the candidate lists' length); every
+    // RDY scan is against the contexts present before the call (rows [0, n0),
+    // P:552-553 computes one RDY matrix) and a later sub-batch's scan skips
+    // the slots earlier sub-batches claimed (a device bitmap), so the result
+    // is the sequential rule of Reading R8 for any batch size.  Within a
+    // sub-batch kk = min(rows, n0) candidates per row always suffice; a first
+    // pass keeps kRdyFirst, and only when some row finds all of them claimed
+    // does a second, gated pass (device flag, no host sync) rescan with kk.
     const float w = float(st->cfg.d) / float(L);
-    const int k1 = kk < kRdyFirst ? kk : kRdyFirst;
-    UmmaPlanIn p1{}, p2{};
-    const bool two = k1 < kk && umma_plan(st, nrep, k1, L, w, n0, 0u, &p1) && umma_plan(st, nrep, kk, L, w, n0, 0u, &p2);
-    uint64_t* keys = static_cast<uint64_t*>(S.scratch(size_t(nrep) * (kk > 0 ? kk : 1) * 8));
-    uint64_t* keys1 = two ? static_cast<uint64_t*>(S.scratch(size_t(nrep) * k1 * 8)) : nullptr;
-    int* need = two ? static_cast<int*>(S.scratch(sizeof(int))) : nullptr;
-    r = S.check();
-    // RDY_{x,y} = d/L sem + (L-d)/L traj over full maps, against
-    // the contexts present before this call: rows [0, n0).
-    CosArgs cos;
-    cos.in = dcos ? dcos + a * cos_stride : nullptr;     // cos(emb_x, sem_y) from the semantic search
-    cos.stride = cos_stride;
-    const float* qe = de + a * D;
-    const float* qm = dm + a * int64_t(L) * E;
-    if (r == FMOE_OK && two) {
-      r = run_search(st, nrep, qe, qm, int64_t(L) * E, L, w, k1, n0, 0u, s, nullptr, nullptr, keys1, false, cos);
+    const int64_t nsub_rows = FMOE_MAX_K;
+    for (int64_t sb = 0; sb < nrep && r == FMOE_OK; sb += nsub_rows) {
+      const int64_t nb = nrep - sb < nsub_rows ? nrep - sb : nsub_rows;
+      const int kk = int(nb < n0 ? nb : n0);
+      const int k1 = kk < kRdyFirst ? kk : kRdyFirst;
+      UmmaPlanIn p1{}, p2{};
+      const bool two = k1 < kk && umma_plan(st, nb, k1, L, w, n0, 0u, &p1) && umma_plan(st, nb, kk, L, w, n0, 0u, &p2);
+      uint64_t* keys = static_cast<uint64_t*>(S.scratch(size_t(nb) * (kk > 0 ? kk : 1) * 8));
+      uint64_t* keys1 = two ? static_cast<uint64_t*>(S.scratch(size_t(nb) * k1 * 8)) : nullptr;
+      int* need = two ? static_cast<int*>(S.scratch(sizeof(int))) : nullptr;
+      r = S.check();
+      // RDY_{x,y} = d/L sem + (L-d)/L traj over full maps, against
+      // the contexts present before this call: rows [0, n0).
+      CosArgs cos;
+      cos.in = dcos ? dcos + (a + sb) * cos_stride : nullptr;     // cos(emb_x, sem_y) from the semantic search
+      cos.stride = cos_stride;
+      cos.excl = sb > 0 ? st->excl : nullptr;
+      const float* qe = de + (a + sb) * D;
+      const float* qm = dm + (a + sb) * int64_t(L) * E;
+      const int x0 = int(a + sb), mark = sb == 0 ? int(a) : 0;
+      if (r == FMOE_OK && two) {
+        r = run_search(st, nb, qe, qm, int64_t(L) * E, L, w, k1, n0, 0u, s, nullptr, nullptr, keys1, false, cos);
+        if (r == FMOE_OK) {
+          cudaError_t e = launch_resolve(int(nb), k1, keys1, off, slots_all, x0, n0, dslot, drep, s, need, kk,
+                                         nullptr, mark);
+          if (e != cudaSuccess) r = cuda_fail(e, "resolve launch");
+        }
+      }
+      if (r == FMOE_OK && kk > 0)
+        r = run_search(st, nb, qe, qm, int64_t(L) * E, L, w, kk, n0, 0u, s, nullptr, nullptr, keys, false, cos,
+                       nullptr, 0, 0, 0, nullptr, need);
       if (r == FMOE_OK) {
-        cudaError_t e = launch_resolve(int(nrep), k1, keys1, off, slots_all, int(a), n0, dslot, drep, s, need, kk);
+        cudaError_t e = launch_resolve(int(nb), kk, keys, off, slots_all, x0, n0, dslot, drep, s, nullptr, 0, need,
+                                       mark);
+        if (e == cudaSuccess && sb + nb < nrep)       // claimed: no candidate of later sub-batches
+          e = launch_excl(st->excl, slots_all + x0, int(nb), 0, cap, 1, s);
         if (e != cudaSuccess) r = cuda_fail(e, "resolve launch");
       }
     }
-    if (r == FMOE_OK && kk > 0)
-      r = run_search(st, nrep, qe, qm, int64_t(L) * E, L, w, kk, n0, 0u, s, nullptr, nullptr, keys, false, cos,
-                     nullptr, 0, 0, 0, nullptr, need);
-    if (r == FMOE_OK) {
-      cudaError_t e = launch_resolve(int(nrep), kk, keys, off, slots_all, int(a), n0, dslot, drep, s, nullptr, 0, need);
-      if (e != cudaSuccess) r = cuda_fail(e, "resolve launch");
+    if (r == FMOE_OK && nrep > nsub_rows) {         // leave the bitmap zero for the next call
+      cudaError_t e = launch_excl(st->excl, slots_all + a, int(nrep - nsub_rows), 0, cap, 0, s);
+      if (e != cudaSuccess) r = cuda_fail(e, "bitmap reset launch");
     }
   } else if (r == FMOE_OK) {
     cudaError_t e = launch_append_ids(int(a), n0, off, dslot, drep, s);
@@ -1558,7 +1592,8 @@ fmoe_status sharded_insert(fmoe_store* st, int64_t B, const float* emb, const fl
   fmoe_store::Dist& ds_ = *st->dist;
   const int64_t C = ds_.cap_total, n0 = ds_.n_total, off = st->cfg.id_offset, capl = st->cfg.capacity;
   const int64_t a = B < C - n0 ? B : C - n0, nrep = B - a;
-  if (nrep > FMOE_MAX_K) return fail(FMOE_ERR_INVALID_ARG, "more than 64 rows of one insert need replacement");
+  fmoe_status xs = ensure_excl(st, nrep);
+  if (xs != FMOE_OK) return xs;
   const int L = st->cfg.L, E = st->cfg.E, D = st->cfg.D;
   DeviceGuard g(st->device);
   cudaStream_t s = static_cast<cudaStream_t>(stream);
@@ -1570,29 +1605,44 @@ fmoe_status sharded_insert(fmoe_store* st, int64_t B, const float* emb, const fl
   int64_t* dslot = S.out(out_slot, size_t(B));
   int64_t* drep = S.out(out_replaced, size_t(B));
   int64_t* slots_all = static_cast<int64_t*>(S.scratch(size_t(B) * 8));
-  const int kk = int(nrep < n0 ? nrep : n0) > 0 ? int(nrep < n0 ? nrep : n0) : 1;
-  float* ls = static_cast<float*>(S.scratch(size_t(nrep > 0 ? nrep : 1) * kk * 4));
-  int64_t* li = static_cast<int64_t*>(S.scratch(size_t(nrep > 0 ? nrep : 1) * kk * 8));
-  uint64_t* mkeys = static_cast<uint64_t*>(S.scratch(size_t(nrep > 0 ? nrep : 1) * kk * 8));
   fmoe_status r = S.check();
-  if (r == FMOE_OK && nrep > 0) {
-    if (n_loc0 > 0) {
-      CosArgs cos;
-      cos.in = dcos ? dcos + a * cos_stride : nullptr;
-      cos.stride = cos_stride;
-      // RDY = d/L sem + (L-d)/L traj over full maps, unchecked queries
-      r = run_search(st, nrep, de + a * D, dm + a * int64_t(L) * E, int64_t(L) * E, L, float(st->cfg.d) / float(L),
-                     kk, n_loc0, uint32_t(off), s, ls, li, nullptr, false, cos);
-    } else {
-      cudaError_t e = launch_merge_keys(int(nrep), 0, kk, nullptr, kk, nullptr, ls, li, nullptr, s);
-      if (e != cudaSuccess) r = cuda_fail(e, "merge launch");
+  // sub-batches of <= 64 rows, as the single-GPU insert (later ones skip the
+  // slots earlier ones claimed; every rank marks the victims it owns)
+  const int64_t nsub_rows = FMOE_MAX_K;
+  for (int64_t sb = 0; r == FMOE_OK && (sb < nrep || (sb == 0 && nrep == 0)); sb += nsub_rows) {
+    const int64_t nb = nrep - sb < nsub_rows ? nrep - sb : nsub_rows;
+    const int kk = int(nb < n0 ? nb : n0) > 0 ? int(nb < n0 ? nb : n0) : 1;
+    float* ls = static_cast<float*>(S.scratch(size_t(nb > 0 ? nb : 1) * kk * 4));
+    int64_t* li = static_cast<int64_t*>(S.scratch(size_t(nb > 0 ? nb : 1) * kk * 8));
+    uint64_t* mkeys = static_cast<uint64_t*>(S.scratch(size_t(nb > 0 ? nb : 1) * kk * 8));
+    r = S.check();
+    if (r == FMOE_OK && nb > 0) {
+      if (n_loc0 > 0) {
+        CosArgs cos;
+        cos.in = dcos ? dcos + (a + sb) * cos_stride : nullptr;
+        cos.stride = cos_stride;
+        cos.excl = sb > 0 ? st->excl : nullptr;
+        // RDY = d/L sem + (L-d)/L traj over full maps, unchecked queries
+        r = run_search(st, nb, de + (a + sb) * D, dm + (a + sb) * int64_t(L) * E, int64_t(L) * E, L,
+                       float(st->cfg.d) / float(L), kk, n_loc0, uint32_t(off), s, ls, li, nullptr, false, cos);
+      } else {
+        cudaError_t e = launch_merge_keys(int(nb), 0, kk, nullptr, kk, nullptr, ls, li, nullptr, s);
+        if (e != cudaSuccess) r = cuda_fail(e, "merge launch");
+      }
+      if (r == FMOE_OK) r = exchange_topk(st, S, nb, kk, ls, li, nullptr, nullptr, mkeys, s);
     }
-    if (r == FMOE_OK) r = exchange_topk(st, S, nrep, kk, ls, li, nullptr, nullptr, mkeys, s);
+    if (r == FMOE_OK) {
+      // keys hold global ids; appended rows get global slots n0 + x
+      cudaError_t e = launch_resolve(int(nb > 0 ? nb : 0), kk, mkeys, 0u, slots_all, int(a + sb), n0, dslot, drep, s,
+                                     nullptr, 0, nullptr, sb == 0 ? int(a) : 0);
+      if (e == cudaSuccess && sb + nb < nrep) e = launch_excl(st->excl, slots_all + a + sb, int(nb), off, capl, 1, s);
+      if (e != cudaSuccess) r = cuda_fail(e, "resolve launch");
+    }
+    if (nrep == 0) break;
   }
-  if (r == FMOE_OK) {
-    // keys hold global ids; appended rows get global slots n0 + x
-    cudaError_t e = launch_resolve(int(nrep), kk, mkeys, 0u, slots_all, int(a), n0, dslot, drep, s);
-    if (e != cudaSuccess) r = cuda_fail(e, "resolve launch");
+  if (r == FMOE_OK && nrep > nsub_rows) {
+    cudaError_t e = launch_excl(st->excl, slots_all + a, int(nrep - nsub_rows), off, capl, 0, s);
+    if (e != cudaSuccess) r = cuda_fail(e, "bitmap reset launch");
   }
   if (r == FMOE_OK) {
     WriteArgs w{};

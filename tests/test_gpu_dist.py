@@ -66,6 +66,10 @@ def _calls(lib, st, sh, emb, maps, dev):
     lib.fmoe_search_semantic_cos(st._h, emb[C + 40:C + 64].to(dev), 8, s0, i0, cos, stride)
     lib.fmoe_store_insert_cos(st._h, emb[C + 40:C + 64].to(dev), maps[C + 40:C + 64].to(dev), cos, stride, sl, rp)
     res["ins_cos"] = (sl, rp)
+    # > 64 replacements in one call: sub-batches with the claimed-slot bitmap
+    big_e = torch.cat([emb[100:101].repeat(30, 1), emb[200:270]])
+    big_m = torch.cat([maps[100:101].repeat(30, 1, 1), maps[200:270]])
+    res["ins_big"] = st.insert(big_e.to(dev), big_m.to(dev))
     res["sem2"] = st.search_semantic(qe, 8)
     res["size"] = (torch.tensor([len(st)]),)
     return {k: tuple(t.cpu().numpy().copy() for t in v if t is not None) for k, v in res.items()}

@@ -197,13 +197,14 @@ def test_session_sweep_midsize(mid):
             assert int(gc[ell - 1, 0]) == oc[0][0]
 
 
+@pytest.mark.parametrize("B", [64, 256])
 @pytest.mark.parametrize("name,dt", [("qwen", "bf16"), ("mixtral", "bf16"), ("mixtral", "f32")])
-def test_rdy_insert_midsize(lib, name, dt):
+def test_rdy_insert_midsize(lib, name, dt, B):
     """Insert at full capacity (Reading R8) with many conflicting rows
     (copies of one stored context) next to fresh ones, plain and with the
     cached semantic cosines: slots equal O.Store.insert."""
     sh = SHAPES[name]
-    C, B = 160_013, 64
+    C = 160_013
     st = lib.ExpertMapStore(sh.L, sh.E, sh.K, sh.D, 3, C, dt)
     st2 = lib.ExpertMapStore(sh.L, sh.E, sh.K, sh.D, 3, C, dt)
     for a in range(0, C, 65536):
@@ -214,7 +215,7 @@ def test_rdy_insert_midsize(lib, name, dt):
     ref = O.Store(C, sh.L, sh.E, sh.D, 3)
     ref.insert(Qe, Qm)
     fe, fm_, _ = S.store_rows(sh, 79, 0, B)
-    n_dup = 24
+    n_dup = 24 if B <= 64 else 90
     be = torch.cat([torch.from_numpy(Qe[4321:4322]).float().repeat(n_dup, 1), fe[:B - n_dup]])
     bm = torch.cat([torch.from_numpy(Qm[4321:4322]).float().repeat(n_dup, 1, 1), fm_[:B - n_dup]])
     slot, rep = st.insert(be.cuda(), bm.cuda())

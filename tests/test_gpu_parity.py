@@ -280,8 +280,37 @@ def test_insert_duplicate_batch_distinct_victims(lib):
     rs, _ = ref.insert(O.quantize(emb[17:18].repeat(5, 1).numpy(), "bf16"),
                        O.quantize(maps[17:18].repeat(5, 1, 1).numpy(), "bf16"))
     assert s == rs
-    with pytest.raises(lib.FmoeError):                  # > 64 replacements in one call
-        st.insert(emb[:65].cuda(), maps[:65].cuda())
+    st.close()
+
+
+@pytest.mark.parametrize("dtype", ["bf16", "f32"])
+@pytest.mark.parametrize("B,n_dup", [(65, 0), (130, 70), (256, 100), (300, 200)])
+def test_insert_large_batches_match_oracle(lib, dtype, B, n_dup):
+    """More than 64 rows of one insert need a victim: sub-batches of 64, later
+    ones skipping the slots earlier ones claimed (Reading R8) --
+    equal to the oracle's sequential rule, with many rows competing for the
+    same victims (n_dup copies of one stored context) and a mixed
+    append/replace batch."""
+    sh = S.Shape("mixL", 8, 8, 2, 48, n_clusters=4)
+    C = 900
+    emb, maps, _ = S.store_rows(sh, 14, 0, C + 400)
+    st = lib.ExpertMapStore(sh.L, sh.E, sh.K, sh.D, 3, C, dtype)
+    ref = O.Store(C, sh.L, sh.E, sh.D, 3)
+    Qz = lambda x: O.quantize(x.numpy(), dtype)
+    st.insert(emb[:C - 20].cuda(), maps[:C - 20].cuda())      # 20 slots left: the batch appends first
+    ref.insert(Qz(emb[:C - 20]), Qz(maps[:C - 20]))
+    be = torch.cat([emb[77:78].repeat(n_dup, 1), emb[C:C + B - n_dup]])
+    bm = torch.cat([maps[77:78].repeat(n_dup, 1, 1), maps[C:C + B - n_dup]])
+    slot, rep = st.insert(be.cuda(), bm.cuda())
+    rs, rr = ref.insert(Qz(be), Qz(bm))
+    assert slot.cpu().tolist() == rs
+    assert rep.cpu().tolist() == rr
+    ge, gm = st.read(0, C)
+    assert np.array_equal(ge.cpu().numpy().astype(np.float64), ref.emb)
+    assert np.array_equal(gm.cpu().numpy().astype(np.float64), ref.maps)
+    slot, rep = st.insert(be[:70].cuda(), bm[:70].cuda())       # the bitmap was left clean
+    rs, rr = ref.insert(Qz(be[:70]), Qz(bm[:70]))
+    assert slot.cpu().tolist() == rs
     st.close()
 
 
