@@ -319,6 +319,30 @@ fmoe_status fmoe_prefetch_plan(const fmoe_store* store, int64_t B, const int64_t
                                int32_t max_jobs, int32_t* out_layer, int32_t* out_expert, double* out_priority,
                                int32_t* out_njobs, void* stream);
 
+/* Expert prefetch copies driven by the guidance (P:528-533 publisher/
+ * subscriber, P:573-580 PRI^prefetch, P:595-597 loading the experts of the
+ * next layers, P:618-619 expert management through the CUDA runtime).  On
+ * `copy_stream`: optionally wait (on the device, cuStreamWaitValue32) until
+ * the DEVICE flag `wait_flag` >= 1 -- e.g. guidance_ready[s] of a session
+ * sweep --, run fmoe_prefetch_plan for queries [B] (map_id, score: DEVICE
+ * arrays the guidance wrote, read after the wait), bring the jobs to the host,
+ * then issue ONE cudaMemcpyAsync per job, in plan order (priority descending),
+ * host_expert[t*E + j] -> dev_expert[t*E + j] of expert_bytes bytes, skipping
+ * experts whose bit j is set in resident_mask[t] (host, [L], may be NULL; the
+ * call sets the bits of the experts it copies).  The calling thread blocks
+ * until the plan is known (the copies themselves are asynchronous on
+ * copy_stream): a copy-manager thread of a serving system.  host_expert must
+ * be pinned for the copies to overlap.  Outputs (host, may be NULL):
+ * out_layer / out_expert [B][max_jobs] of the jobs issued (-1 past the end),
+ * out_njobs [B].  Same argument rules as fmoe_prefetch_plan; not for sharded
+ * stores.  FMOE_ERR_UNSUPPORTED if the device lacks stream memory operations
+ * (wait_flag given). */
+fmoe_status fmoe_prefetch_issue(const fmoe_store* store, int64_t B, const int64_t* map_id, const float* score,
+                                float delta, int32_t l_now, int32_t layer_begin, int32_t layer_end, int32_t max_jobs,
+                                const void* const* host_expert, void* const* dev_expert, int64_t expert_bytes,
+                                uint64_t* resident_mask, const uint32_t* wait_flag, void* copy_stream,
+                                int32_t* out_layer, int32_t* out_expert, int32_t* out_njobs);
+
 /* Eviction order of n cached experts: PRI^evict = 1 / (max(p, eps)
  * * freq) in float64 (p floored at eps, Reading R13), and out_order [n]
  * = cache indices by priority descending, ties -> lower index (= earlier

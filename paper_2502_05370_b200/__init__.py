@@ -82,6 +82,7 @@ def _load():
         "fmoe_topk_merge": (I32, [I64, I32, I32, P, P, I32, P, P, ctypes.c_int, P]),
         "fmoe_prefetch_plan": (I32, [P, I64, P, P, F, I32, I32, I32, I32, P, P, P, P, P]),
         "fmoe_eviction_order": (I32, [I64, P, P, F, P, P, ctypes.c_int, P]),
+        "fmoe_prefetch_issue": (I32, [P, I64, P, P, F, I32, I32, I32, I32, P, P, I64, P, P, P, P, P, P]),
         "fmoe_expert_hits": (I32, [I64, I32, I32, I32, P, P, P, P, ctypes.c_int, P]),
         "fmoe_status_string": (ctypes.c_char_p, [I32]),
         "fmoe_last_error": (ctypes.c_char_p, []),
@@ -102,7 +103,7 @@ ABI_SYMBOLS = ("fmoe_store_create", "fmoe_store_create_sharded", "fmoe_get_nccl_
                "fmoe_search_blend", "fmoe_search_blend_cos", "fmoe_select_experts", "fmoe_traj_session_create", "fmoe_traj_session_step",
                "fmoe_traj_session_step_select", "fmoe_traj_session_sweep",
                "fmoe_traj_session_reset", "fmoe_traj_session_abandoned", "fmoe_traj_session_destroy", "fmoe_topk_merge",
-               "fmoe_prefetch_plan", "fmoe_eviction_order", "fmoe_expert_hits", "fmoe_status_string",
+               "fmoe_prefetch_plan", "fmoe_prefetch_issue", "fmoe_eviction_order", "fmoe_expert_hits", "fmoe_status_string",
                "fmoe_last_error", "fmoe_kernel_launch_count", "fmoe_set_host_sync")
 
 
@@ -230,6 +231,24 @@ def fmoe_prefetch_plan(h, map_id, score, delta, l_now, layer_begin, layer_end, m
     _check(_lib.fmoe_prefetch_plan(h, map_id.shape[0], _ptr(map_id), _ptr(score), delta, l_now, layer_begin, layer_end,
                                    max_jobs, _ptr(out_layer), _ptr(out_expert), _ptr(out_priority), _ptr(out_njobs),
                                    _stream(stream)))
+
+
+def fmoe_prefetch_issue(h, map_id, score, delta, l_now, layer_begin, layer_end, max_jobs, host_expert_ptrs,
+                        dev_expert_ptrs, expert_bytes, resident_mask=None, wait_flag=None, copy_stream=None):
+    """Issue the expert copies of the prefetch plan (include/fmoe.h).  host_expert_ptrs /
+    dev_expert_ptrs: sequences of L*E addresses (int); resident_mask: CPU int64 tensor [L]
+    (updated in place) or None.  Returns (layers, experts, njobs) host tensors of the copies issued."""
+    B = map_id.shape[0]
+    n = len(host_expert_ptrs)
+    hp = (ctypes.c_void_p * n)(*host_expert_ptrs)
+    dp = (ctypes.c_void_p * n)(*dev_expert_ptrs)
+    lay = torch.empty(B, max_jobs, dtype=torch.int32)
+    exp = torch.empty(B, max_jobs, dtype=torch.int32)
+    nj = torch.empty(B, dtype=torch.int32)
+    _check(_lib.fmoe_prefetch_issue(h, B, _ptr(map_id), _ptr(score), delta, l_now, layer_begin, layer_end, max_jobs,
+                                    hp, dp, int(expert_bytes), _ptr(resident_mask), _ptr(wait_flag),
+                                    _stream(copy_stream), _ptr(lay), _ptr(exp), _ptr(nj)))
+    return lay, exp, nj
 
 
 def fmoe_eviction_order(p, freq, eps, out_priority, out_order, device=0, stream=None):

@@ -11,6 +11,8 @@
 #include <unordered_map>
 #include <vector>
 
+#include <cuda.h>
+
 #include "../../include/fmoe.h"
 #include "common.cuh"
 #include "kernels.cuh"
@@ -1414,6 +1416,86 @@ fmoe_status fmoe_prefetch_plan(const fmoe_store* st, int64_t B, const int64_t* m
     cudaError_t e = launch_prefetch_plan(st->view(), int(B), did, dsc, delta, st->cfg.K, l_now, layer_begin,
                                          layer_end, st->cfg.id_offset, st->n, max_jobs, dl, de, dp, dn, s);
     if (e != cudaSuccess) r = cuda_fail(e, "plan launch");
+  }
+  return S.finish(r);
+}
+
+fmoe_status fmoe_prefetch_issue(const fmoe_store* st, int64_t B, const int64_t* map_id, const float* score,
+                                float delta, int32_t l_now, int32_t layer_begin, int32_t layer_end, int32_t max_jobs,
+                                const void* const* host_expert, void* const* dev_expert, int64_t expert_bytes,
+                                uint64_t* resident_mask, const uint32_t* wait_flag, void* copy_stream,
+                                int32_t* out_layer, int32_t* out_expert, int32_t* out_njobs) {
+  if (!st || !map_id || !host_expert || !dev_expert || expert_bytes < 1)
+    return fail(FMOE_ERR_INVALID_ARG, "null argument / expert_bytes");
+  if (st->dist) return fail(FMOE_ERR_UNSUPPORTED, "prefetch copies on a sharded store");
+  if (B < 0 || max_jobs < 1) return fail(FMOE_ERR_INVALID_ARG, "B / max_jobs");
+  if (layer_begin < 0 || layer_begin >= layer_end || layer_end > st->cfg.L || l_now >= layer_begin)
+    return fail(FMOE_ERR_INVALID_ARG, "need l_now < layer_begin < layer_end <= L");
+  if ((layer_end - layer_begin) * st->cfg.E > 2048) return fail(FMOE_ERR_INVALID_ARG, "too many (layer, expert) jobs");
+  if (!(delta <= 1.f)) return fail(FMOE_ERR_INVALID_ARG, "delta must be <= 1 (negative = dynamic)");
+  if (delta < 0.f && !score) return fail(FMOE_ERR_INVALID_ARG, "dynamic delta needs score");
+  if (B == 0) return FMOE_OK;
+  DeviceGuard g(st->device);
+  cudaStream_t s = static_cast<cudaStream_t>(copy_stream);
+  if (ptr_kind(map_id, st->device) != 1 || (score && ptr_kind(score, st->device) != 1) ||
+      (wait_flag && ptr_kind(wait_flag, st->device) != 1))
+    return fail(FMOE_ERR_INVALID_ARG, "map_id / score / wait_flag must be device memory of the store's device");
+  if (wait_flag) {
+    // the guidance is published by a device flag: the copy stream waits on the
+    // device (no host polling), then reads the plan
+    using WaitFn = CUresult (*)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
+    static WaitFn wait = nullptr;
+    static std::once_flag once;
+    std::call_once(once, [] {
+      void* fn = nullptr;
+      cudaDriverEntryPointQueryResult q;
+      if (cudaGetDriverEntryPoint("cuStreamWaitValue32", &fn, cudaEnableDefault, &q) == cudaSuccess &&
+          q == cudaDriverEntryPointSuccess)
+        wait = reinterpret_cast<WaitFn>(fn);
+    });
+    if (!wait) return fail(FMOE_ERR_UNSUPPORTED, "cuStreamWaitValue32 unavailable");
+    if (wait(s, reinterpret_cast<CUdeviceptr>(wait_flag), 1u, CU_STREAM_WAIT_VALUE_GEQ) != CUDA_SUCCESS)
+      return fail(FMOE_ERR_UNSUPPORTED, "stream memory operations unsupported on this device");
+  }
+  const size_t nj = size_t(B) * max_jobs;
+  Staging S(s, st->device, true);
+  int32_t* dl = static_cast<int32_t*>(S.scratch(nj * 4));
+  int32_t* de = static_cast<int32_t*>(S.scratch(nj * 4));
+  double* dp = static_cast<double*>(S.scratch(nj * 8));
+  int32_t* dn = static_cast<int32_t*>(S.scratch(size_t(B) * 4));
+  fmoe_status r = S.check();
+  if (r != FMOE_OK) return S.finish(r);
+  cudaError_t e = launch_prefetch_plan(st->view(), int(B), map_id, delta < 0.f ? score : nullptr, delta, st->cfg.K,
+                                       l_now, layer_begin, layer_end, st->cfg.id_offset, st->n, max_jobs, dl, de, dp,
+                                       dn, s);
+  std::vector<int32_t> hl(nj), he(nj), hn(static_cast<size_t>(B));
+  if (e == cudaSuccess) e = cudaMemcpyAsync(hl.data(), dl, nj * 4, cudaMemcpyDeviceToHost, s);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(he.data(), de, nj * 4, cudaMemcpyDeviceToHost, s);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(hn.data(), dn, size_t(B) * 4, cudaMemcpyDeviceToHost, s);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(s);           // the plan is on the host
+  if (e != cudaSuccess) return S.finish(cuda_fail(e, "prefetch plan"));
+  const int E = st->cfg.E;
+  // plan order per query (priority descending); queries in batch order
+  for (int64_t x = 0; x < B && r == FMOE_OK; ++x) {
+    int issued = 0;
+    for (int j = 0; j < hn[x] && j < max_jobs; ++j) {
+      const int t = hl[x * max_jobs + j], ex = he[x * max_jobs + j];
+      if (t < 0 || ex < 0) continue;
+      const uint64_t bit = uint64_t(1) << ex;
+      if (resident_mask && (resident_mask[t] & bit)) continue;   // already resident (or copied for an earlier query)
+      const size_t idx = size_t(t) * E + ex;
+      e = cudaMemcpyAsync(dev_expert[idx], host_expert[idx], size_t(expert_bytes), cudaMemcpyHostToDevice, s);
+      if (e != cudaSuccess) { r = cuda_fail(e, "expert copy"); break; }
+      if (resident_mask) resident_mask[t] |= bit;
+      if (out_layer) out_layer[x * max_jobs + issued] = t;
+      if (out_expert) out_expert[x * max_jobs + issued] = ex;
+      ++issued;
+    }
+    for (int j = issued; j < max_jobs; ++j) {
+      if (out_layer) out_layer[x * max_jobs + j] = -1;
+      if (out_expert) out_expert[x * max_jobs + j] = -1;
+    }
+    if (out_njobs) out_njobs[x] = issued;
   }
   return S.finish(r);
 }

@@ -782,3 +782,53 @@ def test_semantic_rerank_fallback_on_ties(lib, B, k):
     check_topk(gs, gi, ref, k)
     assert gi[0].tolist() == ([7] + list(range(100, 100 + k - 1)))[:k]
     st.close()
+
+
+def test_prefetch_issue_copies_the_plan(setup):
+    """fmoe_prefetch_issue: the copy stream
+    waits on the device for the guidance flag (set late by another stream),
+    then one cudaMemcpyAsync per planned expert, in PRI^prefetch order,
+    skipping resident experts: the copied set and order equal O.prefetch_plan
+    and exactly those device slots receive the host weights."""
+    lib, st, sh = setup["lib"], setup["st"], setup["shape"]
+    L, E = sh.L, sh.E
+    B, l_now, lb, le = 3, 2, 3, min(6, sh.L)
+    max_jobs = (le - lb) * E
+    q = setup["q_emb"][:B].cuda()
+    gs, gi = st.search_semantic(q, 1)
+    ids, sc = gi[:, 0].contiguous(), gs[:, 0].contiguous()
+    eb = 256                                                  # bytes per (synthetic) expert
+    host = torch.arange(L * E, dtype=torch.int32).repeat_interleave(eb // 4).view(L * E, eb // 4).pin_memory()
+    dev = torch.full((L * E, eb // 4), -1, dtype=torch.int32, device="cuda")
+    hp = [host[i].data_ptr() for i in range(L * E)]
+    dp = [dev[i].data_ptr() for i in range(L * E)]
+    resident = torch.zeros(L, dtype=torch.int64)
+    resident[lb] = 1                                          # expert 0 of layer lb is already on the GPU
+    flag = torch.zeros(1, dtype=torch.int32, device="cuda")
+    side, copy = torch.cuda.Stream(), torch.cuda.Stream()
+    torch.cuda.synchronize()
+    with torch.cuda.stream(side):
+        torch.cuda._sleep(20_000_000)                        # the guidance arrives late
+        flag.fill_(1)
+    lay, exp, nj = lib.fmoe_prefetch_issue(st._h, ids, sc, -1.0, l_now, lb, le, max_jobs, hp, dp, eb,
+                                           resident, flag, copy)
+    copy.synchronize()
+    plans = O.prefetch_plan(setup["Qm"], ids.cpu().tolist(), sc.cpu().double().tolist(), -1.0, list(range(lb, le)),
+                            sh.K, l_now)
+    seen = {(lb, 0)}
+    copied = set()
+    for x in range(B):
+        want = []
+        for t, j, _ in plans[x][:max_jobs]:
+            if (t, j) not in seen:
+                seen.add((t, j))
+                want.append((t, j))
+        n = nj[x].item()
+        assert list(zip(lay[x, :n].tolist(), exp[x, :n].tolist())) == want
+        copied |= set(want)
+    got = dev.cpu()
+    for t in range(L):
+        for j in range(E):
+            i = t * E + j
+            assert torch.equal(got[i], host[i]) == ((t, j) in copied), (t, j)
+            assert bool(resident[t].item() >> j & 1) == ((t, j) in copied or (t, j) == (lb, 0))

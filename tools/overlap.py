@@ -17,8 +17,18 @@ overhead), the matcher alone, and per target layer the slack between "guidance
 ready" (side-stream event) and "forward starts that layer" (main-stream event):
 negative slack = the guidance arrived too late to prefetch.
 
-  python tools/overlap.py [--N 1000000] [--iters 20] [--out profiles/...json]
+  python tools/overlap.py [--N 1000000] [--iters 20] [--out profiles/...json] [--copies --expert-mb 352]
+
+--copies adds the expert loading the guidance drives (P:573-580, P:595-597,
+P:618-619): after each session step the side stream raises a device flag; a
+copy-manager thread calls fmoe_prefetch_issue, which makes a copy stream wait
+on that flag on the device, computes the PRI^prefetch plan of the target layer
+and issues one cudaMemcpyAsync per planned expert from pinned host memory into
+device expert slots (a ring: weights of every expert share one pinned buffer
+of --expert-mb MB; content is irrelevant, the DMA is real).  Reports per target
+layer the copy completion vs the forward reaching that layer.
 """
+import threading
 import argparse
 import json
 import os
@@ -41,6 +51,9 @@ def main():
     ap.add_argument("--iters", type=int, default=20)
     ap.add_argument("--tokens", type=int, default=1)
     ap.add_argument("--out", default=None)
+    ap.add_argument("--copies", action="store_true")
+    ap.add_argument("--expert-mb", type=float, default=3 * 4096 * 14336 * 2 / 2 ** 20)   # one Mixtral expert
+    ap.add_argument("--slots", type=int, default=8)
     a = ap.parse_args()
     dev = torch.device("cuda:0")
     torch.cuda.set_device(dev)
@@ -95,13 +108,49 @@ def main():
     def E():
         return torch.cuda.Event(enable_timing=True)
 
-    def iteration(do_fwd, do_match, rec=None):
+    # ---- expert copies driven by the guidance (--copies)
+    eb = int(a.expert_mb * 2 ** 20) // 16 * 16
+    if a.copies:
+        host_w = torch.empty(eb, dtype=torch.uint8).pin_memory()
+        dev_slots = torch.empty(a.slots, eb, dtype=torch.uint8, device=dev)
+        host_ptrs = [host_w.data_ptr()] * (L * sh.E)
+        dev_ptrs = [dev_slots[(t * sh.E + j) % a.slots].data_ptr() for t in range(L) for j in range(sh.E)]
+        copy_s = torch.cuda.Stream(device=dev)
+        flags = torch.zeros(L, dtype=torch.int32, device=dev)
+        one = torch.ones(1, dtype=torch.int32).pin_memory()
+        step_ids = torch.empty(L, 1, dtype=torch.int64, device=dev)
+        step_sc = torch.empty(L, 1, device=dev)
+
+    def copy_manager(t0, copied, n_jobs):
+        """One fmoe_prefetch_issue per target layer, each gated on its step's device flag."""
+        resident = torch.zeros(L, dtype=torch.int64)
+        for ell in range(1, L):
+            tgt = ell - 1 + d
+            if tgt >= L:
+                break
+            lay, exp, nj = fm.fmoe_prefetch_issue(h, step_ids[ell], step_sc[ell], -1.0, ell - 1, tgt, tgt + 1, sh.E,
+                                                  host_ptrs, dev_ptrs, eb, resident, flags[ell:ell + 1], copy_s)
+            ev = E()
+            ev.record(copy_s)
+            copied[tgt] = ev
+            n_jobs[tgt] = int(nj[0])
+
+    def iteration(do_fwd, do_match, rec=None, do_copy=False):
         t0, start, ready, gate_ev = E(), [E() for _ in range(L)], [None] * L, [E() for _ in range(L)]
         f_end, m_end = E(), E()
         main_s.wait_stream(torch.cuda.current_stream())
         side_s.wait_stream(torch.cuda.current_stream())
+        copied, n_jobs, th = [None] * L, [0] * L, None
+        if do_copy:
+            flags.zero_()
+            copy_s.wait_stream(torch.cuda.current_stream())
+            torch.cuda.synchronize()
         t0.record(main_s)
         side_s.wait_event(t0)
+        if do_copy:
+            copy_s.wait_event(t0)
+            th = threading.Thread(target=copy_manager, args=(t0, copied, n_jobs))
+            th.start()
         if do_match:
             with torch.cuda.stream(side_s):
                 step.semantic(h, q_emb, k, out_s, out_i)
@@ -128,6 +177,10 @@ def main():
                         r = E()
                         r.record(side_s)
                         ready[tgt] = r
+                        if do_copy:                                  # publish the guidance of step ell
+                            step_ids[ell].copy_(out_i[0])
+                            step_sc[ell].copy_(out_s[0])
+                            flags[ell:ell + 1].copy_(one, non_blocking=True)
                     else:
                         fm.fmoe_traj_session_step(step.sess, lay, k, out_s, out_i)
         if do_match:
@@ -135,13 +188,22 @@ def main():
                 step.insert(h, new_emb, new_maps)
         f_end.record(main_s)
         m_end.record(side_s)
+        if th is not None:
+            th.join()
         torch.cuda.current_stream().wait_stream(main_s)
         torch.cuda.current_stream().wait_stream(side_s)
+        if do_copy:
+            torch.cuda.current_stream().wait_stream(copy_s)
         torch.cuda.synchronize()
         res = {"fwd_ms": t0.elapsed_time(f_end) if do_fwd else None,
                "match_ms": t0.elapsed_time(m_end) if do_match else None}
         if do_fwd and do_match:
             res["slack_ms"] = [t0.elapsed_time(start[t]) - t0.elapsed_time(ready[t]) for t in range(L)]
+        if do_copy:
+            res["copy_slack_ms"] = [t0.elapsed_time(start[t]) - t0.elapsed_time(copied[t]) if copied[t] else None
+                                    for t in range(L)]
+            res["copy_done_ms"] = max(t0.elapsed_time(c) for c in copied if c)
+            res["experts_copied"] = sum(n_jobs)
         return res
 
     for _ in range(3):
@@ -150,6 +212,9 @@ def main():
     for name, fw, mt in (("forward_alone", True, False), ("matcher_alone", False, True), ("concurrent", True, True)):
         rs = [iteration(fw, mt) for _ in range(a.iters)]
         runs[name] = rs
+    if a.copies:
+        iteration(True, True, do_copy=True)
+        runs["with_copies"] = [iteration(True, True, do_copy=True) for _ in range(a.iters)]
     med = lambda v: sorted(v)[len(v) // 2]  # noqa: E731
     fa = med([r["fwd_ms"] for r in runs["forward_alone"]])
     fc = med([r["fwd_ms"] for r in runs["concurrent"]])
@@ -168,6 +233,22 @@ def main():
         "late_layers": [t for t in range(L) if slack[t] < 0],
         "expert_weight_bytes_per_forward": int(L * K * (H * 2 * F + F * H) * 2),
     }
+    if a.copies:
+        wc = runs["with_copies"]
+        cs = [med([r["copy_slack_ms"][t] for r in wc]) if wc[0]["copy_slack_ms"][t] is not None else None
+              for t in range(L)]
+        nexp = med([r["experts_copied"] for r in wc])
+        done = med([r["copy_done_ms"] for r in wc])
+        res["copies"] = {
+            "expert_bytes": eb, "experts_copied_per_iteration": nexp,
+            "forward_ms_with_matcher_and_copies": round(med([r["fwd_ms"] for r in wc]), 4),
+            "copies_done_ms_after_start": round(done, 4),
+            "copy_GBps": round(nexp * eb / (done * 1e-3) / 1e9, 2) if done > 0 else None,
+            "copy_slack_ms_per_target_layer": [None if v is None else round(v, 4) for v in cs],
+            "what": "fmoe_prefetch_issue per target layer ell+d: the copy stream waits on the device for the flag "
+                    "the side stream raises after step ell, then one cudaMemcpyAsync per planned expert "
+                    "(pinned host -> device slot), PRI^prefetch order; slack = forward reaches the layer - "
+                    "that layer's copies done (negative: late)"}
     js = json.dumps(res, indent=1)
     print(js)
     if a.out:
