@@ -1440,6 +1440,19 @@ fmoe_status fmoe_prefetch_issue(const fmoe_store* st, int64_t B, const int64_t* 
   if (ptr_kind(map_id, st->device) != 1 || (score && ptr_kind(score, st->device) != 1) ||
       (wait_flag && ptr_kind(wait_flag, st->device) != 1))
     return fail(FMOE_ERR_INVALID_ARG, "map_id / score / wait_flag must be device memory of the store's device");
+  // pinned plan buffer, allocated before the stream waits (an allocation may
+  // synchronise)
+  thread_local int32_t* pin = nullptr;
+  thread_local size_t pin_n = 0;
+  const size_t need = 2 * size_t(B) * max_jobs + size_t(B);
+  if (pin_n < need) {
+    if (pin) cudaFreeHost(pin);
+    pin = nullptr;
+    pin_n = 0;
+    cudaError_t ea = cudaMallocHost(&pin, need * 4);
+    if (ea != cudaSuccess) return cuda_fail(ea, "pinned plan buffer");
+    pin_n = need;
+  }
   if (wait_flag) {
     // the guidance is published by a device flag: the copy stream waits on the
     // device (no host polling), then reads the plan
@@ -1468,10 +1481,16 @@ fmoe_status fmoe_prefetch_issue(const fmoe_store* st, int64_t B, const int64_t* 
   cudaError_t e = launch_prefetch_plan(st->view(), int(B), map_id, delta < 0.f ? score : nullptr, delta, st->cfg.K,
                                        l_now, layer_begin, layer_end, st->cfg.id_offset, st->n, max_jobs, dl, de, dp,
                                        dn, s);
-  std::vector<int32_t> hl(nj), he(nj), hn(static_cast<size_t>(B));
-  if (e == cudaSuccess) e = cudaMemcpyAsync(hl.data(), dl, nj * 4, cudaMemcpyDeviceToHost, s);
-  if (e == cudaSuccess) e = cudaMemcpyAsync(he.data(), de, nj * 4, cudaMemcpyDeviceToHost, s);
-  if (e == cudaSuccess) e = cudaMemcpyAsync(hn.data(), dn, size_t(B) * 4, cudaMemcpyDeviceToHost, s);
+  // the plan comes back through PINNED memory: a copy into pageable memory
+  // would block inside the runtime (holding its locks) until the device wait
+  // on the guidance flag resolves, stalling every other thread's CUDA calls --
+  // including the ones that will eventually raise the flag
+  int32_t* hl = pin;
+  int32_t* he = pin + nj;
+  int32_t* hn = pin + 2 * nj;
+  if (e == cudaSuccess) e = cudaMemcpyAsync(hl, dl, nj * 4, cudaMemcpyDeviceToHost, s);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(he, de, nj * 4, cudaMemcpyDeviceToHost, s);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(hn, dn, size_t(B) * 4, cudaMemcpyDeviceToHost, s);
   if (e == cudaSuccess) e = cudaStreamSynchronize(s);           // the plan is on the host
   if (e != cudaSuccess) return S.finish(cuda_fail(e, "prefetch plan"));
   const int E = st->cfg.E;
