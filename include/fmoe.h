@@ -336,7 +336,11 @@ fmoe_status fmoe_prefetch_plan(const fmoe_store* store, int64_t B, const int64_t
  * out_layer / out_expert [B][max_jobs] of the jobs issued (-1 past the end),
  * out_njobs [B].  Same argument rules as fmoe_prefetch_plan; not for sharded
  * stores.  FMOE_ERR_UNSUPPORTED if the device lacks stream memory operations
- * (wait_flag given). */
+ * (wait_flag given).  A device-side wait blocks the hardware queue copy_stream
+ * maps to: the flag's producer must already be enqueued (or run on a stream
+ * that cannot share that queue), else the two wait on each other -- a
+ * copy-manager thread that learns of the guidance later waits on the host
+ * (an event) and passes wait_flag = NULL. */
 fmoe_status fmoe_prefetch_issue(const fmoe_store* store, int64_t B, const int64_t* map_id, const float* score,
                                 float delta, int32_t l_now, int32_t layer_begin, int32_t layer_end, int32_t max_jobs,
                                 const void* const* host_expert, void* const* dev_expert, int64_t expert_bytes,

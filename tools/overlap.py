@@ -20,11 +20,11 @@ negative slack = the guidance arrived too late to prefetch.
   python tools/overlap.py [--N 1000000] [--iters 20] [--out profiles/...json] [--copies --expert-mb 352]
 
 --copies adds the expert loading the guidance drives (P:573-580, P:595-597,
-P:618-619): after each session step the side stream raises a device flag; a
-copy-manager thread calls fmoe_prefetch_issue, which makes a copy stream wait
-on that flag on the device, computes the PRI^prefetch plan of the target layer
-and issues one cudaMemcpyAsync per planned expert from pinned host memory into
-device expert slots (a ring: weights of every expert share one pinned buffer
+P:618-619): after each session step the side stream records an event; a
+copy-manager thread waits for it and calls fmoe_prefetch_issue, which computes
+the PRI^prefetch plan of the target layer on a copy stream and issues one
+cudaMemcpyAsync per planned expert from pinned host memory into device expert
+slots (a ring: weights of every expert share one pinned buffer
 of --expert-mb MB; content is irrelevant, the DMA is real).  Reports per target
 layer the copy completion vs the forward reaching that layer.
 """
@@ -61,6 +61,7 @@ def main():
     cfg["N"] = a.N
     sh = cfg["shape"]
     L, d, K = sh.L, 3, sh.K
+    print("build", file=sys.stderr, flush=True)
     st = bench.build_store(fm, cfg, a.N, 0, dev, S.BASE_SEED + 1)
     step = bench.Step(fm, st, cfg, "session", True)
     q_emb, q_pre, new_emb, new_maps = bench.make_queries(cfg, a.N, 1, S.BASE_SEED + 1, dev)[0]
@@ -116,20 +117,23 @@ def main():
         host_ptrs = [host_w.data_ptr()] * (L * sh.E)
         dev_ptrs = [dev_slots[(t * sh.E + j) % a.slots].data_ptr() for t in range(L) for j in range(sh.E)]
         copy_s = torch.cuda.Stream(device=dev)
-        flags = torch.zeros(L, dtype=torch.int32, device=dev)
-        one = torch.ones(1, dtype=torch.int32).pin_memory()
         step_ids = torch.empty(L, 1, dtype=torch.int64, device=dev)
         step_sc = torch.empty(L, 1, device=dev)
 
-    def copy_manager(t0, copied, n_jobs):
-        """One fmoe_prefetch_issue per target layer, each gated on its step's device flag."""
+    def copy_manager(t0, copied, n_jobs, guide_ev, guide_set):
+        """One fmoe_prefetch_issue per target layer, each after its step's guidance event.
+        (The library can also make the copy stream wait on a device flag -- wait_flag -- but a
+        device-side wait ahead of the flag's producer in a shared hardware queue deadlocks, and
+        here the producer is enqueued later by another thread: the host waits on the event.)"""
         resident = torch.zeros(L, dtype=torch.int64)
         for ell in range(1, L):
             tgt = ell - 1 + d
             if tgt >= L:
                 break
+            guide_set[ell].wait()              # the main thread has recorded the event
+            guide_ev[ell].synchronize()        # the guidance of step ell is written
             lay, exp, nj = fm.fmoe_prefetch_issue(h, step_ids[ell], step_sc[ell], -1.0, ell - 1, tgt, tgt + 1, sh.E,
-                                                  host_ptrs, dev_ptrs, eb, resident, flags[ell:ell + 1], copy_s)
+                                                  host_ptrs, dev_ptrs, eb, resident, None, copy_s)
             ev = E()
             ev.record(copy_s)
             copied[tgt] = ev
@@ -141,15 +145,16 @@ def main():
         main_s.wait_stream(torch.cuda.current_stream())
         side_s.wait_stream(torch.cuda.current_stream())
         copied, n_jobs, th = [None] * L, [0] * L, None
+        guide_ev = [E() for _ in range(L)]
+        guide_set = [threading.Event() for _ in range(L)]
         if do_copy:
-            flags.zero_()
             copy_s.wait_stream(torch.cuda.current_stream())
             torch.cuda.synchronize()
         t0.record(main_s)
         side_s.wait_event(t0)
         if do_copy:
             copy_s.wait_event(t0)
-            th = threading.Thread(target=copy_manager, args=(t0, copied, n_jobs))
+            th = threading.Thread(target=copy_manager, args=(t0, copied, n_jobs, guide_ev, guide_set))
             th.start()
         if do_match:
             with torch.cuda.stream(side_s):
@@ -180,7 +185,8 @@ def main():
                         if do_copy:                                  # publish the guidance of step ell
                             step_ids[ell].copy_(out_i[0])
                             step_sc[ell].copy_(out_s[0])
-                            flags[ell:ell + 1].copy_(one, non_blocking=True)
+                            guide_ev[ell].record(side_s)
+                            guide_set[ell].set()
                     else:
                         fm.fmoe_traj_session_step(step.sess, lay, k, out_s, out_i)
         if do_match:
@@ -206,13 +212,17 @@ def main():
             res["experts_copied"] = sum(n_jobs)
         return res
 
+    log = lambda *m: print(*m, file=sys.stderr, flush=True)  # noqa: E731
+    log("warm-up")
     for _ in range(3):
         iteration(True, True)
     runs = {}
     for name, fw, mt in (("forward_alone", True, False), ("matcher_alone", False, True), ("concurrent", True, True)):
+        log(name)
         rs = [iteration(fw, mt) for _ in range(a.iters)]
         runs[name] = rs
     if a.copies:
+        log("with copies")
         iteration(True, True, do_copy=True)
         runs["with_copies"] = [iteration(True, True, do_copy=True) for _ in range(a.iters)]
     med = lambda v: sorted(v)[len(v) // 2]  # noqa: E731
@@ -245,8 +255,8 @@ def main():
             "copies_done_ms_after_start": round(done, 4),
             "copy_GBps": round(nexp * eb / (done * 1e-3) / 1e9, 2) if done > 0 else None,
             "copy_slack_ms_per_target_layer": [None if v is None else round(v, 4) for v in cs],
-            "what": "fmoe_prefetch_issue per target layer ell+d: the copy stream waits on the device for the flag "
-                    "the side stream raises after step ell, then one cudaMemcpyAsync per planned expert "
+            "what": "fmoe_prefetch_issue per target layer ell+d, called by a copy-manager thread once step ell's "
+                    "guidance event completed: PRI^prefetch plan on the copy stream, then one cudaMemcpyAsync per planned expert "
                     "(pinned host -> device slot), PRI^prefetch order; slack = forward reaches the layer - "
                     "that layer's copies done (negative: late)"}
     js = json.dumps(res, indent=1)

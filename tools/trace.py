@@ -42,6 +42,11 @@ def main():
     out_i = torch.empty(a.B, a.k, dtype=torch.int64, device="cuda")
 
     sess = fm.fmoe_traj_session_create(st._h, a.B) if a.mode == "session" else None
+    stride = (a.n + 3) // 4 * 4
+    cos = None
+    if a.mode == "blend_cos":
+        cos = torch.empty(a.B, stride, device="cuda")
+        fm.fmoe_search_semantic_cos(st._h, qe, a.k, out_s, out_i, cos, stride)
     lays = [qm[:, l].contiguous() for l in range(a.L)]
 
     def call():
@@ -57,6 +62,8 @@ def main():
             return
         if a.mode == "traj":
             fm.fmoe_search_trajectory(st._h, pre, a.ell, a.k, out_s, out_i)
+        elif a.mode == "blend_cos":
+            fm.fmoe_search_blend_cos(st._h, cos, stride, pre, a.ell, -1.0, a.k, out_s, out_i)
         else:
             fm.fmoe_search_semantic(st._h, qe, a.k, out_s, out_i)
     for _ in range(5):
