@@ -665,6 +665,25 @@ __global__ void __launch_bounds__(kUmThreads, 1)
       cos_issue(1);
     }
     unsigned ci = 0;                                    // this warp's chunk sequence number
+    uint64_t st0 = 0ull, st1 = 0ull, st2 = 0ull, st3 = 0ull;   // candidate stash (see the rare path)
+    int ns = 0;
+    auto admit = [&](uint64_t key) {
+      if (key > g) {
+        const uint64_t root = list_admit(ml_s, uint32_t(LQ) * 8, k, cnt, key);
+        cnt += cnt < k ? 1 : 0;
+        if (root > g) {                                 // a full list: its k-th key bounds the query
+          g = root;
+          thr_s = key_score(g);
+        }
+      }
+    };
+    auto flush = [&]() {
+      if (ns > 0) admit(st0);
+      if (ns > 1) admit(st1);
+      if (ns > 2) admit(st2);
+      if (ns > 3) admit(st3);
+      ns = 0;
+    };
     if (p.no_epi) {
       for (int t = cid; t < p.n_tiles; t += ncl, ++ti) {
         const int as = int(ti % unsigned(AS));
@@ -832,7 +851,10 @@ __global__ void __launch_bounds__(kUmThreads, 1)
         m = 0;
 #endif
         // (the scores go through a local copy: one indexed load per candidate
-        // instead of a 31-deep select chain)
+        // instead of a 31-deep select chain).  Candidates go to a 4-key
+        // register stash admitted once per tile (or when it is full): a warp
+        // then pays one divergent heap insert per stashed key of its busiest
+        // lane, instead of one per chunk in which any lane had a candidate.
         if (m) {
           const uint32_t idb = p.id_offset + uint32_t(yc);
           float scl[32];
@@ -843,17 +865,18 @@ __global__ void __launch_bounds__(kUmThreads, 1)
             m &= m - 1;
             const uint64_t key = pack_key(scl[j], idb + uint32_t(j));
             if (key > g) {
-              const uint64_t root = list_admit(ml_s, uint32_t(LQ) * 8, k, cnt, key);
-              cnt += cnt < k ? 1 : 0;
-              if (root > g) {                     // a full list: its k-th key bounds the query
-                g = root;
-                thr_s = key_score(g);
-              }
+              if (ns == 4) flush();
+              if (ns == 0) st0 = key;
+              else if (ns == 1) st1 = key;
+              else if (ns == 2) st2 = key;
+              else st3 = key;
+              ++ns;
             }
           } while (m);
         }
         EPI_T(4);
       }
+      flush();
       // hand the accumulator stage back first: the arrive is a release, and
       // placed after the threshold's global red it would wait for that red's
       // round trip (the MMA warp, not this warp, is what waits on it)
