@@ -723,10 +723,20 @@ def blas_threads():
 
 
 def cpu_baseline(cfg, seed):
+    """The oracle as it stands on the host: once with every BLAS thread the host
+    offers (`value`, `cores`), once pinned to one thread (`single_thread`)."""
     n_sample = oracle_sample_rows(cfg)
-    v, steps, el, _ = oracle_step_sample(cfg, seed, n_sample, budget_s=15.0)
+    v, steps, el, _ = oracle_step_sample(cfg, seed, n_sample, budget_s=12.0)
+    single = None
+    try:
+        from threadpoolctl import threadpool_limits
+        with threadpool_limits(limits=1):
+            v1, steps1, el1, _ = oracle_step_sample(cfg, seed, n_sample, budget_s=8.0, max_steps=3)
+        single = {"value": round(v1, 4), "cores": 1, "sample": f"{steps1} step(s), {el1:.1f}s"}
+    except ImportError:
+        pass
     return {"value": round(v, 4), "unit": "searches/s", "cores": blas_threads(), "kind": "oracle",
-            "cpu": cpu_model(),
+            "cpu": cpu_model(), "nproc": os.cpu_count(), "single_thread": single,
             "sample": f"{steps} full step(s) ({step_counts(cfg)[0]} searches each) against {n_sample} of the "
                       f"{cfg['N']} stored maps, {el:.1f}s; time scaled x{cfg['N'] / n_sample:.2f} to N (scans are linear in N)"}
 

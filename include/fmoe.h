@@ -149,9 +149,11 @@ fmoe_status fmoe_store_get_config(const fmoe_store* store, fmoe_store_config* ou
  * Outputs: out_slot[B] = the slot (id) written, or -1 if no unclaimed slot was
  * left; out_replaced[B] = the id that was evicted (== out_slot) or -1 if the
  * row was appended.  Either output may be NULL.
- * Limits: at most FMOE_MAX_K rows of one call may need replacement
- * (INVALID_ARG otherwise; split the batch).  A zero-norm embedding is stored
- * and scores 0 against every query (Reading R3). */
+ * Any number of rows may need replacement: they are resolved in sub-batches
+ * of FMOE_MAX_K rows, each scanned against the pre-call store with the slots
+ * earlier sub-batches claimed excluded (a device bitmap), which is the same
+ * rule as one pass over the batch.  A zero-norm embedding is stored and
+ * scores 0 against every query (Reading R3). */
 fmoe_status fmoe_store_insert(fmoe_store* store, int64_t B, const float* emb, const float* maps,
                               int64_t* out_slot, int64_t* out_replaced, void* stream);
 
