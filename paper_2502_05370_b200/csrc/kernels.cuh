@@ -136,6 +136,37 @@ struct SweepArgs {
 int traj_sweep_rows(int64_t n_rows, int* grid_out);   // 0: the store is too large for the register sweep
 cudaError_t launch_traj_sweep(const SweepArgs& a, cudaStream_t stream);
 
+// fp32 batched scan (scan_f32mm.cu): 5 <= nq <= 64 queries per pass, the store
+// streamed once per pass, register-tiled FFMA, per-warp top-k lists.
+struct F32mmPrep {
+  const float* q_emb;      // [nq][D] (null: no semantic part)
+  const float* q_prefix;   // [nq][q_stride] (null: no trajectory part)
+  int64_t q_stride;
+  int D, E, Ep, ell;
+  int n_sem_ch, n_traj_ch, qpitch;
+  int sem, traj;           // parts that decide validity (sem: embeddings scored)
+  float* qop;              // [nq][qpitch]
+  float* rq_s; float* rq_t; float* valid;   // [nq]
+};
+struct F32mmArgs {
+  StoreView st;
+  int64_t n_rows;
+  int ell; float w; int k;
+  int nq, wq;              // queries of this pass, query groups (f32mm_wq(nq))
+  const float* qop; int qpitch;
+  int n_sem_ch, n_traj_ch; // 32-float K chunks (semantic over Dp, trajectory over ell*Ep)
+  const float* rq_s; const float* rq_t;
+  uint32_t id_offset;
+  uint64_t* cand; int cand_q0; int grid;    // cand [B][grid * lists_per_cta][k]
+  float* out_cos; const float* sem_cos; int64_t cos_stride;   // this pass's first query row
+  const uint32_t* excl;
+};
+int f32mm_wq(int nq);
+int f32mm_grid(int64_t n_rows, int nq, bool blend);
+int f32mm_lists_per_cta(int nq);
+cudaError_t launch_f32mm_prep(const F32mmPrep& p, int nq, cudaStream_t s);
+cudaError_t launch_f32mm(const F32mmArgs& a, cudaStream_t s);
+
 // tcgen05 batched scan (scan_umma.cu)
 struct UmmaPlanIn {
   int bf16, nq, k, D, Dp, E, Ep, L, ell;

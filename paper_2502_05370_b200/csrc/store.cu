@@ -557,6 +557,76 @@ fmoe_status run_search_umma_approx(const fmoe_store* st, UmmaPlanIn in, int64_t 
 }
 
 // One scoring call: GEMV scan passes of <= 4 queries, each merging its
+
+// fp32 store, B >= 5: passes of <= 64 queries on the FFMA batched scan
+// (scan_f32mm.cu), each reading the store once, then one merge.
+fmoe_status run_search_f32mm(const fmoe_store* st, int64_t B, const float* dq, const float* dp, int64_t q_stride,
+                             int ell, float w, int k, int64_t n_rows, uint32_t id_offset, cudaStream_t s, float* ds,
+                             int64_t* di, uint64_t* dkeys, bool check_queries, const CosArgs& cos, int k_out) {
+  const bool sem = w != 0.f && !cos.in, traj = w != 1.f;
+  const int nq0 = int(B < 64 ? B : 64);
+  const int grid = f32mm_grid(n_rows, nq0, sem && traj);
+  const int n_lists = grid * f32mm_lists_per_cta(nq0);
+  const int n_sem_ch = sem ? (st->Dp + 31) / 32 : 0;
+  const int n_traj_ch = traj ? (ell * st->Ep + 31) / 32 : 0;
+  const int qpitch = (n_sem_ch + n_traj_ch) * 32;
+  const size_t cand_b = align_up(size_t(B) * n_lists * k * 8);
+  const size_t vec_b = align_up(size_t(B) * 4);
+  const size_t qop_b = align_up(size_t(64) * qpitch * 4);
+  char* buf = nullptr;
+  unsigned* counters = nullptr;
+  unsigned long long* best = nullptr;
+  fmoe_status cs = stream_scratch(st, s, cand_b + 3 * vec_b + qop_b, 1, 1, &buf, &counters, &best);
+  if (cs != FMOE_OK) return cs;
+  uint64_t* cand = reinterpret_cast<uint64_t*>(buf);
+  float* valid = reinterpret_cast<float*>(buf + cand_b);
+  float* rq_s = reinterpret_cast<float*>(buf + cand_b + vec_b);
+  float* rq_t = reinterpret_cast<float*>(buf + cand_b + 2 * vec_b);
+  float* qop = reinterpret_cast<float*>(buf + cand_b + 3 * vec_b);
+  for (int64_t q0 = 0; q0 < B; q0 += 64) {
+    const int nq = int(B - q0 < 64 ? B - q0 : 64);
+    F32mmPrep p{};
+    p.q_emb = sem ? dq + q0 * st->cfg.D : nullptr;
+    p.q_prefix = traj ? dp + q0 * q_stride : nullptr;
+    p.q_stride = q_stride;
+    p.D = st->cfg.D; p.E = st->cfg.E; p.Ep = st->Ep; p.ell = traj ? ell : 0;
+    p.n_sem_ch = n_sem_ch; p.n_traj_ch = n_traj_ch; p.qpitch = qpitch;
+    p.sem = sem; p.traj = traj;
+    p.qop = qop; p.rq_s = rq_s + q0; p.rq_t = rq_t + q0; p.valid = valid + q0;
+    cudaError_t e = launch_f32mm_prep(p, nq, s);
+    if (e != cudaSuccess) return cuda_fail(e, "f32mm prep launch");
+    F32mmArgs a{};
+    a.st = st->view();
+    a.n_rows = n_rows;
+    a.ell = traj ? ell : 0;
+    a.w = w;
+    a.k = k;
+    a.nq = nq;
+    a.wq = f32mm_wq(nq0);          // uniform over the passes (the cand layout)
+    a.qop = qop;
+    a.qpitch = qpitch;
+    a.n_sem_ch = n_sem_ch;
+    a.n_traj_ch = n_traj_ch;
+    a.rq_s = rq_s + q0;
+    a.rq_t = rq_t + q0;
+    a.id_offset = id_offset;
+    a.cand = cand;
+    a.cand_q0 = int(q0);
+    // every pass writes n_lists lists per query: a smaller last pass uses the
+    // first pass's grid and lists-per-CTA so the cand layout stays uniform
+    a.grid = grid;
+    a.out_cos = cos.out ? cos.out + q0 * cos.stride : nullptr;
+    a.sem_cos = cos.in ? cos.in + q0 * cos.stride : nullptr;
+    a.cos_stride = cos.stride;
+    a.excl = cos.excl;
+    e = launch_f32mm(a, s);
+    if (e != cudaSuccess) return cuda_fail(e, "f32mm scan launch");
+  }
+  cudaError_t e = launch_merge_keys(int(B), n_lists, k, cand, k_out > k ? k_out : k,
+                                    check_queries ? valid : nullptr, ds, di, dkeys, s);
+  return e == cudaSuccess ? FMOE_OK : cuda_fail(e, "merge launch");
+}
+
 // candidates in its last block.  `extra` bytes of scratch are reserved after
 // the candidate lists (returned in *extra_ptr) for the caller.
 fmoe_status run_search(const fmoe_store* st, int64_t B, const float* dq, const float* dp, int64_t q_stride, int ell,
@@ -589,6 +659,10 @@ fmoe_status run_search(const fmoe_store* st, int64_t B, const float* dq, const f
                            seed_n, k_out, gate);
   }
   if (gate) return fail(FMOE_ERR_UNSUPPORTED, "gated search needs the tensor-core path");
+  static const bool no_f32mm = getenv("FMOE_NO_F32MM") != nullptr;   // knob: GEMV passes of 4 queries
+  if (!st->bf16 && B > 4 && !seed_ids && !no_f32mm)
+    return run_search_f32mm(st, B, dq, dp, q_stride, ell, w, k, n_rows, id_offset, s, ds, di, dkeys, check_queries,
+                            cos, k_out);
   ScanArgs a{};
   a.st = st->view();
   a.n_rows = n_rows;
@@ -1210,8 +1284,10 @@ fmoe_status fmoe_traj_session_sweep(fmoe_traj_session* ss, const float* q_layers
   }
   const int esz = st->bf16 ? 2 : 4;
   int grid = 1;
+  // without ready flags the row-major sweep takes any store size; with them the
+  // step-major kernel keeps its rows in registers (n <= 8 * 4 * SMs * 256)
   const bool fused = ss->B == 1 && !ss->batched && st->view().Ep * esz == 16 && st->n > 0 && n_steps <= 64 &&
-                     traj_sweep_rows(st->n, &grid) != 0;
+                     ((!layer_ready && !guidance_ready) || traj_sweep_rows(st->n, &grid) != 0);
   if (!fused) {
     // same results through one step call per layer; device flags cannot gate host-issued steps
     if (layer_ready || guidance_ready)

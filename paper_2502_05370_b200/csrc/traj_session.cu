@@ -16,6 +16,7 @@
 // 32/GT rows per pass, PASSES passes per warp iteration so a lane keeps 8
 // slab loads in flight; fused top-k via merge.cuh.
 #include <cstdlib>
+#include <cstring>
 
 #include "common.cuh"
 #include "kernels.cuh"
@@ -712,6 +713,188 @@ __global__ void __launch_bounds__(kSweepTmaThreads, 2) traj_sweep_tma_kernel(con
   if (blockIdx.x == 0 && tid == 0) a.qn_out[0] = qn;
 }
 
+// ------------------------------------------------------------------ sweep, row-major (every layer observed)
+// When every layer of the sweep is already observed (no layer_ready /
+// guidance_ready flags: trace replay, a request whose gates are all known),
+// the steps need no order between them except through each row's running dot,
+// which is private to the row.  So the sweep walks ROWS in the outer loop and
+// the steps in the inner loop: a thread takes a row, streams its n_steps slab
+// entries (16 B) and prefix-norm entries (4 B) in chunks of kRowChunk loads,
+// carries acc in one register from step to step, and folds each step's key
+// into its own per-step best in shared memory.  Nothing synchronises between
+// steps, so the loads of the next chunk / row are never held back by a step
+// barrier (the step-major kernel pays load latency + transfer + reduction per
+// step).  One reduction per block at the end (per-step atomicMax); a second,
+// PDL-launched kernel (one warp per step) writes every step's top-1 and runs
+// the Eq. 4-6 selections, all steps in parallel.  Arithmetic per (row, step)
+// is the step kernel's (same fmaf order, acc + d, acc * r_q * rsqrt(psq)) and
+// the max of packed keys is order-free, so outputs are bit-identical to the
+// step-major kernel.  Any number of rows (no register-residency limit).
+constexpr int kRowChunk = 8;
+
+// Query layers of steps [0, ns) (store-dtype values, qs[s][0..8)) and their
+// running norms, all steps at once (warp w: steps w, w+8, ...), in the step
+// kernel's order: part_s = butterfly sum of v^2 over lanes 0..7 of one warp,
+// t_s = (layer > 0 ? t_{s-1} : 0) + part_s (the step kernel adds the other
+// seven warps' zero partials, which leaves the double unchanged).  Returns the
+// norm after the last step on tid 0.
+template <class Tag>
+__device__ __forceinline__ double sweep_stage_all(const SweepArgs& a, float (*qs)[8], float* rqs, int* valids,
+                                                  double* parts) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int E = a.st.E, ns = a.n_steps;
+  for (int s = warp; s < ns; s += kSweepWarps) {
+    double part = 0.0;
+    if (lane < 8) {
+      const float v = lane < E ? to_store_value(a.q_layers[int64_t(s) * E + lane], Tag()) : 0.f;
+      qs[s][lane] = v;
+      part = double(v) * double(v);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
+    if (lane == 0) parts[s] = part;
+  }
+  __syncthreads();
+  double qn = a.layer0 > 0 ? a.qn_in[0] : 0.0;
+  if (tid == 0)
+    for (int s = 0; s < ns; ++s) {
+      double red[kSweepWarps] = {parts[s]};      // warps 1..7 contribute 0, as in the step kernel
+      qn = sweep_norm(qn, a.layer0 + s, red);
+      rqs[s] = qn > 0.0 ? float(1.0 / sqrt(qn)) : 0.f;
+      valids[s] = qn > 0.0;
+    }
+  __syncthreads();
+  return qn;
+}
+
+template <class Tag>
+__global__ void __launch_bounds__(kSweepThreads, 3) traj_sweep_rowmajor_kernel(const SweepArgs a) {
+  using ST = StoreT<Tag>;
+  constexpr int EP = ST::kElemsPer16B;
+  extern __shared__ __align__(16) unsigned long long bk[];   // [n_steps][kSweepThreads] per-thread best keys
+  __shared__ __align__(16) float qs[kSweepMaxSteps][8];
+  __shared__ float rqs[kSweepMaxSteps];
+  __shared__ int valids[kSweepMaxSteps];
+  __shared__ double parts[kSweepMaxSteps];
+
+  const StoreView& st = a.st;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int64_t n = a.n_rows;
+  const int ns = a.n_steps;
+  const int64_t nthr = int64_t(gridDim.x) * kSweepThreads;
+  const char* maps = static_cast<const char*>(st.maps);
+  pdl_wait();
+  pdl_trigger();                 // the finalize kernel may be scheduled; it waits for this grid
+  if (a.abort && ld_acquire_u32(a.abort) != 0u) return;   // poisoned: the finalize kernel reports it
+  // the first chunk of this thread's first row is in flight while the queries are staged
+  const int64_t row0 = int64_t(blockIdx.x) * kSweepThreads + tid;
+  uint4 buf[kRowChunk];
+  float ps[kRowChunk];
+  auto issue = [&](int64_t row, int s0) {
+#pragma unroll
+    for (int j = 0; j < kRowChunk; ++j) {
+      const int64_t layer = a.layer0 + s0 + j;
+      buf[j] = (row < n && s0 + j < ns) ? ld_stream(maps + (layer * st.cap + row) * 16) : make_uint4(0u, 0u, 0u, 0u);
+    }
+#pragma unroll
+    for (int j = 0; j < kRowChunk; ++j) {
+      const int64_t layer = a.layer0 + s0 + j;
+      ps[j] = (row < n && s0 + j < ns) ? __ldcs(st.psq + layer * st.cap + row) : 0.f;
+    }
+  };
+  issue(row0, 0);
+  sweep_stage_all<Tag>(a, qs, rqs, valids, parts);
+  for (int s = 0; s < ns; ++s) bk[s * kSweepThreads + tid] = 0ull;
+
+  for (int64_t row = row0; row < n; row += nthr) {
+    float acc = a.layer0 > 0 ? __ldcs(a.acc + row) : 0.f;
+    const uint32_t gid = a.id_offset + uint32_t(row);
+    for (int s0 = 0; s0 < ns; s0 += kRowChunk) {
+      if (row != row0 || s0 != 0) issue(row, s0);
+#pragma unroll
+      for (int j = 0; j < kRowChunk; ++j) {
+        const int s = s0 + j;
+        if (s < ns) {
+          float x[8];
+          unpack_sess<Tag>(buf[j], x);
+          const float* qv = qs[s];
+          float d = 0.f;
+#pragma unroll
+          for (int e = 0; e < EP; ++e) d = fmaf(x[e], qv[e], d);
+          acc = acc + d;
+          const float rm = ps[j] > 0.f ? rsqrtf(ps[j]) : 0.f;
+          const float sc = acc * rqs[s] * rm;
+          const unsigned long long key = pack_key(sc, gid);
+          unsigned long long& b = bk[s * kSweepThreads + tid];
+          b = key > b ? key : b;
+        }
+      }
+    }
+    __stcs(a.acc + row, acc);
+  }
+  __syncthreads();
+  for (int s = warp; s < ns; s += kSweepWarps) {
+    unsigned long long b = 0ull;
+#pragma unroll
+    for (int j = 0; j < kSweepThreads / 32; ++j) {
+      const unsigned long long v = bk[s * kSweepThreads + j * 32 + lane];
+      b = v > b ? v : b;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const unsigned long long x2 = shfl_u64(b, lane ^ o);
+      b = x2 > b ? x2 : b;
+    }
+    if (lane == 0 && b) atomicMax(a.best + s, b);
+  }
+}
+
+// Outputs of a row-major sweep: one warp per step (after the sweep grid
+// completed): top-1 from the packed best key, the Eq. 4-6 selection of target
+// layer layer0 + s + sel_d (warp_select, as the step kernel), best reset; the
+// running query norm goes to qn_out.  A poisoned session reports (NaN, -1).
+template <class Tag>
+__global__ void __launch_bounds__(kSweepThreads) traj_sweep_finalize_kernel(const SweepArgs a) {
+  __shared__ __align__(16) float qs[kSweepMaxSteps][8];
+  __shared__ float rqs[kSweepMaxSteps];
+  __shared__ int valids[kSweepMaxSteps];
+  __shared__ double parts[kSweepMaxSteps];
+  __shared__ float sel_p[kSweepWarps][kMaxE];
+  __shared__ int sel_i[kSweepWarps][kMaxE];
+  const StoreView& st = a.st;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  pdl_wait();
+  const bool poisoned = a.abort && ld_acquire_u32(a.abort) != 0u;
+  const double qn = sweep_stage_all<Tag>(a, qs, rqs, valids, parts);
+  for (int f = int(blockIdx.x) * kSweepWarps + warp; f < a.n_steps; f += int(gridDim.x) * kSweepWarps) {
+    const uint64_t key = __ldcg(a.best + f);
+    const bool valid = valids[f] != 0 && !poisoned;
+    const int64_t id = valid ? key_id(key) : -1;
+    const float score = valid ? key_score(key) : __int_as_float(0x7fc00000);
+    if (lane == 0) {
+      a.out_score[f] = score;
+      a.out_id[f] = id;
+    }
+    const int tgt = a.layer0 + f + a.sel_d;
+    if (a.sel_mask) {
+      const int64_t loc = id - int64_t(a.id_offset);
+      if (tgt >= st.L || id < 0 || loc < 0 || loc >= a.n_rows) {
+        if (lane == 0) { a.sel_mask[f] = 0ull; a.sel_count[f] = 0; }
+      } else {
+        uint64_t mask;
+        int m;
+        warp_select<Tag>(st, tgt, loc, selection_delta(a.sel_delta, score), a.sel_K, sel_p[warp], sel_i[warp],
+                         &mask, &m);
+        if (lane == 0) { a.sel_mask[f] = mask; a.sel_count[f] = m; }
+      }
+    }
+    __syncwarp();
+    if (lane == 0) a.best[f] = 0ull;
+  }
+  if (blockIdx.x == 0 && tid == 0 && !poisoned) a.qn_out[0] = qn;
+  pdl_trigger();
+}
+
 int traj_sweep_rows(int64_t n_rows, int* grid_out) {
   static int sms = 0;
   if (!sms) {
@@ -734,10 +917,47 @@ cudaError_t launch_traj_sweep(const SweepArgs& a, cudaStream_t stream) {
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   }
-  const char* env = getenv("FMOE_SWEEP_TMA");
-  // opt-in: measured slower than the register kernel at C2 (0.262 vs 0.217 ms per
-  // sweep, profiles/r01f_c2_sweep.md); kept as an experiment knob
-  const bool tma_ok = env != nullptr && atoi(env) != 0;
+  // Kernel choice (FMOE_SWEEP_KERNEL, read per call: a measurement/test knob):
+  //  "row" (default) -- row-major sweep when no ready flags are given;
+  //  "reg" -- the step-major register kernel; "tma" -- the step-major
+  //  shared-memory staged kernel (measured slower at C2: 0.262 vs 0.217 ms,
+  //  profiles/r01f_c2_sweep.md).  Ready flags always take a step-major kernel.
+  const char* env = getenv("FMOE_SWEEP_KERNEL");
+  const bool want_tma = env != nullptr && strcmp(env, "tma") == 0;
+  const bool want_reg = env != nullptr && strcmp(env, "reg") == 0;
+  int unused_grid = 0;
+  const bool flagless = !a.layer_ready && !a.guidance_ready;
+  if (flagless && ((!want_tma && !want_reg) || traj_sweep_rows(a.n_rows, &unused_grid) == 0)) {
+    using Fn = void (*)(const SweepArgs);
+    Fn fn = a.st.bf16 ? traj_sweep_rowmajor_kernel<Bf16Tag> : traj_sweep_rowmajor_kernel<F32Tag>;
+    const int smem = a.n_steps * kSweepThreads * 8;
+    // the attribute allows the largest sweep (64 steps), set once per kernel;
+    // resident blocks per SM cached by (dtype, n_steps)
+    static int occ[2][kSweepMaxSteps + 1];
+    static bool attr_set[2];
+    const int di = a.st.bf16 ? 1 : 0;
+    int& per_sm = occ[di][a.n_steps];
+    if (per_sm == 0) {
+      cudaError_t e = cudaSuccess;
+      if (!attr_set[di]) {
+        e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, kSweepMaxSteps * kSweepThreads * 8);
+        if (e == cudaSuccess) attr_set[di] = true;
+      }
+      if (e == cudaSuccess) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kSweepThreads, size_t(smem));
+      if (e != cudaSuccess) return e;
+      if (per_sm < 1) return cudaErrorInvalidConfiguration;
+    }
+    int64_t grid = int64_t(per_sm) * sms;
+    const int64_t need = (a.n_rows + kSweepThreads - 1) / kSweepThreads;
+    if (need < grid) grid = need < 1 ? 1 : need;
+    count_launch(2);
+    cudaError_t e = launch_pdl(fn, dim3(unsigned(grid)), dim3(kSweepThreads), size_t(smem), stream, a);
+    if (e != cudaSuccess) return e;
+    Fn fin = a.st.bf16 ? traj_sweep_finalize_kernel<Bf16Tag> : traj_sweep_finalize_kernel<F32Tag>;
+    return launch_pdl(fin, dim3(unsigned((a.n_steps + kSweepWarps - 1) / kSweepWarps)), dim3(kSweepThreads), 0,
+                      stream, a);
+  }
+  const bool tma_ok = want_tma;
   const int64_t per_block = int64_t(kSweepTmaR) * kSweepTmaThreads;
   const int64_t tgrid = (a.n_rows + per_block - 1) / per_block;
   if (tma_ok && tgrid <= int64_t(2) * sms) {

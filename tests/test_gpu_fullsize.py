@@ -152,10 +152,13 @@ def test_c3_insert_batch_of_64_at_capacity(c3):
     assert slot.cpu().tolist() == victims and rep.cpu().tolist() == victims
 
 
-def test_c2_session_sweep_full_size(c2):
-    """The bench's launch configuration (N = 1M: 592 CTAs, 7 rows per thread in
+@pytest.mark.parametrize("kern", ["row", "reg"])
+def test_c2_session_sweep_full_size(c2, kern, monkeypatch):
+    """The bench's launch configuration (N = 1M; row-major: every thread walks
+    ~2-3 rows through all steps; step-major: 592 CTAs, 7 rows per thread in
     registers): sweep == per-step calls bit for bit; returned scores equal the
     oracle's for the returned ids; planted queries find their row."""
+    monkeypatch.setenv("FMOE_SWEEP_KERNEL", kern)
     lib, st, sh, N = c2
     qe, qm, planted = S.queries(sh, SEED + 1, N, 2, device="cuda")
     L, d = sh.L, 3

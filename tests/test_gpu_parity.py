@@ -354,13 +354,15 @@ def test_topk_merge_api(lib):
     assert (out_i.cpu().numpy()[~valid] == -1).all()
 
 
-# ---------------------------------------------------------------- batched (tcgen05 path, B >= 5, bf16)
-# 130, 256: one pass on CTA pairs (cta_group::2, M = 256); 300: a 256-query pass + a ragged 44-query pass
-@pytest.mark.parametrize("B,k", [(16, 1), (64, 8), (130, 64), (256, 8), (300, 3)])
+# ---------------------------------------------------------------- batched (B >= 5)
+# bf16: tcgen05 path; 130, 256: one pass on CTA pairs (cta_group::2, M = 256);
+# 300: a 256-query pass + a ragged 44-query pass.
+# fp32: the FFMA batched scan (scan_f32mm.cu), passes of <= 64 queries:
+# 16 (2 query groups), 64 (8 groups, blend on 128-row tiles), 130 / 300 (a
+# ragged last pass with the first pass's list layout), k up to 64.
+@pytest.mark.parametrize("B,k", [(5, 4), (16, 1), (64, 8), (130, 64), (256, 8), (300, 3)])
 @pytest.mark.parametrize("mode", ["sem", "traj3", "trajL", "blend"])
 def test_batched_tcgen05(setup, B, k, mode):
-    if setup["dtype"] != "bf16":
-        pytest.skip("tensor-core path is bf16")
     st, dt, sh = setup["st"], setup["dtype"], setup["shape"]
     q_emb, q_maps, _ = S.queries(sh, 1, setup["N"], B)
     if mode == "sem":
@@ -636,14 +638,15 @@ def _steps_reference(st, qm, delta, d, ell0=0, n=None):
         ref.close()
 
 
-@pytest.mark.parametrize("tma", ["0", "1"])
+@pytest.mark.parametrize("kern", ["row", "reg", "tma"])
 @pytest.mark.parametrize("B,delta", [(1, -1.0), (1, 0.9), (3, -1.0)])
-def test_session_sweep_equals_steps(setup, B, delta, tma, monkeypatch):
+def test_session_sweep_equals_steps(setup, B, delta, kern, monkeypatch):
     """fmoe_traj_session_sweep = n calls of step_select, bit for bit (fused kernel
     for B = 1 on 16-byte slab rows -- mixtral_tiny bf16 -- else the per-step
     path), including a sweep split in three and continued by plain steps; ids
     follow the Eq. 2 oracle at every prefix."""
-    monkeypatch.setenv("FMOE_SWEEP_TMA", tma)            # register kernel / shared-memory staged kernel
+    # row-major kernel / step-major register kernel / step-major shared-memory staged kernel
+    monkeypatch.setenv("FMOE_SWEEP_KERNEL", kern)
     st, dt, sh = setup["st"], setup["dtype"], setup["shape"]
     qm = S.queries(sh, 5, setup["N"], B)[1]
     d, L = 3, sh.L
@@ -704,11 +707,11 @@ def test_session_sweep_ready_flags(setup):
         a.close()
 
 
-@pytest.mark.parametrize("tma", ["0", "1"])
-def test_session_sweep_edge_cases(lib, tma, monkeypatch):
+@pytest.mark.parametrize("kern", ["row", "reg", "tma"])
+def test_session_sweep_edge_cases(lib, kern, monkeypatch):
     """Zero query layers (prefix norm 0 -> (NaN, -1), empty selection, as the
     step kernel), single-step sweeps, an empty store (per-step path: id -1)."""
-    monkeypatch.setenv("FMOE_SWEEP_TMA", tma)
+    monkeypatch.setenv("FMOE_SWEEP_KERNEL", kern)
     sh = SHAPES["mixtral_tiny"]
     st, _, _ = make(lib, sh, 777, "bf16")
     empty = lib.ExpertMapStore(sh.L, sh.E, sh.K, sh.D, 3, 16, "bf16")

@@ -30,9 +30,11 @@ def main():
     p.add_argument("--reps", type=int, default=5)
     p.add_argument("--once", action="store_true")
     p.add_argument("--only", default="")
+    p.add_argument("--dtype", default="bf16", help="store dtype: bf16 (tcgen05 path) or f32 (FFMA batched scan)")
     a = p.parse_args()
     sh = S.Shape("m", a.L, a.E, 2, a.D, 1024)
-    st = fm.ExpertMapStore(sh.L, sh.E, sh.K, sh.D, 3, a.n, "bf16")
+    st = fm.ExpertMapStore(sh.L, sh.E, sh.K, sh.D, 3, a.n, a.dtype)
+    es = 2 if a.dtype == "bf16" else 4
     for s0 in range(0, a.n, 65536):
         c = min(65536, a.n - s0)
         e, m, _ = S.store_rows(sh, 1, s0, c, device="cuda")
@@ -65,7 +67,7 @@ def main():
             ev1.record()
             torch.cuda.synchronize()
             us = ev0.elapsed_time(ev1) * 1e3 / a.reps
-            print(f"traj ell={ell:2d} B={a.B}: {us:8.1f} us  {a.n * ell * a.E * 2 / us / 1e3:7.1f} GB/s", flush=True)
+            print(f"traj ell={ell:2d} B={a.B}: {us:8.1f} us  {a.n * ell * a.E * es / us / 1e3:7.1f} GB/s", flush=True)
         st.close()
         return
     for name, (fn, kdim) in calls.items():
@@ -84,7 +86,7 @@ def main():
         ev1.record()
         torch.cuda.synchronize()
         us = ev0.elapsed_time(ev1) * 1e3 / a.reps
-        gb = (a.n * kdim * 2 + (a.n * a.B * 4 if name.endswith("_cos") else 0)) / us / 1e3
+        gb = (a.n * kdim * es + (a.n * a.B * 4 if name.endswith("_cos") else 0)) / us / 1e3
         tf = 2.0 * a.B * a.n * kdim / us / 1e6
         print(f"{name:10s} B={a.B} n={a.n}: {us:9.1f} us  {gb:7.1f} GB/s  {tf:7.1f} TFLOP/s", flush=True)
     st.close()
