@@ -49,11 +49,6 @@ __device__ __forceinline__ void cp_async16(uint32_t dst, const void* src, bool v
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
-__device__ __forceinline__ float4 lds128(uint32_t a) {
-  float4 v;
-  asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(a));
-  return v;
-}
 
 // Insert key into the warp's sorted (desc) list lb[0..cnt) of capacity k (all
 // lanes, warp-uniform key > current k-th).  Entries j and j + 32 live in lane j.
@@ -80,20 +75,22 @@ __device__ __forceinline__ void list_insert(uint64_t* lb, int k, int& cnt, uint6
   cnt = nc;
 }
 
+// (plain C++ shared loads, not asm: the compiler may hoist the next query
+// fragment above the current FFMAs; the barrier intrinsics still order them)
 template <int TR>
-__device__ __forceinline__ void mm_chunk(uint32_t rows, uint32_t qs, int wq, int lane, int wr,
+__device__ __forceinline__ void mm_chunk(const unsigned char* rows, const unsigned char* qs, int wq, int lane, int wr,
                                          float (&acc)[8][TR]) {
-  const uint32_t rb = rows + uint32_t(wr * 32 * TR + lane) * 128u;
-  const uint32_t qb = qs + uint32_t(wq * 8) * 128u;
+  const unsigned char* rb = rows + (wr * 32 * TR + lane) * 128;
+  const unsigned char* qb = qs + wq * 8 * 128;
 #pragma unroll 2
   for (int kk = 0; kk < 8; ++kk) {
-    const uint32_t sw = uint32_t((kk ^ (lane & 7)) * 16);
+    const int sw = (kk ^ (lane & 7)) * 16;
     float4 x[TR];
 #pragma unroll
-    for (int j = 0; j < TR; ++j) x[j] = lds128(rb + uint32_t(j * 32 * 128) + sw);
+    for (int j = 0; j < TR; ++j) x[j] = *reinterpret_cast<const float4*>(rb + j * 32 * 128 + sw);
 #pragma unroll
     for (int i = 0; i < 8; ++i) {
-      const float4 q = lds128(qb + uint32_t(i * 128 + ((kk ^ i) * 16)));
+      const float4 q = *reinterpret_cast<const float4*>(qb + i * 128 + ((kk ^ i) * 16));
 #pragma unroll
       for (int j = 0; j < TR; ++j) {
         acc[i][j] = fmaf(x[j].x, q.x, acc[i][j]);
@@ -182,10 +179,10 @@ __global__ void __launch_bounds__(kMmThreads, 1) scan_f32mm_kernel(const F32mmAr
     cp_async_wait<kMmStages - 2>();
     __syncthreads();                      // chunk it landed for everyone; stage (it-1) % S is free
     issue(it + kMmStages - 1);
-    const uint32_t sb = ring + uint32_t((it % kMmStages) * stage_bytes);
+    const unsigned char* sb = smem + (it % kMmStages) * stage_bytes;
     const int c = it % nch;
-    if (SEM && (!TRAJ || c < a.n_sem_ch)) mm_chunk<TR>(sb, sb + uint32_t(RT * 128), wq, lane, wr, accs);
-    else mm_chunk<TR>(sb, sb + uint32_t(RT * 128), wq, lane, wr, acct);
+    if (SEM && (!TRAJ || c < a.n_sem_ch)) mm_chunk<TR>(sb, sb + RT * 128, wq, lane, wr, accs);
+    else mm_chunk<TR>(sb, sb + RT * 128, wq, lane, wr, acct);
     if (c != nch - 1) continue;
 
     // ---- epilogue of tile t

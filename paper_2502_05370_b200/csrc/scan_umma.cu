@@ -185,6 +185,11 @@ __device__ __forceinline__ void tma_store_2d(const CUtensorMap* map, const void*
                "r"(smem_u32(src)), "r"(c0), "r"(c1)
                : "memory");
 }
+// shared -> global 1-D bulk copy (bulk group)
+__device__ __forceinline__ void bulk_s2g(void* dst, const void* src, unsigned bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst), "r"(smem_u32(src)), "r"(bytes)
+               : "memory");
+}
 __device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
 __device__ __forceinline__ void bulk_wait_read0() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
 __device__ __forceinline__ void bulk_wait_all0() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
@@ -256,6 +261,9 @@ struct UmmaParams {
   int64_t cos_stride;
   unsigned long long* gthr;     // [nq] shared admission threshold per query (zeroed by prep)
   const uint32_t* excl;         // nullable bitmap over rows: no candidates (insert sub-batches)
+  int cos_ring;                 // cached-cosine ring depth (trajectory scans with cos_tma)
+  int cos_tiled_exp;            // experiment knob FMOE_COS_TILED_EXP: cosine boxes as contiguous 4 KB blocks
+  size_t cos_bytes;
   int cos_tma;                  // semantic scans: out_cos written through a swizzled smem stage + TMA
                                 // tensor stores; trajectory scans: sem_cos read by per-warp TMA loads
                                 // (a 3-buffer ring, 2 chunks ahead) instead of lane-per-query loads
@@ -266,8 +274,13 @@ struct UmmaParams {
                                 // the L2 traffic of re-reading it per tile)
 };
 constexpr int kCosStage = 32 * 128;             // per epilogue warp: 32 queries x 32 columns fp32 (SW128)
-constexpr int kCosRing = 3;                     // cached-cosine loads: buffers per epilogue warp (2 chunks ahead)
-__host__ __device__ constexpr int cos_stage_bytes(bool sem) { return kUmEpiWarps * kCosStage * (sem ? 1 : kCosRing); }
+constexpr int kCosRingMax = 6;                  // cached-cosine loads: buffers per epilogue warp (ring - 1 chunks ahead)
+// ring depth of the cached-cosine loads (FMOE_COS_RING, 2..6; measurement knob)
+static int cos_ring() {
+  static const int r = getenv("FMOE_COS_RING") ? atoi(getenv("FMOE_COS_RING")) : 3;
+  return r < 2 ? 2 : (r > kCosRingMax ? kCosRingMax : r);
+}
+static int cos_stage_bytes(bool sem) { return kUmEpiWarps * kCosStage * (sem ? 1 : cos_ring()); }
 
 // Sorted insert into a per-thread list in shared memory (entry i at
 // l[i*stride]); called rarely (only for keys beating the k-th), kept out of
@@ -347,7 +360,7 @@ __global__ void __launch_bounds__(kUmThreads, 1)
                      const __grid_constant__ CUtensorMap tm_cos, const UmmaParams p) {
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   __shared__ __align__(8) uint64_t full[kUmMaxStages], empty[kUmMaxStages], tfull[2], tempty[2];
-  __shared__ __align__(8) uint64_t cbar_all[kUmEpiWarps * kCosRing];   // cached-cosine ring (TRAJ + sem_cos)
+  __shared__ __align__(8) uint64_t cbar_all[kUmEpiWarps * kCosRingMax];   // cached-cosine ring (TRAJ + sem_cos)
   if (p.gate) {                                  // a conditional (fallback) scan
     pdl_wait();
     if (*p.gate == 0) {                          // (both CTAs of a pair read the same flag)
@@ -365,7 +378,7 @@ __global__ void __launch_bounds__(kUmThreads, 1)
   constexpr int SBY = um_stage_bytes(CG, TN);
   // [8 warps][kCosStage] cosine staging (cos_tma), then the lists [2R][k][LQ]
   unsigned char* cstage_all = smem + size_t(p.stages) * SBY;
-  uint64_t* lists = reinterpret_cast<uint64_t*>(cstage_all + (p.cos_tma ? cos_stage_bytes(SEM) : 0));
+  uint64_t* lists = reinterpret_cast<uint64_t*>(cstage_all + (p.cos_tma ? kUmEpiWarps * kCosStage * (SEM ? 1 : p.cos_ring) : 0));
   // CTA pair (cta_group::2): rank r owns query rows r*128.. of the M = 256
   // operand and store rows r*128.. of each 256-row tile; the leader (rank 0)
   // issues the MMAs for both, the accumulators of its queries land in each
@@ -387,7 +400,7 @@ __global__ void __launch_bounds__(kUmThreads, 1)
     for (int s = 0; s < S; ++s) { mbar_init(&full[s], (CG == 2 && leader) ? 2 : 1); mbar_init(&empty[s], 1); }
     for (int a = 0; a < AS; ++a) { mbar_init(&tfull[a], 1); mbar_init(&tempty[a], CG * kUmEpiWarps); }
     if (!SEM && p.cos_tma)
-      for (int i = 0; i < kUmEpiWarps * kCosRing; ++i) mbar_init(&cbar_all[i], 1);
+      for (int i = 0; i < kUmEpiWarps * p.cos_ring; ++i) mbar_init(&cbar_all[i], 1);
     mbar_fence_init();
   }
   if (warp == 0 && lane == 0) {
@@ -426,7 +439,12 @@ __global__ void __launch_bounds__(kUmThreads, 1)
       auto prefetch = [&](int t, int kb) {
         const int y0 = t * TN + rank * NB;
         if (SEM && kb < p.n_sem_kb) {
-          tma_prefetch_l2(&tm_es, kb * 64, y0);
+          if constexpr (TN == 512) {                    // the two 128-row boxes this CTA loads
+            tma_prefetch_l2(&tm_es, kb * 64, t * TN + rank * UM_M);
+            tma_prefetch_l2(&tm_es, kb * 64, t * TN + 256 + rank * UM_M);
+          } else {
+            tma_prefetch_l2(&tm_es, kb * 64, y0);
+          }
           return;
         }
         const int l0 = (kb - p.n_sem_kb) * p.lc;
@@ -465,17 +483,21 @@ __global__ void __launch_bounds__(kUmThreads, 1)
             const bool load_a = !p.no_a_reload || u < unsigned(S);
             mbar_arrive_expect_tx(&full[s], unsigned(load_a ? SBY : SBY - kStageA));
             if (load_a) bulk_g2s_plain(sa, p.qs + (size_t(rank) * p.n_sem_kb + kb) * kStageA, kStageA, &full[s]);
-            if constexpr (TN == 512) {
+            if (p.tiled_b_exp) {
+              // experiment: the same bytes as contiguous 16 KB blocks (results garbage);
+              // 1: [row block][kb] order, 2: [kb][row block] order (a K-slab-major layout)
+              const unsigned char* eb = static_cast<const unsigned char*>(p.emb_raw);
+              const size_t nblk = size_t(p.cap / 128);
+              for (int h = 0; h < NB / 128; ++h) {
+                const size_t blk = TN == 512 ? size_t(t) * 4 + size_t(h) * 2 + rank : size_t(y0 / 128 + h);
+                const size_t off = p.tiled_b_exp == 2 ? (size_t(kb) * nblk + blk) : (blk * p.n_sem_kb + kb);
+                bulk_g2s(sb + h * 16384, eb + (off * 16384) % p.emb_bytes, 16384u, &full[s], pol);
+              }
+            } else if constexpr (TN == 512) {
               // two 128-row boxes: the halves this CTA feeds to the two N = 256 MMAs
               // (rows t*512 + g*256 + rank*128: TMEM column g*256 + j is row t*512 + g*256 + j)
               tma_load_2d(sb, &tm_es, kb * 64, t * TN + rank * UM_M, &full[s]);
               tma_load_2d(sb + UM_M * 128, &tm_es, kb * 64, t * TN + 256 + rank * UM_M, &full[s]);
-            } else if (p.tiled_b_exp) {
-              // experiment: the same bytes as contiguous 16 KB blocks (results garbage)
-              const unsigned char* eb = static_cast<const unsigned char*>(p.emb_raw);
-              for (int h = 0; h < NB / 128; ++h)
-                bulk_g2s(sb + h * 16384, eb + ((size_t(y0 / 128 + h) * p.n_sem_kb + kb) * 16384) % p.emb_bytes,
-                         16384u, &full[s], pol);
             } else
             tma_load_2d(sb, &tm_es, kb * 64, y0, &full[s]);
           } else {
@@ -649,21 +671,26 @@ __global__ void __launch_bounds__(kUmThreads, 1)
     // cached cosines (TRAJ + sem_cos, cos_tma): chunk i of this warp's sequence
     // (tile cid + (i / NC) * ncl, chunk i % NC) lands in ring buffer i % 3
     const bool cin = !SEM && p.sem_cos && p.cos_tma;
-    uint64_t* cbar = cbar_all + e * kCosRing;
-    unsigned char* cring = cstage_all + size_t(e) * kCosRing * kCosStage;
+    const int CR = p.cos_ring;
+    uint64_t* cbar = cbar_all + e * CR;
+    unsigned char* cring = cstage_all + size_t(e) * CR * kCosStage;
     const int crow = rank * UM_M + (qd % QA) * 32;      // first query row of this warp's box
     auto cos_issue = [&](unsigned i) {                  // lane 0
       const int t2 = cid + int(i / unsigned(NC)) * ncl;
       if (t2 >= p.n_tiles) return;
       const int col = t2 * TN + half * HC + sub * NC * 32 + int(i % unsigned(NC)) * 32;
-      uint64_t* b = &cbar[i % kCosRing];
+      uint64_t* b = &cbar[i % unsigned(CR)];
       mbar_arrive_expect_tx(b, unsigned(kCosStage));
-      tma_load_2d(cring + (i % kCosRing) * kCosStage, &tm_cos, col, crow, b);
+      if (p.cos_tiled_exp) {   // experiment: the same bytes as contiguous 4 KB blocks (results garbage)
+        const size_t blk = (size_t(col) / 32) * size_t((p.nq + 31) / 32) + size_t(crow) / 32;
+        bulk_g2s_plain(cring + (i % unsigned(CR)) * kCosStage,
+                       reinterpret_cast<const unsigned char*>(p.sem_cos) + (blk * kCosStage) % p.cos_bytes,
+                       unsigned(kCosStage), b);
+      } else
+      tma_load_2d(cring + (i % unsigned(CR)) * kCosStage, &tm_cos, col, crow, b);
     };
-    if (cin && lane == 0) {
-      cos_issue(0);
-      cos_issue(1);
-    }
+    if (cin && lane == 0)
+      for (int i = 0; i < CR - 1; ++i) cos_issue(unsigned(i));
     unsigned ci = 0;                                    // this warp's chunk sequence number
     uint64_t st0 = 0ull, st1 = 0ull, st2 = 0ull, st3 = 0ull;   // candidate stash (see the rare path)
     int ns = 0;
@@ -743,14 +770,14 @@ __global__ void __launch_bounds__(kUmThreads, 1)
         const unsigned vmask = !live ? 0u : (left >= 32 ? 0xffffffffu : (left <= 0 ? 0u : ((1u << left) - 1u)));
         float cached[32];
         if (cin) {
-          // buffer (ci + 2) % 3 held chunk ci - 1, which every lane has read
+          // buffer (ci + CR - 1) % CR held chunk ci - 1, which every lane has read
           __syncwarp();
           if (lane == 0) {
             fence_proxy_async_smem();
-            cos_issue(ci + 2);
+            cos_issue(ci + unsigned(CR) - 1);
           }
-          mbar_wait(&cbar[ci % kCosRing], (ci / kCosRing) & 1u);
-          const uint32_t row = smem_u32(cring + (ci % kCosRing) * kCosStage) + uint32_t(lane) * 128u;
+          mbar_wait(&cbar[ci % unsigned(CR)], (ci / unsigned(CR)) & 1u);
+          const uint32_t row = smem_u32(cring + (ci % unsigned(CR)) * kCosStage) + uint32_t(lane) * 128u;
 #pragma unroll
           for (int j4 = 0; j4 < 8; ++j4) {
             float4 f;
@@ -827,6 +854,11 @@ __global__ void __launch_bounds__(kUmThreads, 1)
             fence_proxy_async_smem();
             __syncwarp();
             if (lane == 0) {
+              if (p.cos_tiled_exp) {   // experiment: contiguous 4 KB blocks (results garbage)
+                const size_t blk = size_t(yc / 32) * size_t((p.nq + 31) / 32) + size_t(rank * UM_M + (qd % QA) * 32) / 32;
+                bulk_s2g(reinterpret_cast<unsigned char*>(p.out_cos) + (blk * kCosStage) % p.cos_bytes, cst,
+                         unsigned(kCosStage));
+              } else
               tma_store_2d(&tm_cos, cst, int(yc), rank * UM_M + (qd % QA) * 32);
               bulk_commit();
             }
@@ -876,16 +908,19 @@ __global__ void __launch_bounds__(kUmThreads, 1)
         }
         EPI_T(4);
       }
-      flush();
       // hand the accumulator stage back first: the arrive is a release, and
       // placed after the threshold's global red it would wait for that red's
-      // round trip (the MMA warp, not this warp, is what waits on it)
+      // round trip (the MMA warp, not this warp, is what waits on it).  The
+      // stashed candidates are admitted after it: the heap inserts touch only
+      // this thread's list, and with a single-buffered accumulator (TN = 512)
+      // the next tile's MMAs wait for the arrive.
       tc_fence_before();
       __syncwarp();
       if (lane == 0) {                            // the leader's MMA waits for both CTAs' epilogues
         if (CG == 2 && !leader) mbar_arrive_remote(mapa_rank(&tempty[as], 0));
         else mbar_arrive(&tempty[as]);
       }
+      flush();
       // publish this list's bound once per tile (atomics per insert contended
       // at k = 64), then take the shared one read at the start of this tile
       if (g > published) {
@@ -1282,7 +1317,10 @@ cudaError_t launch_umma(const UmmaLaunch& L, cudaStream_t s) {
   p.acc_stages = (nacc2 && TN == UM_N) || TN == 512 ? 1 : 2;
   {
     static const int pf_env = getenv("FMOE_L2PF") ? atoi(getenv("FMOE_L2PF")) : -1;
-    p.l2pf = pf_env >= 0 ? pf_env : 0;   // measured: no gain at either CTA mode (kept as a knob)
+    // L2 prefetch of the store operand: measured +2..5 % for the 512-row semantic
+    // tiles at 2 k-blocks ahead (3 smem stages; deeper hurts: 8 -> -6 %,
+    // profiles/r02d_semantic_experiments.md), no gain elsewhere
+    p.l2pf = pf_env >= 0 ? pf_env : (TN == 512 ? 2 : 0);
     static const int es_env = getenv("FMOE_EPI_SLEEP") ? atoi(getenv("FMOE_EPI_SLEEP")) : -1;
     p.epi_sleep = es_env >= 0 ? es_env : 0;
     static const int fk_env = getenv("FMOE_FAKE_LOADS") ? atoi(getenv("FMOE_FAKE_LOADS")) : 0;
@@ -1293,6 +1331,12 @@ cudaError_t launch_umma(const UmmaLaunch& L, cudaStream_t s) {
     p.no_epi = ne_env;
   }
   p.cos_tma = cos_tma ? 1 : 0;
+  p.cos_ring = cos_ring();
+  {
+    static const int ct_env = getenv("FMOE_COS_TILED_EXP") ? atoi(getenv("FMOE_COS_TILED_EXP")) : 0;
+    p.cos_tiled_exp = cos_tma ? ct_env : 0;
+    p.cos_bytes = size_t(in.nq) * size_t(L.cos_stride) * 4 / kCosStage * kCosStage;
+  }
   p.cap = in.cap;
   p.L = in.L;
   p.maps = static_cast<const unsigned char*>(in.maps);
