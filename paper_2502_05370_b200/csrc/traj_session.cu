@@ -719,7 +719,7 @@ __global__ void __launch_bounds__(kSweepTmaThreads, 2) traj_sweep_tma_kernel(con
 // the steps need no order between them except through each row's running dot,
 // which is private to the row.  So the sweep walks ROWS in the outer loop and
 // the steps in the inner loop: a thread takes a row, streams its n_steps slab
-// entries (16 B) and prefix-norm entries (4 B) in chunks of kRowChunk loads,
+// entries (16 B) and prefix-norm entries (4 B) in chunks of CH (8 or 16) loads,
 // carries acc in one register from step to step, and folds each step's key
 // into its own per-step best in shared memory.  Nothing synchronises between
 // steps, so the loads of the next chunk / row are never held back by a step
@@ -730,7 +730,7 @@ __global__ void __launch_bounds__(kSweepTmaThreads, 2) traj_sweep_tma_kernel(con
 // is the step kernel's (same fmaf order, acc + d, acc * r_q * rsqrt(psq)) and
 // the max of packed keys is order-free, so outputs are bit-identical to the
 // step-major kernel.  Any number of rows (no register-residency limit).
-constexpr int kRowChunk = 8;
+
 
 // Query layers of steps [0, ns) (store-dtype values, qs[s][0..8)) and their
 // running norms, all steps at once (warp w: steps w, w+8, ...), in the step
@@ -767,8 +767,8 @@ __device__ __forceinline__ double sweep_stage_all(const SweepArgs& a, float (*qs
   return qn;
 }
 
-template <class Tag>
-__global__ void __launch_bounds__(kSweepThreads, 3) traj_sweep_rowmajor_kernel(const SweepArgs a) {
+template <class Tag, int CH>
+__global__ void __launch_bounds__(kSweepThreads, CH > 8 ? 2 : 3) traj_sweep_rowmajor_kernel(const SweepArgs a) {
   using ST = StoreT<Tag>;
   constexpr int EP = ST::kElemsPer16B;
   extern __shared__ __align__(16) unsigned long long bk[];   // [n_steps][kSweepThreads] per-thread best keys
@@ -788,16 +788,16 @@ __global__ void __launch_bounds__(kSweepThreads, 3) traj_sweep_rowmajor_kernel(c
   if (a.abort && ld_acquire_u32(a.abort) != 0u) return;   // poisoned: the finalize kernel reports it
   // the first chunk of this thread's first row is in flight while the queries are staged
   const int64_t row0 = int64_t(blockIdx.x) * kSweepThreads + tid;
-  uint4 buf[kRowChunk];
-  float ps[kRowChunk];
+  uint4 buf[CH];
+  float ps[CH];
   auto issue = [&](int64_t row, int s0) {
 #pragma unroll
-    for (int j = 0; j < kRowChunk; ++j) {
+    for (int j = 0; j < CH; ++j) {
       const int64_t layer = a.layer0 + s0 + j;
       buf[j] = (row < n && s0 + j < ns) ? ld_stream(maps + (layer * st.cap + row) * 16) : make_uint4(0u, 0u, 0u, 0u);
     }
 #pragma unroll
-    for (int j = 0; j < kRowChunk; ++j) {
+    for (int j = 0; j < CH; ++j) {
       const int64_t layer = a.layer0 + s0 + j;
       ps[j] = (row < n && s0 + j < ns) ? __ldcs(st.psq + layer * st.cap + row) : 0.f;
     }
@@ -809,10 +809,10 @@ __global__ void __launch_bounds__(kSweepThreads, 3) traj_sweep_rowmajor_kernel(c
   for (int64_t row = row0; row < n; row += nthr) {
     float acc = a.layer0 > 0 ? __ldcs(a.acc + row) : 0.f;
     const uint32_t gid = a.id_offset + uint32_t(row);
-    for (int s0 = 0; s0 < ns; s0 += kRowChunk) {
+    for (int s0 = 0; s0 < ns; s0 += CH) {
       if (row != row0 || s0 != 0) issue(row, s0);
 #pragma unroll
-      for (int j = 0; j < kRowChunk; ++j) {
+      for (int j = 0; j < CH; ++j) {
         const int s = s0 + j;
         if (s < ns) {
           float x[8];
@@ -929,13 +929,17 @@ cudaError_t launch_traj_sweep(const SweepArgs& a, cudaStream_t stream) {
   const bool flagless = !a.layer_ready && !a.guidance_ready;
   if (flagless && ((!want_tma && !want_reg) || traj_sweep_rows(a.n_rows, &unused_grid) == 0)) {
     using Fn = void (*)(const SweepArgs);
-    Fn fn = a.st.bf16 ? traj_sweep_rowmajor_kernel<Bf16Tag> : traj_sweep_rowmajor_kernel<F32Tag>;
+    // loads in flight per thread (FMOE_SWEEP_CHUNK = 8 or 16; measurement knob)
+    const char* ce = getenv("FMOE_SWEEP_CHUNK");
+    const int ch = ce && atoi(ce) == 8 ? 8 : 16;
+    Fn fn = a.st.bf16 ? (ch == 8 ? traj_sweep_rowmajor_kernel<Bf16Tag, 8> : traj_sweep_rowmajor_kernel<Bf16Tag, 16>)
+                      : (ch == 8 ? traj_sweep_rowmajor_kernel<F32Tag, 8> : traj_sweep_rowmajor_kernel<F32Tag, 16>);
     const int smem = a.n_steps * kSweepThreads * 8;
     // the attribute allows the largest sweep (64 steps), set once per kernel;
     // resident blocks per SM cached by (dtype, n_steps)
-    static int occ[2][kSweepMaxSteps + 1];
-    static bool attr_set[2];
-    const int di = a.st.bf16 ? 1 : 0;
+    static int occ[4][kSweepMaxSteps + 1];
+    static bool attr_set[4];
+    const int di = (a.st.bf16 ? 1 : 0) + (ch == 8 ? 0 : 2);
     int& per_sm = occ[di][a.n_steps];
     if (per_sm == 0) {
       cudaError_t e = cudaSuccess;
