@@ -196,6 +196,7 @@ struct UmmaLaunch {
   const uint32_t* excl;        // nullable bitmap over rows: set bits are no candidates (insert sub-batches)
 };
 bool umma_supported(const UmmaPlanIn& in);
+bool umma_cos_bound();
 int umma_rep(const UmmaPlanIn& in);
 size_t umma_scratch_bytes(const UmmaPlanIn& in);
 int umma_grid(const UmmaPlanIn& in);   // CTAs to launch (a multiple of umma_cg)

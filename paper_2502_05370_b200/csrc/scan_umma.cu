@@ -262,6 +262,8 @@ struct UmmaParams {
   unsigned long long* gthr;     // [nq] shared admission threshold per query (zeroed by prep)
   const uint32_t* excl;         // nullable bitmap over rows: no candidates (insert sub-batches)
   int cos_ring;                 // cached-cosine ring depth (trajectory scans with cos_tma)
+  int cos_bound;                // trajectory scans with sem_cos: read only the cosines whose blend bound
+                                // reaches the admission threshold (direct loads, no TMA ring)
   int cos_tiled_exp;            // experiment knob FMOE_COS_TILED_EXP: cosine boxes as contiguous 4 KB blocks
   size_t cos_bytes;
   int cos_tma;                  // semantic scans: out_cos written through a swizzled smem stage + TMA
@@ -273,12 +275,18 @@ struct UmmaParams {
                                 // first ring pass, reused stale afterwards (results garbage; measures
                                 // the L2 traffic of re-reading it per tile)
 };
+constexpr float kCosMax = 1.001f;               // bound on a cached cosine (|cos| <= 1 plus rounding)
 constexpr int kCosStage = 32 * 128;             // per epilogue warp: 32 queries x 32 columns fp32 (SW128)
 constexpr int kCosRingMax = 6;                  // cached-cosine loads: buffers per epilogue warp (ring - 1 chunks ahead)
 // ring depth of the cached-cosine loads (FMOE_COS_RING, 2..6; measurement knob)
 static int cos_ring() {
   static const int r = getenv("FMOE_COS_RING") ? atoi(getenv("FMOE_COS_RING")) : 3;
   return r < 2 ? 2 : (r > kCosRingMax ? kCosRingMax : r);
+}
+// bounded cached-cosine reads for blends / RDY scans with sem_cos (FMOE_COS_BOUND=0: every cosine, measurement knob)
+bool umma_cos_bound() {
+  static const bool on = !(getenv("FMOE_COS_BOUND") && atoi(getenv("FMOE_COS_BOUND")) == 0);
+  return on;
 }
 static int cos_stage_bytes(bool sem) { return kUmEpiWarps * kCosStage * (sem ? 1 : cos_ring()); }
 
@@ -787,7 +795,7 @@ __global__ void __launch_bounds__(kUmThreads, 1)
             cached[4 * j4] = f.x; cached[4 * j4 + 1] = f.y; cached[4 * j4 + 2] = f.z; cached[4 * j4 + 3] = f.w;
           }
           ++ci;
-        } else if (!SEM && p.sem_cos) {
+        } else if (!SEM && p.sem_cos && !p.cos_bound) {
           const float* cp = p.sem_cos + int64_t(p.cand_q0 + qg) * p.cos_stride + yc;
 #pragma unroll
           for (int j = 0; j < 32; j += 4) {
@@ -803,6 +811,42 @@ __global__ void __launch_bounds__(kUmThreads, 1)
         const float4* res = reinterpret_cast<const float4*>(&escale[as][half][0][(sub * NC + c) * 32]);
         const float4* rms = reinterpret_cast<const float4*>(&escale[as][half][1][(sub * NC + c) * 32]);
         tc_wait_ld();
+        // Bounded cached-cosine reads (cos_bound): cos <= 1, so a row's blend
+        // is at most fmaf(w1, traj, w * kCosMax) (fmaf is monotone in its
+        // addend; kCosMax covers the semantic scan's rounding).  Only the
+        // columns whose bound reaches the thread's admission threshold can
+        // enter the top-k, and only their cosines are read: after the first
+        // tiles almost none, so the scan streams the map prefix instead of
+        // B x 4 bytes of cosines per row.  Scores of the read columns are
+        // computed exactly as on the unbounded path.
+        unsigned need = 0u;
+        if (!SEM && p.sem_cos && p.cos_bound) {
+          const int nv = nvalid_rows(yc, p.n_rows, live);
+          const float wc = w * kCosMax;
+#pragma unroll
+          for (int j4 = 0; j4 < 8; ++j4) {
+            const float4 rm4 = rms[j4];
+            const float rma[4] = {rm4.x, rm4.y, rm4.z, rm4.w};
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+              const int j = 4 * j4 + u;
+              const float b = fmaf(w1, __uint_as_float(vt[j]) * rqt * rma[u], wc);
+              need |= (b >= thr_s ? 1u : 0u) << j;
+            }
+          }
+          need &= nv >= 32 ? 0xffffffffu : ((1u << nv) - 1u);
+          const float* cp = p.sem_cos + int64_t(p.cand_q0 + qg) * p.cos_stride + yc;
+          if (need == 0xffffffffu && vec4) {
+#pragma unroll
+            for (int j = 0; j < 32; j += 4) {
+              const float4 f = __ldcs(reinterpret_cast<const float4*>(cp + j));
+              cached[j] = f.x; cached[j + 1] = f.y; cached[j + 2] = f.z; cached[j + 3] = f.w;
+            }
+          } else {
+#pragma unroll
+            for (int j = 0; j < 32; ++j) cached[j] = ((need >> j) & 1u) ? __ldcs(cp + j) : 0.f;
+          }
+        }
         EPI_T(2);
         // fast path: 32 scores and their maximum, one compare against the k-th score
         float sc[32];
@@ -823,6 +867,7 @@ __global__ void __launch_bounds__(kUmThreads, 1)
             }
             if (TRAJ) v = SEM || p.sem_cos ? fmaf(w1, __uint_as_float(vt[j]) * rqt * rma[u], v)
                                            : __uint_as_float(vt[j]) * ct * rma[u];
+            if (!SEM && p.sem_cos && p.cos_bound && !((need >> j) & 1u)) v = -__int_as_float(0x7f800000);
             sc[j] = v;
             vmax = fmaxf(vmax, v);
           }
@@ -1332,6 +1377,7 @@ cudaError_t launch_umma(const UmmaLaunch& L, cudaStream_t s) {
   }
   p.cos_tma = cos_tma ? 1 : 0;
   p.cos_ring = cos_ring();
+  p.cos_bound = !sem && traj && L.sem_cos != nullptr && !cos_tma && umma_cos_bound();
   {
     static const int ct_env = getenv("FMOE_COS_TILED_EXP") ? atoi(getenv("FMOE_COS_TILED_EXP")) : 0;
     p.cos_tiled_exp = cos_tma ? ct_env : 0;

@@ -651,7 +651,8 @@ fmoe_status run_search(const fmoe_store* st, int64_t B, const float* dq, const f
   }
   if (umma_plan(st, B, k, ell, w, n_rows, id_offset, &in)) {
     in.cos_out = cos.out != nullptr && w == 1.f;
-    in.cos_in = cos.in != nullptr && w != 1.f;
+    // the bounded reads of the cached cosines need no TMA ring (umma_cos_bound)
+    in.cos_in = cos.in != nullptr && w != 1.f && !umma_cos_bound();
     if (in.cos_out && !umma_supported(in)) in.cos_out = 0;   // no room for the staging: direct stores
     if (in.cos_in && !umma_supported(in)) in.cos_in = 0;     // no room for the ring: direct loads
     if (out_stride && k_out > k) *out_stride = k_out;
