@@ -256,7 +256,7 @@ struct UmmaParams {
                         // query, so all four TMEM lane quadrants (= SM sub-partitions) carry
                         // live queries when nq <= 64; each replica scores 1/R of the columns
   unsigned long long* trace;
-  float* out_cos;               // semantic kernels: cosines [B][cos_stride] (optional)
+  float* out_cos;               // semantic kernels: cosines [B][cos_stride] (optional; this pass's first row)
   const float* sem_cos;         // trajectory kernels: cached semantic cosines to blend (optional)
   int64_t cos_stride;
   unsigned long long* gthr;     // [nq] shared admission threshold per query (zeroed by prep)
@@ -796,7 +796,7 @@ __global__ void __launch_bounds__(kUmThreads, 1)
           }
           ++ci;
         } else if (!SEM && p.sem_cos && !p.cos_bound) {
-          const float* cp = p.sem_cos + int64_t(p.cand_q0 + qg) * p.cos_stride + yc;
+          const float* cp = p.sem_cos + int64_t(qg) * p.cos_stride + yc;
 #pragma unroll
           for (int j = 0; j < 32; j += 4) {
             if (vec4 && j + 4 <= nvalid_rows(yc, p.n_rows, live)) {
@@ -835,7 +835,9 @@ __global__ void __launch_bounds__(kUmThreads, 1)
             }
           }
           need &= nv >= 32 ? 0xffffffffu : ((1u << nv) - 1u);
-          const float* cp = p.sem_cos + int64_t(p.cand_q0 + qg) * p.cos_stride + yc;
+          // no column of this chunk can reach any lane's list: nothing to read or score
+          if (!__any_sync(0xffffffffu, need != 0u)) continue;
+          const float* cp = p.sem_cos + int64_t(qg) * p.cos_stride + yc;
           if (need == 0xffffffffu && vec4) {
 #pragma unroll
             for (int j = 0; j < 32; j += 4) {
@@ -909,7 +911,7 @@ __global__ void __launch_bounds__(kUmThreads, 1)
             }
           }
         } else if (SEM && !TRAJ && p.out_cos && live) {
-          float* op = p.out_cos + int64_t(p.cand_q0 + qg) * p.cos_stride + yc;
+          float* op = p.out_cos + int64_t(qg) * p.cos_stride + yc;
           const int nv = nvalid_rows(yc, p.n_rows, live);
 #pragma unroll
           for (int j = 0; j < 32; j += 4) {
@@ -1203,9 +1205,13 @@ static int umma_tn(const UmmaPlanIn& in, int cg) {
 }
 static int stages_for(const UmmaPlanIn& in, int R, int tn = UM_N) {
   const size_t l = lists_bytes(in, R);
-  if (l + 1024 > 216 * 1024) return 0;
+  // dynamic smem budget (FMOE_UMMA_SMEM_KB, measurement knob; the static
+  // shared memory is <= 9 KB, the per-block limit 227 KB)
+  static const int kb_env = getenv("FMOE_UMMA_SMEM_KB") ? atoi(getenv("FMOE_UMMA_SMEM_KB")) : 216;
+  const size_t budget = size_t(kb_env < 64 ? 64 : (kb_env > 218 ? 218 : kb_env)) * 1024;
+  if (l + 1024 > budget) return 0;
   const int cg = cg_of(in);
-  const int S = int((216 * 1024 - 1024 - l) / size_t(um_stage_bytes(cg, tn)));
+  const int S = int((budget - 1024 - l) / size_t(um_stage_bytes(cg, tn)));
   static const int env = getenv("FMOE_UMMA_STAGES") ? atoi(getenv("FMOE_UMMA_STAGES")) : 0;
   const int cap = env > 0 ? env : (tn == 512 ? 4 : tn == UM_N ? (cg == 2 ? 6 : 4) : kUmMaxStages);
   return S > cap ? cap : S;

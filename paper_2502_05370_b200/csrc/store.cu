@@ -427,6 +427,9 @@ fmoe_status run_search_umma(const fmoe_store* st, UmmaPlanIn in, int64_t B, cons
 // by gated GEMV passes (none in practice) whose results are scattered back.
 constexpr int kApproxMaxK = 48;
 int approx_list_len(int k) {
+  // candidates kept per query for the exact re-rank (FMOE_APPROX_EXTRA: k + extra, measurement knob)
+  static const int extra = getenv("FMOE_APPROX_EXTRA") ? atoi(getenv("FMOE_APPROX_EXTRA")) : -1;
+  if (extra >= 1) return k + extra < kMaxK ? k + extra : kMaxK;
   const int a = k + 8 > 2 * k ? k + 8 : 2 * k;
   return a < kMaxK ? a : kMaxK;
 }
@@ -646,7 +649,9 @@ fmoe_status run_search(const fmoe_store* st, int64_t B, const float* dq, const f
   if (!no_approx && w == 1.f && !cos.in && !seed_ids && !gate && k <= kApproxMaxK &&
       umma_plan(st, B, approx_list_len(k), 0, 1.f, n_rows, id_offset, &in)) {
     in.approx = 1;
-    in.cos_out = cos.out != nullptr;
+    // FMOE_COS_DIRECT=1: the cosine side output by direct stores (no smem staging; measurement knob)
+    static const bool cos_direct = getenv("FMOE_COS_DIRECT") != nullptr && atoi(getenv("FMOE_COS_DIRECT")) != 0;
+    in.cos_out = cos.out != nullptr && !cos_direct;
     if (umma_supported(in)) return run_search_umma_approx(st, in, B, dq, s, ds, di, dkeys, cos, k);
   }
   if (umma_plan(st, B, k, ell, w, n_rows, id_offset, &in)) {
