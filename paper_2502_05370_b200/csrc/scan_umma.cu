@@ -283,9 +283,14 @@ static int cos_ring() {
   static const int r = getenv("FMOE_COS_RING") ? atoi(getenv("FMOE_COS_RING")) : 3;
   return r < 2 ? 2 : (r > kCosRingMax ? kCosRingMax : r);
 }
-// bounded cached-cosine reads for blends / RDY scans with sem_cos (FMOE_COS_BOUND=0: every cosine, measurement knob)
+// bounded cached-cosine reads for blends / RDY scans with sem_cos (opt-in,
+// FMOE_COS_BOUND=1).  Measured slower on the synthetic C5 workload (2M shard,
+// B = 256, ell = 31: 1070 vs 955 us, profiles/r02i_cos_bound.md): the
+// softmax gate maps give many rows trajectory cosines close to the admission
+// threshold, so most chunks still need their cosines, now through per-lane
+// loads instead of the TMA ring.  Kept for stores whose trajectories separate.
 bool umma_cos_bound() {
-  static const bool on = !(getenv("FMOE_COS_BOUND") && atoi(getenv("FMOE_COS_BOUND")) == 0);
+  static const bool on = getenv("FMOE_COS_BOUND") && atoi(getenv("FMOE_COS_BOUND")) == 1;
   return on;
 }
 static int cos_stage_bytes(bool sem) { return kUmEpiWarps * kCosStage * (sem ? 1 : cos_ring()); }
