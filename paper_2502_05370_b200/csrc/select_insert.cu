@@ -255,7 +255,6 @@ __global__ void __launch_bounds__(32) resolve_kernel(int nrep, int kk, const uin
                                                      const int* gate, int mark_append) {
   pdl_wait();
   if (gate && *gate == 0) return;
-  __shared__ int64_t claimed[kMaxK];
   __shared__ uint64_t ks[kMaxK * kMaxK];   // the candidate lists, staged once (independent, coalesced loads)
   const int lane = threadIdx.x;
   bool need = false;
@@ -266,34 +265,35 @@ __global__ void __launch_bounds__(32) resolve_kernel(int nrep, int kk, const uin
     if (out_slot) out_slot[x] = int64_t(id_offset) + first_append_slot + x;
     if (out_replaced) out_replaced[x] = -1;
   }
+  // the victims claimed so far live in registers: row i's in lane i % 32,
+  // slot i / 32 (nrep <= 64); a candidate is checked against all of them by
+  // one vote.  Row j walks its list in order (best first) and takes the first
+  // candidate no earlier row claimed -- usually the first, so a row costs a
+  // few votes instead of a j-long scan per lane.
+  int64_t cl0 = -3, cl1 = -3;
   for (int j = 0; j < nrep; ++j) {
     int64_t best = -1;
-    for (int c0 = 0; c0 < kk; c0 += 32) {
-      const int c = c0 + lane;
-      int64_t loc = -1;
-      if (c < kk) {
-        const uint64_t key = ks[j * kk + c];
-        if (key != 0ull) {
-          loc = key_id(key);
-          for (int i = 0; i < j; ++i)
-            if (claimed[i] == loc) { loc = -1; break; }
-        }
-      }
-      const unsigned m = __ballot_sync(0xffffffffu, loc >= 0);
-      if (m) {
-        best = __shfl_sync(0xffffffffu, loc, __ffs(m) - 1);
+    for (int c = 0; c < kk; ++c) {
+      const uint64_t key = ks[j * kk + c];
+      if (key == 0ull) continue;
+      const int64_t loc = key_id(key);
+      if (!__any_sync(0xffffffffu, cl0 == loc || cl1 == loc)) {
+        best = loc;
         break;
       }
     }
     // exhausted while the list was full: the victim may lie beyond the kk keys
     if (best < 0 && k_full > kk && ks[j * kk + kk - 1] != 0ull) need = true;
+    const int64_t claim = best >= 0 ? best : -2;
+    if (lane == (j & 31)) {
+      if (j < 32) cl0 = claim;
+      else cl1 = claim;
+    }
     if (lane == 0) {
-      claimed[j] = best >= 0 ? best : -2;
       slots_all[x0 + j] = best;
       if (out_slot) out_slot[x0 + j] = best >= 0 ? int64_t(id_offset) + best : -1;
       if (out_replaced) out_replaced[x0 + j] = best >= 0 ? int64_t(id_offset) + best : -1;
     }
-    __syncwarp();
   }
   if (need_full && lane == 0) *need_full = need ? 1 : 0;
 }
@@ -331,30 +331,25 @@ cudaError_t launch_excl(uint32_t* excl, const int64_t* slots, int n, int64_t off
 __global__ void __launch_bounds__(32) resolve_ids_kernel(int B, int k, const int64_t* __restrict__ ids,
                                                          int64_t* out_victim) {
   pdl_wait();
-  __shared__ int64_t claimed[kMaxK];
   const int lane = threadIdx.x;
+  // claims in registers (row i in lane i % 32, slot i / 32; B <= 64), one vote per candidate (as resolve_kernel)
+  int64_t cl0 = -3, cl1 = -3;
   for (int j = 0; j < B; ++j) {
     int64_t best = -1;
-    for (int c0 = 0; c0 < k; c0 += 32) {
-      const int c = c0 + lane;
-      int64_t id = -1;
-      if (c < k) {
-        id = ids[int64_t(j) * k + c];
-        if (id >= 0)
-          for (int i = 0; i < j; ++i)
-            if (claimed[i] == id) { id = -1; break; }
-      }
-      const unsigned m = __ballot_sync(0xffffffffu, id >= 0);
-      if (m) {
-        best = __shfl_sync(0xffffffffu, id, __ffs(m) - 1);
+    for (int c = 0; c < k; ++c) {
+      const int64_t id = ids[int64_t(j) * k + c];
+      if (id < 0) continue;
+      if (!__any_sync(0xffffffffu, cl0 == id || cl1 == id)) {
+        best = id;
         break;
       }
     }
-    if (lane == 0) {
-      claimed[j] = best >= 0 ? best : -2;
-      out_victim[j] = best;
+    const int64_t claim = best >= 0 ? best : -2;
+    if (lane == (j & 31)) {
+      if (j < 32) cl0 = claim;
+      else cl1 = claim;
     }
-    __syncwarp();
+    if (lane == 0) out_victim[j] = best;
   }
 }
 
