@@ -1101,22 +1101,38 @@ __global__ void __launch_bounds__(256) umma_prep_kernel(const float* __restrict_
     if (live && q == x && !keep_gthr) gthr[q] = 0ull;   // keep: seeded by a sample pass
     red[0][0] = sb > 0.0 ? 1.0 / sqrt(sb) : 0.0;
   }
-  if (!(sd.ids && traj && !sem && live && q == x && sd.k > 0 && sd.n >= sd.k && sd.n <= 64)) return;
+  // (no seed bound -- an unseeded scan -- when the prefix does not fit the staging below)
+  if (!(sd.ids && traj && !sem && live && q == x && sd.k > 0 && sd.n >= sd.k && sd.n <= 64 && ell * Ep <= kMaxE * 64))
+    return;
   // ---- seed bound: the k-th best trajectory score of the valid seed rows
-  // (ids -1, e.g. from a short candidate union, are skipped), less a margin
+  // (ids -1, e.g. from a short candidate union, are skipped), less a margin.
+  // The query prefix (store-dtype values, pad columns 0) is staged in shared
+  // memory; a seed's dot is spread over the warp as 16-byte chunks of its
+  // layer rows (Ep*2 bytes each, 16-byte multiples), all loads independent.
   __shared__ unsigned s_sc[64];
+  __shared__ __align__(16) float s_q[kMaxE * 64];      // [ell][Ep], ell * Ep <= 64 * 64
+  for (int i = tid; i < ell * Ep; i += 256) {
+    const int l = i / Ep, j = i - l * Ep;
+    s_q[i] = j < E ? __bfloat162float(__float2bfloat16_rn(q_prefix[int64_t(x) * q_stride + l * E + j])) : 0.f;
+  }
   __syncthreads();
   const float rq = float(red[0][0]);
+  const int cpr = Ep / 8;                                // 16-byte chunks per layer row
+  const int nch = ell * cpr;
   for (int i = warp; i < sd.n; i += 8) {
     const int64_t gid = sd.ids[int64_t(x) * sd.stride + i];
     const int64_t y = gid - int64_t(sd.id_offset);
     const bool ok = gid >= 0 && y >= 0 && y < sd.n_rows;
     float dot = 0.f;
     if (ok)
-      for (int t = lane; t < ell * E; t += 32) {
-        const int l = t / E, j = t - l * E;
-        const float qv = __bfloat162float(__float2bfloat16_rn(q_prefix[int64_t(x) * q_stride + t]));
-        dot = fmaf(qv, __bfloat162float(sd.maps[(int64_t(l) * sd.cap + y) * Ep + j]), dot);
+      for (int c = lane; c < nch; c += 32) {
+        const int l = c / cpr, j0 = (c - l * cpr) * 8;
+        const uint4 u = __ldg(reinterpret_cast<const uint4*>(sd.maps + (int64_t(l) * sd.cap + y) * Ep + j0));
+        float m8[8];
+        unpack8(u, m8, Bf16Tag());
+        const float* qv = s_q + l * Ep + j0;
+#pragma unroll
+        for (int e = 0; e < 8; ++e) dot = fmaf(qv[e], m8[e], dot);
       }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) dot += __shfl_xor_sync(0xffffffffu, dot, o);
