@@ -67,11 +67,12 @@ __global__ void __launch_bounds__(kMergeWarps * 32) merge_keys_kernel(int n_list
   }
 }
 
-// Small merges (n_lists * k_in <= 2048 keys per query, e.g. the per-CTA lists
-// of a tcgen05 scan): one block per query sorts the padded keys descending in
-// shared memory (bitonic network, 256 threads) and writes the first k -- a
-// fixed ~66 barrier steps instead of the warp lists' chain of dependent
-// inserts (17 us per 64-query merge of 148 x 8 keys into 32).  Keys are
+// Alternative merge for n_lists * k_in <= 2048 keys per query (opt-in,
+// FMOE_MERGE_SORT=1): one block per query sorts the padded keys descending in
+// shared memory (bitonic network, 256 threads) and writes the first k.
+// Measured slower than the warp lists below: 32 vs 17 us per 64-query merge
+// of 148 x 8 keys into 32 (C3 session step, profiles/r02n_merge_sort.md) --
+// the 66 block barriers cost more than the warps' dependent inserts.  Keys are
 // unique (a row lives in one list) and empty slots are key 0, so the order is
 // the (score desc, id asc) order of the warp lists.
 constexpr int kSortMax = 2048;
@@ -109,8 +110,8 @@ cudaError_t launch_merge_keys(int B, int n_lists, int k_in, const uint64_t* keys
                               const int* gate) {
   if (B <= 0) return cudaSuccess;
   const int64_t total = int64_t(n_lists) * k_in;
-  static const bool no_sort = getenv("FMOE_MERGE_SORT") && atoi(getenv("FMOE_MERGE_SORT")) == 0;   // knob
-  if (total >= 1 && total <= kSortMax && !no_sort) {
+  static const bool sort = getenv("FMOE_MERGE_SORT") && atoi(getenv("FMOE_MERGE_SORT")) == 1;   // knob
+  if (total >= 1 && total <= kSortMax && sort) {
     int n2 = 64;
     while (n2 < total) n2 <<= 1;
     count_launch();
