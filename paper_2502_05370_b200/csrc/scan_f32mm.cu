@@ -37,8 +37,9 @@
 namespace fmoe {
 
 #ifndef FMOE_F32MM_UNROLL
-#define FMOE_F32MM_UNROLL 2   // k-steps of the FFMA loop unrolled (code size vs. scheduling freedom)
+#define FMOE_F32MM_UNROLL 2
 #endif
+constexpr int kMmUnroll = FMOE_F32MM_UNROLL;   // k-steps of the FFMA loop unrolled (code size vs. scheduling)
 constexpr int kMmThreads = 256;
 constexpr int kMmWarps = kMmThreads / 32;
 constexpr int kMmQ = 64;            // queries per pass (8 per warp query group)
@@ -85,7 +86,7 @@ __device__ __forceinline__ void mm_chunk(const unsigned char* rows, const unsign
                                          float (&acc)[8][TR]) {
   const unsigned char* rb = rows + (wr * 32 * TR + lane) * 128;
   const unsigned char* qb = qs + wq * 8 * 128;
-#pragma unroll FMOE_F32MM_UNROLL
+#pragma unroll kMmUnroll
   for (int kk = 0; kk < 8; ++kk) {
     const int sw = (kk ^ (lane & 7)) * 16;
     float4 x[TR];
