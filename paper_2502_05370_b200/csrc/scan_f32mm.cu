@@ -31,6 +31,8 @@
 // shared memory (ballot the keys beating the list's k-th, insert warp-
 // cooperatively); lists go to cand[q][CTA*(8/WQ) + wr][k] and the merge
 // kernel finishes.
+#include <cstdlib>
+
 #include "common.cuh"
 #include "kernels.cuh"
 
@@ -106,8 +108,8 @@ __device__ __forceinline__ void mm_chunk(const unsigned char* rows, const unsign
   }
 }
 
-template <int TR, bool SEM, bool TRAJ>
-__global__ void __launch_bounds__(kMmThreads, 1) scan_f32mm_kernel(const F32mmArgs a) {
+template <int TR, bool SEM, bool TRAJ, int MINB = 1>
+__global__ void __launch_bounds__(kMmThreads, MINB) scan_f32mm_kernel(const F32mmArgs a) {
   extern __shared__ __align__(128) unsigned char smem[];
   const StoreView& st = a.st;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -290,9 +292,22 @@ __global__ void __launch_bounds__(256) f32mm_prep_kernel(const F32mmPrep p) {
 
 int f32mm_wq(int nq) { return nq <= 8 ? 1 : nq <= 16 ? 2 : nq <= 32 ? 4 : 8; }
 
+// Two CTAs per SM for single-part passes of > 32 queries: thread tiles of
+// 8 queries x 4 rows, <= 128 registers, 128-row tiles, twice the warps per SM
+// to hide the shared-memory and FMA latencies.  Measured (Qwen shape, N = 1M,
+// B = 64, profiles/r02p_f32mm_2cta.md): semantic 8.40 -> 8.12 ms, trajectory
+// ell = 16 5.29 -> 4.37 ms; a blend (two accumulator sets -> 8 x 2 tiles) got
+// slower (13.4 -> 15.3 ms) and keeps one CTA per SM.  FMOE_F32MM_2CTA=0: off.
+static bool f32mm_2cta(int wq, bool blend) {
+  static const bool off = getenv("FMOE_F32MM_2CTA") && atoi(getenv("FMOE_F32MM_2CTA")) == 0;
+  return !off && wq == 8 && !blend;
+}
 // thread tile rows: TR = WQ (RT = 256 rows per tile); a blend keeps two
 // accumulator sets, so TR <= 4 there (RT = 128 at WQ = 8)
-static int f32mm_tr(int wq, bool blend) { return blend && wq > 4 ? 4 : wq; }
+static int f32mm_tr(int wq, bool blend) {
+  if (f32mm_2cta(wq, blend)) return 4;
+  return blend && wq > 4 ? 4 : wq;
+}
 
 static size_t f32mm_smem(int wq, int k, bool blend) {
   const int rt = (kMmWarps / wq) * 32 * f32mm_tr(wq, blend);
@@ -309,7 +324,8 @@ int f32mm_grid(int64_t n_rows, int nq, bool blend) {
   const int wq = f32mm_wq(nq);
   const int rt = (kMmWarps / wq) * 32 * f32mm_tr(wq, blend);
   const int64_t tiles = (n_rows + rt - 1) / rt;
-  return int(tiles < sms ? (tiles < 1 ? 1 : tiles) : sms);
+  const int units = f32mm_2cta(wq, blend) ? 2 * sms : sms;
+  return int(tiles < units ? (tiles < 1 ? 1 : tiles) : units);
 }
 
 int f32mm_lists_per_cta(int nq) { return kMmWarps / f32mm_wq(nq); }
@@ -319,11 +335,15 @@ cudaError_t launch_f32mm_prep(const F32mmPrep& p, int nq, cudaStream_t s) {
   return launch_pdl(f32mm_prep_kernel, dim3(unsigned(nq)), dim3(256), 0, s, p);
 }
 
-template <int TR>
+template <int TR, int MINB = 1>
 static cudaError_t launch_tr(const F32mmArgs& a, bool sem, bool traj, size_t smem, int grid, cudaStream_t s) {
   using Fn = void (*)(const F32mmArgs);
-  Fn fn = sem && traj ? scan_f32mm_kernel<(TR > 4 ? 4 : TR), true, true>
-                      : sem ? scan_f32mm_kernel<TR, true, false> : scan_f32mm_kernel<TR, false, true>;
+  Fn fn = nullptr;
+  if constexpr (MINB == 1)   // (two-CTA launches are single-part: no blend variant)
+    fn = sem && traj ? scan_f32mm_kernel<(TR > 4 ? 4 : TR), true, true, 1>
+                     : sem ? scan_f32mm_kernel<TR, true, false, 1> : scan_f32mm_kernel<TR, false, true, 1>;
+  else
+    fn = sem ? scan_f32mm_kernel<TR, true, false, MINB> : scan_f32mm_kernel<TR, false, true, MINB>;
   cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
   if (e != cudaSuccess) return e;
   count_launch();
@@ -338,6 +358,7 @@ cudaError_t launch_f32mm(const F32mmArgs& a, cudaStream_t s) {
     return cudaErrorInvalidValue;
   const size_t smem = f32mm_smem(a.wq, a.k, blend);
   const int grid = a.grid;
+  if (f32mm_2cta(a.wq, blend)) return launch_tr<4, 2>(a, sem, traj, smem, grid, s);
   switch (f32mm_tr(a.wq, blend)) {
     case 1: return launch_tr<1>(a, sem, traj, smem, grid, s);
     case 2: return launch_tr<2>(a, sem, traj, smem, grid, s);
